@@ -23,7 +23,7 @@ IEEE fp32 ops so the device twin matches bitwise):
 
     normal : x
     peaky  : q*4                                                    (sharp attention)
-    drift  : q[...,0] += 2 ;  k[t,...,0] += t*(32/S)                (running max rises every chunk)
+    drift  : q[...,0] += 2 ;  k[t,...,0] += t*(8/S)                 (running max rises every chunk)
     sink   : q += 0.5 ;  k[0] = 2 (all dims)                         (attention sink on token 0)
     same   : k[t] = base(K, token 0)                                (identical keys: closed form)
     class  : k[t] = base(K, token c(t)), c(t) = mix32(t^0xC1A55) % 3 for t < S/2, % 4 for t >= S/2;
@@ -109,7 +109,7 @@ def generate(name: str, dist: str, seed: int, tokens: np.ndarray, n_heads: int, 
         if name == "q":
             x[..., 0] = x[..., 0] + np.float32(2.0)
         elif name == "k":
-            step = np.float32(32.0 / seq_len)
+            step = np.float32(8.0 / seq_len)
             x[..., 0] = x[..., 0] + (tokens.astype(np.float32) * step).reshape(-1, 1)
     elif dist == "sink":
         if name == "q":

@@ -83,7 +83,7 @@ int fpdt_gen_fill(void* out, int out_dtype, int tensor, int dist, uint32_t seed,
                   int64_t chunk_size, cudaStream_t stream) {
   uint32_t a = host_mix32(seed * 0x9E3779B9u + (uint32_t)tensor * 0x85EBCA6Bu + 0x632BE5ABu);
   int64_t chunk_local = chunk_size / world_size;
-  float drift_step = (float)(32.0 / (double)seq_len);
+  float drift_step = (float)(8.0 / (double)seq_len);
   int threads = 256, blocks = 148 * 16;
   if (out_dtype == 0)
     gen_kernel<__nv_bfloat16><<<blocks, threads, 0, stream>>>((__nv_bfloat16*)out, tensor, dist, a,

@@ -1,0 +1,145 @@
+/* fpdt.h — C ABI of libfpdt: the hot path of the Fully Pipelined Distributed Transformer
+ * (FPDT, arXiv 2408.16978) on NVIDIA B200 (sm_100a).
+ *
+ * The library computes sequence-chunked, sequence-parallel (Ulysses) causal attention, forward and
+ * backward, exactly as the paper's FPDT attention block does (§4.1-4.2):
+ *   - every rank holds its local sequence shard [s_local, heads, head_dim] (b = 1 as in
+ *     every experiment of the paper), in the rank-ordinal ("shuffled") token order of
+ *     fig:seq_shuffle: local row t of rank r is global token
+ *         ((t / c) * p + r) * c + (t % c),   c = chunk_size / world_size   (fpdt_global_token);
+ *   - the shard is cut into u = s_local / c chunks T_i; per chunk an all-to-all scatters heads
+ *     and gathers the sequence so each rank attends a contiguous chunk of
+ *     C = chunk_size global tokens with H/p heads;
+ *   - query chunk m attends the resident key/value chunk m (causal), then the earlier
+ *     chunks i < m fetched one by one from pinned host memory, merging partial outputs with the
+ *     online-softmax (log-sum-exp) policy (fig:pipele_case2);
+ *   - q, k, v chunks are offloaded to host memory after use;
+ *   - backward: outer loop over key/value chunks j, inner loop over query chunks i >= j, with the
+ *     dq partials accumulated in host memory and dk_j, dv_j final after outer iteration j (P:L365,
+ *     fig:bw_db); final gradients return to their owner ranks by the reverse all-to-all;
+ *   - copies, all-to-all and compute run on separate CUDA streams with double-buffered device slots
+ *     (§4.2 "Double buffering").
+ *
+ * Conventions for every call below
+ *   - Tensor pointers are DEVICE pointers unless a name says host; tensors are contiguous row-major
+ *     [s_local][heads][head_dim] (head_dim fastest), 16-byte aligned.  The caller owns them.
+ *   - dtype FPDT_BF16: bf16 tensors, fp32 accumulation and softmax, tcgen05 tensor-core kernels.
+ *     dtype FPDT_FP32: fp32 tensors and true-fp32 SIMT kernels (validation mode).
+ *   - softmax_scale <= 0 selects 1/sqrt(head_dim) (the paper never states the scale; R1).
+ *   - causal must be 1 (the paper's causal LLM setting; 0 returns FPDT_ERR_UNSUPPORTED).
+ *   - All calls that take a context are collective over the sequence-parallel group (SPMD): every
+ *     rank must make the same calls with the same shape arguments, in the same order.  A mismatch
+ *     hangs NCCL; it is documented, not detected.
+ *   - Calls are stream-ordered after `stream` (a cudaStream_t; NULL = legacy default stream) and
+ *     return once the work is enqueued (no host synchronisation on the hot path).  Work that the
+ *     caller enqueues on `stream` afterwards sees the results.
+ *   - Return value: FPDT_OK (0) or one of fpdt_status; fpdt_last_error() gives a message.
+ *     Asynchronous CUDA/NCCL faults surface as FPDT_ERR_CUDA / FPDT_ERR_NCCL on a later call.
+ */
+#ifndef FPDT_H_
+#define FPDT_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct fpdt_ctx fpdt_ctx;
+
+enum fpdt_status {
+  FPDT_OK = 0,
+  FPDT_ERR_ARG = 1,           /* null pointer, non-positive size, world_size/rank mismatch */
+  FPDT_ERR_DIVISIBILITY = 2,  /* S % C, C % p, Hq % p, Hkv % p, Hq % Hkv, (C/p... tile) rules, see below */
+  FPDT_ERR_UNSUPPORTED = 3,   /* head_dim not in {64, 80, 128}, causal == 0, unsupported dtype */
+  FPDT_ERR_HOST_OOM = 4,      /* the pinned host chunk store cannot be allocated / is too small */
+  FPDT_ERR_DEVICE_OOM = 5,    /* device working-set allocation failed */
+  FPDT_ERR_STATE = 6,         /* backward without a matching forward on this context */
+  FPDT_ERR_CUDA = 7,
+  FPDT_ERR_NCCL = 8
+};
+
+enum fpdt_dtype { FPDT_BF16 = 0, FPDT_FP32 = 1 };
+
+/* Rank 0 creates the NCCL unique id (128 bytes) for world_size > 1; the caller broadcasts it to the
+ * other ranks (e.g. with torch.distributed).  Not needed when world_size == 1. */
+int fpdt_get_unique_id(unsigned char id[128]);
+
+/* Create a context on CUDA device `device` for rank `rank` of a group of `world_size` ranks.
+ * nccl_id: the 128-byte id from fpdt_get_unique_id (ignored, may be NULL, when world_size == 1).
+ * host_arena_bytes: pinned host chunk store to reserve now; 0 = allocate on the first offloaded
+ * forward (sized for that call).  The context owns the NCCL communicator, its streams and events,
+ * the pinned host store, the device slots and the saved state of ONE attention layer.
+ * Returns FPDT_ERR_HOST_OOM if the store cannot be pinned, FPDT_ERR_NCCL if communicator set-up fails. */
+int fpdt_ctx_create(int world_size, int rank, const unsigned char* nccl_id, int device, size_t host_arena_bytes,
+                    fpdt_ctx** out);
+
+/* Release everything the context owns (synchronises the context's streams first). */
+int fpdt_ctx_destroy(fpdt_ctx* ctx);
+
+/* Forward.
+ *   q [s_local, n_q_heads, head_dim], k, v [s_local, n_kv_heads, head_dim]  (inputs, rank-ordinal order)
+ *   o [s_local, n_q_heads, head_dim]                                      (output, same dtype)
+ *   lse [s_local, n_q_heads] fp32, natural log of the softmax denominator (output; may be NULL)
+ *   chunk_size C: global tokens per chunk (the paper's "chunk size"); the global
+ *     sequence S = s_local * world_size must satisfy S % C == 0, C % world_size == 0 and
+ *     (C / world_size) * world_size == C with C a multiple of 256.
+ *   n_q_heads % world_size == 0, n_kv_heads % world_size == 0, n_q_heads % n_kv_heads == 0 (GQA).
+ *   offload 1: q, k, v chunks go to the pinned host store and earlier key/value chunks are fetched
+ *     back double-buffered (the paper's FPDT with offloading).  offload 0: chunks stay in device
+ *     memory ("FPDT chunking only"); with world_size == 1 the caller's q, k, v are used in
+ *     place and must stay valid and unmodified until fpdt_attn_bwd.
+ * Saves, for the backward, the per-row log-sum-exp and (offload 1) the chunk store. */
+int fpdt_attn_fwd(fpdt_ctx* ctx, const void* q, const void* k, const void* v, void* o, float* lse, int64_t s_local,
+                  int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
+                  int dtype, int offload, float softmax_scale, void* stream);
+
+/* Backward of the last fpdt_attn_fwd on this context, for upstream gradient dout.
+ *   o, dout [s_local, n_q_heads, head_dim] (inputs: the forward output and dL/dO)
+ *   dq [s_local, n_q_heads, head_dim], dk, dv [s_local, n_kv_heads, head_dim] (outputs, overwritten)
+ * Every shape/flag argument must equal the forward's, else FPDT_ERR_STATE (also if no forward ran). */
+int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void* dk, void* dv, int64_t s_local,
+                  int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
+                  int dtype, int offload, float softmax_scale, void* stream);
+
+/* Message of the last non-OK status returned on this thread ("" if none). */
+const char* fpdt_last_error(void);
+
+/* Global token index of rank `rank`'s local row `local_t` (rank-ordinal layout). */
+int64_t fpdt_global_token(int64_t local_t, int64_t chunk_size, int world_size, int rank);
+
+/* Counters of the context since creation (diagnostics for tests and the bench). */
+typedef struct fpdt_stats {
+  int64_t bytes_h2d;          /* host -> device chunk fetches */
+  int64_t bytes_d2h;          /* device -> host chunk offloads */
+  int64_t bytes_a2a;          /* bytes sent to other ranks by the all-to-alls */
+  int64_t kernel_launches;    /* kernels enqueued by the library (attention + support kernels) */
+  int64_t attn_launches;      /* attention pair kernels only */
+  int64_t fetch_slots_highwater; /* max fetched key/value chunk sets resident at once (<= 2) */
+  int64_t host_arena_bytes;   /* pinned host store reserved */
+  int64_t device_bytes;       /* library-owned device working set */
+} fpdt_stats;
+int fpdt_get_stats(const fpdt_ctx* ctx, fpdt_stats* out);
+
+/* Per-launch timing of the attention pair kernels (for bench.py's roofline): when enabled, the library
+ * records a CUDA event pair around every attention kernel on the stream it is launched on.
+ * fpdt_kernel_time synchronises on those events and returns the summed kernel milliseconds and launch
+ * counts of forward and backward attention kernels since the last reset (reset != 0 clears them). */
+int fpdt_set_kernel_timing(fpdt_ctx* ctx, int enable);
+int fpdt_kernel_time(fpdt_ctx* ctx, double* fwd_ms, int64_t* fwd_launches, double* bwd_ms, int64_t* bwd_launches,
+                     int reset);
+
+/* Diagnostic self-test of the tcgen05/TMA operand formats (one 128-row tile product on one CTA).
+ * variant 0: out[128x128] = A[128xD] B[128xD]^T;  1: out[128xD] = P[128x128] V[128xD] (P in TMEM);
+ * 2: out[128xD] = A[128x128] V[128xD] (A MN-major smem).  a, b: device bf16; A/B tiles are rows
+ * [0,128) of head n_heads-1 of [rows][n_heads][head_dim] tensors; P/A of variants 1-2 are [128][128].
+ * out: device fp32.  Returns 0 or a CUDA error code. */
+int fpdt_selftest_umma(int variant, int head_dim, const void* a, const void* b, int n_heads, int rows, void* out,
+                       void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* FPDT_H_ */

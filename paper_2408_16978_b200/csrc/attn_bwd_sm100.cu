@@ -1,0 +1,371 @@
+// Backward chunk-pair attention for sm_100a (KV-stationary; tcgen05 + TMEM + TMA).
+//
+// One launch = one (key/value chunk j, query chunk i) step of FPDT's nested backward loop
+// (fig:bw_db: "The outer loop is on key and value, while the inner one is on query").
+// A CTA owns one 128-row key/value tile of one KV head and walks the query tiles of the range and the
+// G query heads of its group; per (query tile, head) it computes:
+//   S^T  = K Q^T            P^T  = exp2(S^T*scale*log2e - lse2)       (recompute, no stored P)
+//   dP^T = V dO^T           dS^T = P^T o (dP^T - D)
+//   dV  += P^T dO           dK  += dS^T Q          dQ_partial = dS K  (added to fp32 dq_acc)
+// dK/dV accumulate in TMEM across the whole walk and leave once per launch (accumulated across the
+// inner loop in fp32 HBM; final bf16 at the last inner step).
+//
+// Warps: 0-3 softmax-gradient (thread = key row = TMEM lane), then dQ read-out (thread = query row)
+//        and the final dK/dV write; 4 TMA producer; 5 TMEM allocator + MMA issuer.
+// TMEM: S^T [0,128) -> P^T bf16 [0,64) + dS^T bf16 [64,128);  dP^T [128,256) -> dQ [128,128+D);
+//       dK [256,256+D);  dV [384,384+D).
+// smem: K, V (stationary), QS stages of {Q, dO, lse2[128], D[128]}, dS (MN-major 128B-swizzled, A of dQ).
+#include "attn_tile.cuh"
+#include "kernels.h"
+#include "smem_layout.cuh"
+#include "tma_host.h"
+
+namespace fpdt {
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 192;
+
+template <int D>
+struct BwdCfg {
+  using T = Tile<D>;
+  static constexpr int QS = 2;
+  static constexpr int kKV = 2 * T::kBytes;
+  static constexpr int kStage = 2 * T::kBytes;
+  static constexpr int kDS = 128 * 128 * 2;
+  static constexpr int kStats = 2 * 512;
+  static constexpr int oK = 0, oV = T::kBytes, oStage = kKV, oDS = kKV + QS * kStage, oStats = oDS + kDS;
+  static constexpr int oBars = oStats + QS * kStats;
+  static constexpr int kBars = 16 * 8;
+  static constexpr int kSmem = oBars + kBars + 16;
+};
+
+struct TmapSet {
+  CUtensorMap q_main, q_tail, k_main, k_tail, v_main, v_tail, o_main, o_tail;
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+               : "memory");
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdArgs a) {
+  using T = Tile<D>;
+  using C = BwdCfg<D>;
+  constexpr int QS = C::QS;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  if ((smem_u32(smem) & 1023) != 0) __trap();
+  const uint32_t base = smem_u32(smem);
+  const uint32_t sK = base + C::oK, sV = base + C::oV, sDS = base + C::oDS;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::oBars);
+  // barrier slots
+  const uint32_t b_kv = smem_u32(&bars[0]);
+  auto b_qfull = [&](int s) { return smem_u32(&bars[1 + s]); };
+  auto b_qempty = [&](int s) { return smem_u32(&bars[3 + s]); };
+  const uint32_t b_s = smem_u32(&bars[5]), b_dp = smem_u32(&bars[6]), b_p = smem_u32(&bars[7]),
+                 b_ds = smem_u32(&bars[8]), b_dsfree = smem_u32(&bars[9]), b_dqfull = smem_u32(&bars[10]),
+                 b_dqempty = smem_u32(&bars[11]), b_kvdone = smem_u32(&bars[12]);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::oBars + C::kBars);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int kt = blockIdx.x;
+  const int g = blockIdx.y;
+  const int G = a.G;
+  const int64_t kv_base = a.kv_pos0 + (int64_t)kt * 128;
+  int qt_first = 0;
+  const int n_qt_total = a.n_q_rows / 128;
+  if (a.causal) {
+    const int64_t rel = kv_base - a.q_pos0;  // first query tile that can see this key tile
+    if (rel > 0) qt_first = (int)(rel / 128);
+    if (qt_first > n_qt_total) qt_first = n_qt_total;
+  }
+  const int n_iter = (n_qt_total - qt_first) * G;
+
+  if (warp == 5) tmem_alloc<512>(smem_u32(tmem_slot));
+  if (warp == 4 && lane == 0) {
+    mbar_init(b_kv, 1);
+    for (int s = 0; s < QS; ++s) {
+      mbar_init(b_qfull(s), 1);
+      mbar_init(b_qempty(s), 1);
+    }
+    mbar_init(b_s, 1);
+    mbar_init(b_dp, 1);
+    mbar_init(b_p, 128);
+    mbar_init(b_ds, 128);
+    mbar_init(b_dsfree, 1);
+    mbar_init(b_dqfull, 1);
+    mbar_init(b_dqempty, 128);
+    mbar_init(b_kvdone, 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp == 4) {
+    // ------------------------------------------------------------------ producer
+    if (elect_one() && n_iter > 0) {
+      const uint64_t pol_kv = policy_evict_first(), pol_q = policy_evict_last();
+      mbar_expect_tx(b_kv, 2 * T::kBytes);
+      const int krow = (int)(a.kv_row0 + (int64_t)kt * 128);
+      T::load(sK, &tm.k_main, &tm.k_tail, b_kv, a.k.head0 + g, krow, pol_kv);
+      T::load(sV, &tm.v_main, &tm.v_tail, b_kv, a.v.head0 + g, krow, pol_kv);
+      for (int n = 0; n < n_iter; ++n) {
+        const int s = n % QS;
+        if (n >= QS) mbar_wait(b_qempty(s), ((n / QS) - 1) & 1);
+        const int qt = qt_first + n / G, hh = n % G;
+        const int h = g * G + hh;
+        const uint32_t st = base + C::oStage + s * C::kStage;
+        const uint32_t stats = base + C::oStats + s * C::kStats;
+        const int qrow = (int)(a.q_row0 + (int64_t)qt * 128);
+        mbar_expect_tx(b_qfull(s), 2 * T::kBytes + 1024);
+        T::load(st, &tm.q_main, &tm.q_tail, b_qfull(s), a.q.head0 + h, qrow, pol_q);
+        T::load(st + T::kBytes, &tm.o_main, &tm.o_tail, b_qfull(s), a.dout.head0 + h, qrow, pol_q);
+        bulk_load(stats, a.lse2 + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, b_qfull(s));
+        bulk_load(stats + 512, a.Dstat + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, b_qfull(s));
+      }
+    }
+  } else if (warp == 5) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (elect_one() && n_iter > 0) {
+      const uint32_t idS = idesc_bf16(128, 128, 0, 0);           // S^T, dP^T: A,B K-major
+      const uint32_t idGm = idesc_bf16(128, T::kMainN, 0, 1);    // dV, dK: A = TMEM, B MN-major
+      const uint32_t idGt = idesc_bf16(128, 16, 0, 1);
+      const uint32_t idQm = idesc_bf16(128, T::kMainN, 1, 1);    // dQ: A = dS MN-major smem, B = K MN-major
+      const uint32_t idQt = idesc_bf16(128, 16, 1, 1);
+      const uint32_t tS = tmem, tdP = tmem + 128, tdK = tmem + 256, tdV = tmem + 384;
+      mbar_wait(b_kv, 0);
+      tc_fence_after();
+      for (int n = 0; n < n_iter; ++n) {
+        const int s = n % QS;
+        const uint32_t st = base + C::oStage + s * C::kStage;
+        const uint32_t sQ = st, sO = st + T::kBytes;
+        mbar_wait(b_qfull(s), (n / QS) & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < T::kKSteps; ++kk) mma_ss(tS, T::desc_kmajor(sK, kk), T::desc_kmajor(sQ, kk), idS, kk > 0);
+        mma_commit(b_s);
+        if (n > 0) {
+          mbar_wait(b_dqempty, (n - 1) & 1);
+          tc_fence_after();
+        }
+#pragma unroll
+        for (int kk = 0; kk < T::kKSteps; ++kk) mma_ss(tdP, T::desc_kmajor(sV, kk), T::desc_kmajor(sO, kk), idS, kk > 0);
+        mma_commit(b_dp);
+        // dV += P^T dO
+        mbar_wait(b_p, n & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_ts(tdV, tS + kk * 8, T::desc_mn_main(sO, kk), idGm, (n > 0 || kk > 0));
+        if constexpr (T::kTail) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ts(tdV + T::kMainN, tS + kk * 8, T::desc_mn_tail(sO, kk), idGt, (n > 0 || kk > 0));
+        }
+        // dK += dS^T Q ; dQ = dS K
+        mbar_wait(b_ds, n & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_ts(tdK, tS + 64 + kk * 8, T::desc_mn_main(sQ, kk), idGm, (n > 0 || kk > 0));
+        if constexpr (T::kTail) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ts(tdK + T::kMainN, tS + 64 + kk * 8, T::desc_mn_tail(sQ, kk), idGt, (n > 0 || kk > 0));
+        }
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) mma_ss(tdP, desc_a_mn_sw128(sDS, kk), T::desc_mn_main(sK, kk), idQm, kk > 0);
+        if constexpr (T::kTail) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ss(tdP + T::kMainN, desc_a_mn_sw128(sDS, kk), T::desc_mn_tail(sK, kk), idQt, kk > 0);
+        }
+        mma_commit(b_dqfull);
+        mma_commit(b_dsfree);
+        mma_commit(b_qempty(s));
+      }
+      mma_commit(b_kvdone);
+    }
+  } else {
+    // ------------------------------------------------------------------ softmax gradient (key rows)
+    const int r = warp * 32 + lane;
+    const uint32_t lane_off = (warp * 32) << 16;
+    const uint32_t tS = tmem + lane_off, tdP = tmem + 128 + lane_off;
+    const int64_t kpos = kv_base + r;
+    const float sl2 = a.scale_log2;
+    for (int n = 0; n < n_iter; ++n) {
+      const int s = n % QS;
+      const int qt = qt_first + n / G;
+      const float* lse2 = reinterpret_cast<const float*>(smem + C::oStats + s * C::kStats);
+      const float* Dq = lse2 + 128;
+      mbar_wait(b_s, n & 1);
+      tc_fence_after();
+      float p[128];
+      tmem_ld32(tS + 0, reinterpret_cast<uint32_t*>(p));
+      tmem_ld32(tS + 32, reinterpret_cast<uint32_t*>(p) + 32);
+      tmem_ld32(tS + 64, reinterpret_cast<uint32_t*>(p) + 64);
+      tmem_ld32(tS + 96, reinterpret_cast<uint32_t*>(p) + 96);
+      tmem_wait_ld();
+      // stats of this stage were delivered with the Q tile (bar_qfull), which the MMA warp waited on
+      // before issuing S^T; bar_s completing therefore implies they are in smem.
+      const int64_t lim = a.causal ? (kpos - (a.q_pos0 + (int64_t)qt * 128)) : -1;  // q index < lim masked
+#pragma unroll
+      for (int i = 0; i < 128; ++i) {
+        const float v = ex2(fmaf(p[i], sl2, -lse2[i]));
+        p[i] = (i < lim) ? 0.f : v;
+      }
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) pk[i / 2] = pack_bf16x2(p[c + i], p[c + i + 1]);
+        tmem_st16(tS + c / 2, pk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(b_p);
+      mbar_wait(b_dp, n & 1);
+      if (n > 0) mbar_wait(b_dsfree, (n - 1) & 1);
+      tc_fence_after();
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) {
+        float dp[32];
+        tmem_ld32(tdP + c, reinterpret_cast<uint32_t*>(dp));
+        tmem_wait_ld();
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float d0 = p[c + i] * (dp[i] - Dq[c + i]);
+          const float d1 = p[c + i + 1] * (dp[i + 1] - Dq[c + i + 1]);
+          pk[i / 2] = pack_bf16x2(d0, d1);
+        }
+        tmem_st16(tS + 64 + c / 2, pk);
+#pragma unroll
+        for (int m8 = 0; m8 < 4; ++m8) {
+          const uint32_t w[4] = {pk[m8 * 4], pk[m8 * 4 + 1], pk[m8 * 4 + 2], pk[m8 * 4 + 3]};
+          st_shared_v4(sDS + mn_sw128_offset(c + m8 * 8, r), w);
+        }
+      }
+      tmem_wait_st();
+      fence_async_shared();
+      tc_fence_before();
+      mbar_arrive(b_ds);
+      // dQ read-out: TMEM lane r = query row r of this tile
+      {
+        const int h = g * G + n % G;
+        mbar_wait(b_dqfull, n & 1);
+        tc_fence_after();
+        float v[D];
+#pragma unroll
+        for (int c = 0; c < D; c += 16) tmem_ld16(tdP + c, reinterpret_cast<uint32_t(&)[16]>(v[c]));
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(b_dqempty);
+        const int64_t qrow = (int64_t)qt * 128 + r;
+        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (qrow * a.hq + h) * D);
+#pragma unroll
+        for (int c = 0; c < D; c += 4)
+          atomicAdd(dst + c / 4, make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale, v[c + 3] * a.scale));
+      }
+    }
+    // ---- dK / dV out (thread = key row)
+    const int64_t row = (int64_t)kt * 128 + r;  // row within the launch's key range
+    float* dk_acc = a.dk_acc + (row * (a.hq / G) + g) * D;
+    float* dv_acc = a.dv_acc + (row * (a.hq / G) + g) * D;
+    if (n_iter > 0) {
+      mbar_wait(b_kvdone, 0);
+      tc_fence_after();
+    }
+#pragma unroll
+    for (int which = 0; which < 2; ++which) {
+      float* acc = which ? dv_acc : dk_acc;
+      const float sc = which ? 1.f : a.scale;
+      __nv_bfloat16* out = which ? reinterpret_cast<__nv_bfloat16*>(a.dv_out) : reinterpret_cast<__nv_bfloat16*>(a.dk_out);
+      if (a.kv_final) out += row * a.kv_out_ld + (int64_t)(a.kv_out_head0 + g) * D;
+#pragma unroll
+      for (int c = 0; c < D; c += 16) {
+        float v[16];
+        if (n_iter > 0) {
+          tmem_ld16(tmem + (which ? 384 : 256) + lane_off + c, reinterpret_cast<uint32_t(&)[16]>(v));
+          tmem_wait_ld();
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] *= sc;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; ++i) v[i] = 0.f;
+        }
+        if (!a.kv_acc_init) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4) {
+            const float4 x = *reinterpret_cast<const float4*>(acc + c + i);
+            v[i] += x.x; v[i + 1] += x.y; v[i + 2] += x.z; v[i + 3] += x.w;
+          }
+        }
+        if (a.kv_final) {
+#pragma unroll
+          for (int i = 0; i < 16; i += 8) {
+            uint4 w;
+            w.x = pack_bf16x2(v[i], v[i + 1]); w.y = pack_bf16x2(v[i + 2], v[i + 3]);
+            w.z = pack_bf16x2(v[i + 4], v[i + 5]); w.w = pack_bf16x2(v[i + 6], v[i + 7]);
+            *reinterpret_cast<uint4*>(out + c + i) = w;
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 16; i += 4)
+            *reinterpret_cast<float4*>(acc + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        }
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 5) tmem_dealloc<512>(tmem);
+}
+
+template <int D>
+int launch_bwd(const BwdArgs& a, cudaStream_t s) {
+  using C = BwdCfg<D>;
+  TmapSet tm;
+  const CUtensorMapSwizzle s128 = CU_TENSOR_MAP_SWIZZLE_128B, s32 = CU_TENSOR_MAP_SWIZZLE_32B;
+  bool ok = true;
+  ok &= make_tmap_rows_heads_dim(&tm.q_main, a.q.base, a.q.rows, a.q.heads, D, 64, 128, s128);
+  ok &= make_tmap_rows_heads_dim(&tm.q_tail, a.q.base, a.q.rows, a.q.heads, D, 16, 128, s32);
+  ok &= make_tmap_rows_heads_dim(&tm.k_main, a.k.base, a.k.rows, a.k.heads, D, 64, 128, s128);
+  ok &= make_tmap_rows_heads_dim(&tm.k_tail, a.k.base, a.k.rows, a.k.heads, D, 16, 128, s32);
+  ok &= make_tmap_rows_heads_dim(&tm.v_main, a.v.base, a.v.rows, a.v.heads, D, 64, 128, s128);
+  ok &= make_tmap_rows_heads_dim(&tm.v_tail, a.v.base, a.v.rows, a.v.heads, D, 16, 128, s32);
+  ok &= make_tmap_rows_heads_dim(&tm.o_main, a.dout.base, a.dout.rows, a.dout.heads, D, 64, 128, s128);
+  ok &= make_tmap_rows_heads_dim(&tm.o_tail, a.dout.base, a.dout.rows, a.dout.heads, D, 16, 128, s32);
+  if (!ok) return -1;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_bwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr_set = true;
+  }
+  dim3 grid(a.n_kv_rows / 128, a.hq / a.G);
+  attn_bwd_kernel<D><<<grid, kThreads, C::kSmem, s>>>(tm, a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int launch_attn_bwd_bf16(const BwdArgs& a, int head_dim, cudaStream_t s) {
+  switch (head_dim) {
+    case 64: return launch_bwd<64>(a, s);
+    case 80: return launch_bwd<80>(a, s);
+    case 128: return launch_bwd<128>(a, s);
+  }
+  return -2;
+}
+
+}  // namespace fpdt

@@ -1,0 +1,358 @@
+// Forward chunk-pair attention for sm_100a: TMA-fed tcgen05 MMAs with TMEM accumulators.
+//
+// Computes, for one (query range, key/value range) pair of FPDT's chunk loop (PAPER.md L218-230,
+// fig:pipele_case2), the online-softmax attention of the query rows against the key/value rows and
+// merges it with the running partial result of earlier pairs by log-sum-exp (the "online attention
+// policy").  Causal masking on global token positions (key pos <= query pos; reading R3).
+//
+// CTA = 2 query tiles of 128 rows of ONE query head (sharing every K/V tile), 10 warps:
+//   warps 0-3  softmax + correction + epilogue of query tile 0 (thread = query row = TMEM lane)
+//   warps 4-7  same for query tile 1
+//   warp  8    TMA producer (Q once, then a K/V ring of kStages stages)
+//   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D); P_t (bf16) aliases S_t[0,64).
+// MMA order per key tile j:  PV0_j, S0_{j+1}, PV1_j, S1_{j+1} — tcgen05 MMAs of one thread execute in
+// issue order, so S_t{j+1} overwriting P_t_j after PV_t_j is safe, and the commit that signals S_t{j+1}
+// also guarantees PV_t_j has finished (so the softmax warps may rescale O_t in TMEM then).
+// Lazy rescale: the running max used for exponentiation is only raised when a row max exceeds it by
+// more than 8 (log2 units), bounding P by 2^8 (exact result either way; rescale skipped otherwise).
+#include "attn_tile.cuh"
+#include "kernels.h"
+#include "tma_host.h"
+
+namespace fpdt {
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 320;
+constexpr float kRescaleThreshold = 8.0f;
+
+template <int D>
+struct FwdCfg {
+  using T = Tile<D>;
+  static constexpr int kStages = (D == 128) ? 2 : 3;
+  static constexpr int kQBytes = 2 * T::kBytes;
+  static constexpr int kStageBytes = 2 * T::kBytes;  // K + V
+  static constexpr int kSmem = kQBytes + kStages * kStageBytes + 1024;
+};
+
+struct TmapSet {
+  CUtensorMap q_main, q_tail, k_main, k_tail, v_main, v_tail;
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float lg2(float x) {
+  float y;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+template <int D>
+__global__ void __launch_bounds__(kThreads, 1)
+attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdArgs a) {
+  using T = Tile<D>;
+  using C = FwdCfg<D>;
+  constexpr int ST = C::kStages;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  __shared__ uint64_t bar_q, bar_k[ST], bar_v[ST], bar_kv_empty[ST], bar_s[2], bar_p[2], bar_o[2];
+  __shared__ uint32_t tmem_slot;
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const uint32_t sQ = smem_u32(smem);
+  const uint32_t sKV = sQ + C::kQBytes;
+  const int h = blockIdx.y;
+  const int g = h / a.G;
+  // longest-first: for the causal diagonal block the last query tiles have the most key tiles
+  const int pair = gridDim.x - 1 - blockIdx.x;
+  const int64_t q_pos_first = a.q_pos0 + (int64_t)pair * 256;
+  int n_tiles = a.n_kv_rows / 128;
+  if (a.causal) {
+    const int64_t reach = q_pos_first + 256 - a.kv_pos0;  // keys visible to the last row of the CTA
+    const int64_t need = (reach + 127) / 128;
+    n_tiles = (int)(need < n_tiles ? need : n_tiles);
+  }
+
+  if (warp == 9) tmem_alloc<512>(smem_u32(&tmem_slot));
+  if (warp == 8 && lane == 0) {
+    mbar_init(smem_u32(&bar_q), 1);
+    for (int s = 0; s < ST; ++s) {
+      mbar_init(smem_u32(&bar_k[s]), 1);
+      mbar_init(smem_u32(&bar_v[s]), 1);
+      mbar_init(smem_u32(&bar_kv_empty[s]), 1);
+    }
+    for (int t = 0; t < 2; ++t) {
+      mbar_init(smem_u32(&bar_s[t]), 1);
+      mbar_init(smem_u32(&bar_p[t]), 128);
+      mbar_init(smem_u32(&bar_o[t]), 1);
+    }
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = tmem_slot;
+
+  if (warp == 8) {
+    // ------------------------------------------------------------------ TMA producer
+    if (elect_one()) {
+      tma_prefetch_desc(&tm.q_main);
+      tma_prefetch_desc(&tm.k_main);
+      tma_prefetch_desc(&tm.v_main);
+      const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
+      const uint32_t bq = smem_u32(&bar_q);
+      mbar_expect_tx(bq, C::kQBytes);
+      const int qrow = (int)(a.q_row0 + (int64_t)pair * 256);
+      T::load(sQ, &tm.q_main, &tm.q_tail, bq, a.q.head0 + h, qrow, pol_q);
+      T::load(sQ + T::kBytes, &tm.q_main, &tm.q_tail, bq, a.q.head0 + h, qrow + 128, pol_q);
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % ST;
+        if (j >= ST) mbar_wait(smem_u32(&bar_kv_empty[s]), ((j / ST) - 1) & 1);
+        const uint32_t sk = sKV + s * C::kStageBytes, sv = sk + T::kBytes;
+        const int krow = (int)(a.kv_row0 + (int64_t)j * 128);
+        mbar_expect_tx(smem_u32(&bar_k[s]), T::kBytes);
+        T::load(sk, &tm.k_main, &tm.k_tail, smem_u32(&bar_k[s]), a.k.head0 + g, krow, pol_kv);
+        mbar_expect_tx(smem_u32(&bar_v[s]), T::kBytes);
+        T::load(sv, &tm.v_main, &tm.v_tail, smem_u32(&bar_v[s]), a.v.head0 + g, krow, pol_kv);
+      }
+    }
+  } else if (warp == 9) {
+    // ------------------------------------------------------------------ MMA issuer
+    if (elect_one()) {
+      const uint32_t idS = idesc_bf16(128, 128, 0, 0);
+      const uint32_t idPVm = idesc_bf16(128, T::kMainN, 0, 1);
+      const uint32_t idPVt = idesc_bf16(128, 16, 0, 1);
+      const uint32_t tS[2] = {tmem, tmem + 128};
+      const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      auto issue_S = [&](int t, int s) {
+        const uint32_t sq = sQ + t * T::kBytes, sk = sKV + s * C::kStageBytes;
+#pragma unroll
+        for (int kk = 0; kk < T::kKSteps; ++kk)
+          mma_ss(tS[t], T::desc_kmajor(sq, kk), T::desc_kmajor(sk, kk), idS, kk > 0);
+      };
+      auto issue_PV = [&](int t, int s, int j) {
+        const uint32_t sv = sKV + s * C::kStageBytes + T::kBytes;
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk)
+          mma_ts(tO[t], tS[t] + kk * 8, T::desc_mn_main(sv, kk), idPVm, (j > 0 || kk > 0) ? 1u : 0u);
+        if constexpr (T::kTail) {
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ts(tO[t] + T::kMainN, tS[t] + kk * 8, T::desc_mn_tail(sv, kk), idPVt, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+      };
+      mbar_wait(smem_u32(&bar_q), 0);
+      tc_fence_after();
+      for (int j = 0; j < n_tiles; ++j) {
+        const int s = j % ST;
+        const uint32_t ph = (j / ST) & 1;
+        if (j == 0) {
+          mbar_wait(smem_u32(&bar_k[s]), ph);
+          tc_fence_after();
+          issue_S(0, s);
+          mma_commit(smem_u32(&bar_s[0]));
+          issue_S(1, s);
+          mma_commit(smem_u32(&bar_s[1]));
+        }
+        mbar_wait(smem_u32(&bar_v[s]), ph);
+        mbar_wait(smem_u32(&bar_p[0]), j & 1);
+        tc_fence_after();
+        issue_PV(0, s, j);
+        const bool more = j + 1 < n_tiles;
+        const int s2 = (j + 1) % ST;
+        if (more) {
+          mbar_wait(smem_u32(&bar_k[s2]), ((j + 1) / ST) & 1);
+          tc_fence_after();
+          issue_S(0, s2);
+          mma_commit(smem_u32(&bar_s[0]));
+        } else {
+          mma_commit(smem_u32(&bar_o[0]));
+        }
+        mbar_wait(smem_u32(&bar_p[1]), j & 1);
+        tc_fence_after();
+        issue_PV(1, s, j);
+        mma_commit(smem_u32(&bar_kv_empty[s]));
+        if (more) {
+          issue_S(1, s2);
+          mma_commit(smem_u32(&bar_s[1]));
+        } else {
+          mma_commit(smem_u32(&bar_o[1]));
+        }
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ softmax / correction / epilogue
+    const int t = warp >> 2;
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = ((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + t * 128 + lane_off;
+    const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    const int64_t qpos = q_pos_first + t * 128 + r;
+    const float sl2 = a.scale_log2;
+    float m_run = -INFINITY, l_run = 0.f;
+    for (int j = 0; j < n_tiles; ++j) {
+      mbar_wait(smem_u32(&bar_s[t]), j & 1);
+      tc_fence_after();
+      float x[128];
+      tmem_ld32(tS + 0, reinterpret_cast<uint32_t*>(x));
+      tmem_ld32(tS + 32, reinterpret_cast<uint32_t*>(x) + 32);
+      tmem_ld32(tS + 64, reinterpret_cast<uint32_t*>(x) + 64);
+      tmem_ld32(tS + 96, reinterpret_cast<uint32_t*>(x) + 96);
+      tmem_wait_ld();
+      if (a.causal) {
+        const int64_t lim = qpos - (a.kv_pos0 + (int64_t)j * 128);
+        if (lim < 127) {
+#pragma unroll
+          for (int i = 0; i < 128; ++i)
+            if (i > lim) x[i] = -INFINITY;
+        }
+      }
+      float mx = x[0];
+#pragma unroll
+      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, x[i]);
+      mx *= sl2;
+      const bool need = mx > m_run + kRescaleThreshold;
+      if (__any_sync(0xffffffffu, need)) {
+        const float m_new = need ? mx : m_run;
+        const float alpha = need ? ex2(m_run - m_new) : 1.f;
+        l_run *= alpha;
+        if (j > 0) {
+#pragma unroll
+          for (int c = 0; c < D; c += 16) {
+            uint32_t o[16];
+            tmem_ld16(tO + c, o);
+            tmem_wait_ld();
+#pragma unroll
+            for (int i = 0; i < 16; ++i) o[i] = __float_as_uint(__uint_as_float(o[i]) * alpha);
+            tmem_st16(tO + c, o);
+          }
+        }
+        m_run = m_new;
+      }
+      const float mb = (m_run == -INFINITY) ? 0.f : m_run;
+      float sum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 128; c += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float p0 = ex2(fmaf(x[c + i], sl2, -mb));
+          const float p1 = ex2(fmaf(x[c + i + 1], sl2, -mb));
+          sum += p0 + p1;
+          pk[i / 2] = pack_bf16x2(p0, p1);
+        }
+        tmem_st16(tS + c / 2, pk);
+      }
+      l_run += sum;
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(smem_u32(&bar_p[t]));
+    }
+    // epilogue: normalise, merge with the running partial result, write
+    mbar_wait(smem_u32(&bar_o[t]), 0);
+    tc_fence_after();
+    float o[D];
+#pragma unroll
+    for (int c = 0; c < D; c += 16) tmem_ld16(tO + c, reinterpret_cast<uint32_t(&)[16]>(o[c]));
+    tmem_wait_ld();
+    const float inv_l = 1.f / l_run;
+    float lse_b = m_run + lg2(l_run);
+    const int64_t row = (int64_t)pair * 256 + t * 128 + r;  // row within the launch's query range
+    float wb = inv_l;
+    float wa = 0.f;
+    float* acc_row = a.o_acc ? a.o_acc + (row * a.hq + h) * D : nullptr;
+    if (a.has_prev) {
+      const float lse_a = a.lse_acc[(int64_t)h * a.n_q_rows + row];
+      const float mxl = fmaxf(lse_a, lse_b);
+      const float ea = ex2(lse_a - mxl), eb = ex2(lse_b - mxl);
+      const float lse = mxl + lg2(ea + eb);
+      wa = ex2(lse_a - lse);
+      wb = inv_l * ex2(lse_b - lse);
+      lse_b = lse;
+    }
+#pragma unroll
+    for (int c = 0; c < D; c += 4) {
+      float4 v = make_float4(o[c] * wb, o[c + 1] * wb, o[c + 2] * wb, o[c + 3] * wb);
+      if (a.has_prev) {
+        const float4 pa = *reinterpret_cast<const float4*>(acc_row + c);
+        v.x += wa * pa.x; v.y += wa * pa.y; v.z += wa * pa.z; v.w += wa * pa.w;
+      }
+      o[c] = v.x; o[c + 1] = v.y; o[c + 2] = v.z; o[c + 3] = v.w;
+    }
+    if (a.is_final) {
+      __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(a.o_out) + row * a.o_ld + (int64_t)(a.o_head0 + h) * D;
+#pragma unroll
+      for (int c = 0; c < D; c += 8) {
+        uint4 w;
+        w.x = pack_bf16x2(o[c], o[c + 1]);
+        w.y = pack_bf16x2(o[c + 2], o[c + 3]);
+        w.z = pack_bf16x2(o[c + 4], o[c + 5]);
+        w.w = pack_bf16x2(o[c + 6], o[c + 7]);
+        *reinterpret_cast<uint4*>(out + c) = w;
+        if (a.o_resid) {
+          // residual O - bf16(O), so the backward can form D from the fp32 output (R9)
+          const __nv_bfloat162* wb2 = reinterpret_cast<const __nv_bfloat162*>(&w);
+          uint4 rw;
+          uint32_t* rp = reinterpret_cast<uint32_t*>(&rw);
+#pragma unroll
+          for (int i = 0; i < 4; ++i) {
+            const float2 f = __bfloat1622float2(wb2[i]);
+            rp[i] = pack_bf16x2(o[c + 2 * i] - f.x, o[c + 2 * i + 1] - f.y);
+          }
+          *reinterpret_cast<uint4*>(a.o_resid + row * a.o_resid_ld + (int64_t)h * D + c) = rw;
+        }
+      }
+      a.lse_save[(int64_t)h * a.lse_save_ld + row] = lse_b;
+      if (a.lse_user) a.lse_user[row * a.lse_user_ld + a.lse_user_head0 + h] = lse_b * 0.69314718055994531f;
+    } else {
+#pragma unroll
+      for (int c = 0; c < D; c += 4)
+        *reinterpret_cast<float4*>(acc_row + c) = make_float4(o[c], o[c + 1], o[c + 2], o[c + 3]);
+      a.lse_acc[(int64_t)h * a.n_q_rows + row] = lse_b;
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 9) tmem_dealloc<512>(tmem);
+}
+
+template <int D>
+int launch_fwd(const FwdArgs& a, cudaStream_t s) {
+  using C = FwdCfg<D>;
+  TmapSet tm;
+  const CUtensorMapSwizzle s128 = CU_TENSOR_MAP_SWIZZLE_128B, s32 = CU_TENSOR_MAP_SWIZZLE_32B;
+  bool ok = true;
+  ok &= make_tmap_rows_heads_dim(&tm.q_main, a.q.base, a.q.rows, a.q.heads, D, 64, 128, s128);
+  ok &= make_tmap_rows_heads_dim(&tm.q_tail, a.q.base, a.q.rows, a.q.heads, D, 16, 128, s32);
+  ok &= make_tmap_rows_heads_dim(&tm.k_main, a.k.base, a.k.rows, a.k.heads, D, 64, 128, s128);
+  ok &= make_tmap_rows_heads_dim(&tm.k_tail, a.k.base, a.k.rows, a.k.heads, D, 16, 128, s32);
+  ok &= make_tmap_rows_heads_dim(&tm.v_main, a.v.base, a.v.rows, a.v.heads, D, 64, 128, s128);
+  ok &= make_tmap_rows_heads_dim(&tm.v_tail, a.v.base, a.v.rows, a.v.heads, D, 16, 128, s32);
+  if (!ok) return -1;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr_set = true;
+  }
+  dim3 grid(a.n_q_rows / 256, a.hq);
+  attn_fwd_kernel<D><<<grid, kThreads, C::kSmem, s>>>(tm, a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+int launch_attn_fwd_bf16(const FwdArgs& a, int head_dim, cudaStream_t s) {
+  switch (head_dim) {
+    case 64: return launch_fwd<64>(a, s);
+    case 80: return launch_fwd<80>(a, s);
+    case 128: return launch_fwd<128>(a, s);
+  }
+  return -2;
+}
+
+}  // namespace fpdt

@@ -1,0 +1,885 @@
+// libfpdt host runtime: context, pinned host chunk store, device slots, stream/event chunk scheduler,
+// NCCL all-to-all, and the C-ABI entry points declared in include/fpdt.h.
+//
+// Schedules (§4.1-4.2):
+//   forward, offload=1:  per chunk m: [comm] all-to-all of q,k,v chunk m (p>1)  [d2h] offload q_m, kv_m
+//                        [compute] diagonal pair (m,m) ; for i<m: [h2d] fetch kv_i -> slot i%2,
+//                        [compute] pair (m,i) with LSE merge ; [comm] all-to-all of O_m back (p>1)
+//   forward, offload=0:  per chunk m one launch over the resident key range [0,(m+1)C)
+//   backward, offload=1: D preprocess; per chunk all-to-all of (O,dO) (p>1); offload dO_m;
+//                        for j (outer, key/value): [h2d] fetch kv_j; for i>=j (inner, query):
+//                        [h2d] fetch q_i, dO_i, dq_acc_i (j>0) -> slot ; [compute] pair (i,j) ;
+//                        i>j: [d2h] dq_acc_i -> host ; i==j: dq_j final ; after the inner loop dk_j, dv_j
+//                        final -> [comm] all-to-all of dq_j,dk_j,dv_j back (p>1)
+//   backward, offload=0: per j one launch over the resident query range [jC, S)
+// Streams: compute (= the caller's stream), comm, h2d, d2h; every cross-stream dependency is an event.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+
+#include "fpdt.h"
+#include "kernels.h"
+
+using namespace fpdt;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+  int code;
+};
+
+#define FPDT_CHECK_CUDA(x)                                                                          \
+  do {                                                                                              \
+    cudaError_t e_ = (x);                                                                           \
+    if (e_ != cudaSuccess) {                                                                        \
+      g_last_error = std::string(#x) + ": " + cudaGetErrorString(e_);                               \
+      throw Fail{e_ == cudaErrorMemoryAllocation ? FPDT_ERR_DEVICE_OOM : FPDT_ERR_CUDA};            \
+    }                                                                                               \
+  } while (0)
+
+#define FPDT_CHECK_NCCL(x)                                                                          \
+  do {                                                                                              \
+    ncclResult_t r_ = (x);                                                                          \
+    if (r_ != ncclSuccess) {                                                                        \
+      g_last_error = std::string(#x) + ": " + ncclGetErrorString(r_);                               \
+      throw Fail{FPDT_ERR_NCCL};                                                                    \
+    }                                                                                               \
+  } while (0)
+
+#define FPDT_CHECK_LAUNCH(x)                                                                        \
+  do {                                                                                              \
+    int r_ = (x);                                                                                   \
+    if (r_ != 0) {                                                                                  \
+      g_last_error = std::string(#x) + " failed: " +                                                \
+                     (r_ > 0 ? cudaGetErrorString((cudaError_t)r_) : "tensor map / argument error"); \
+      throw Fail{FPDT_ERR_CUDA};                                                                    \
+    }                                                                                               \
+  } while (0)
+
+[[noreturn]] void fail(int code, const std::string& msg) {
+  g_last_error = msg;
+  throw Fail{code};
+}
+
+struct Config {
+  int64_t s_local = 0;
+  int Hq = 0, Hkv = 0, d = 0, causal = 1;
+  int64_t C = 0;
+  int p = 1, dtype = 0, offload = 1;
+  float scale = 0.f;
+  // derived
+  int64_t c = 0, u = 0, S = 0;
+  int hq = 0, hkv = 0, G = 1, eb = 2;
+  bool operator==(const Config& o) const {
+    return s_local == o.s_local && Hq == o.Hq && Hkv == o.Hkv && d == o.d && causal == o.causal && C == o.C &&
+           p == o.p && dtype == o.dtype && offload == o.offload && scale == o.scale;
+  }
+};
+
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+};
+
+enum BufId {
+  B_OACC, B_LSEACC, B_LSESAVE, B_OHAT, B_KVSLOT0, B_KVSLOT1, B_A2A_SEND0, B_A2A_SEND1, B_A2A_RECV0, B_A2A_RECV1,
+  B_STORE, B_D, B_DQDEV, B_QSLOT0, B_QSLOT1, B_DOSLOT0, B_DOSLOT1, B_DQSLOT0, B_DQSLOT1, B_DKACC, B_DVACC,
+  B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_NUM
+};
+
+}  // namespace
+
+struct fpdt_ctx {
+  int p = 1, rank = 0, device = 0;
+  ncclComm_t comm = nullptr;
+  cudaStream_t s_comm = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+  uint8_t* host = nullptr;
+  size_t host_bytes = 0;
+  DevBuf bufs[B_NUM];
+  // per-chunk events
+  std::vector<cudaEvent_t> ev_off, ev_doff, ev_dqoff, ev_a2a;
+  cudaEvent_t ev_enter = nullptr, ev_slot_free[2] = {}, ev_slot_filled[2] = {}, ev_q_free[2] = {}, ev_q_filled[2] = {},
+              ev_dq_ready[2] = {}, ev_kv_free[2] = {}, ev_kv_filled[2] = {}, ev_recv_used_c[2] = {},
+              ev_recv_used_d[2] = {}, ev_o_ready = nullptr, ev_comm_done = nullptr, ev_d2h_done = nullptr,
+              ev_h2d_done = nullptr, ev_tmp = nullptr;
+  // saved state
+  bool fwd_done = false;
+  Config saved;
+  const void *saved_q = nullptr, *saved_k = nullptr, *saved_v = nullptr;
+  fpdt_stats stats{};
+  // kernel timing
+  bool timing = false;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_fwd, t_bwd;
+  size_t n_fwd = 0, n_bwd = 0;
+};
+
+namespace {
+
+void* dev(fpdt_ctx* ctx, int id, size_t bytes) {
+  DevBuf& b = ctx->bufs[id];
+  if (b.bytes < bytes) {
+    if (b.ptr) {
+      FPDT_CHECK_CUDA(cudaDeviceSynchronize());
+      FPDT_CHECK_CUDA(cudaFree(b.ptr));
+      ctx->stats.device_bytes -= (int64_t)b.bytes;
+      b.ptr = nullptr;
+      b.bytes = 0;
+    }
+    cudaError_t e = cudaMalloc(&b.ptr, bytes);
+    if (e != cudaSuccess) {
+      cudaGetLastError();
+      b.ptr = nullptr;
+      fail(FPDT_ERR_DEVICE_OOM, "cudaMalloc of " + std::to_string(bytes) + " bytes failed: " + cudaGetErrorString(e));
+    }
+    b.bytes = bytes;
+    ctx->stats.device_bytes += (int64_t)bytes;
+  }
+  return b.ptr;
+}
+
+void ensure_events(std::vector<cudaEvent_t>& v, size_t n) {
+  while (v.size() < n) {
+    cudaEvent_t e;
+    FPDT_CHECK_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    v.push_back(e);
+  }
+}
+
+void rec(cudaEvent_t e, cudaStream_t s) { FPDT_CHECK_CUDA(cudaEventRecord(e, s)); }
+void wait(cudaStream_t s, cudaEvent_t e) { FPDT_CHECK_CUDA(cudaStreamWaitEvent(s, e, 0)); }
+
+Config make_config(int64_t s_local, int Hq, int Hkv, int d, int causal, int64_t C, int p, int dtype, int offload,
+                   float scale) {
+  Config c;
+  c.s_local = s_local; c.Hq = Hq; c.Hkv = Hkv; c.d = d; c.causal = causal; c.C = C; c.p = p;
+  c.dtype = dtype; c.offload = offload ? 1 : 0;
+  c.scale = scale > 0.f ? scale : (float)(1.0 / std::sqrt((double)d));
+  if (s_local <= 0 || Hq <= 0 || Hkv <= 0 || C <= 0 || p <= 0) fail(FPDT_ERR_ARG, "non-positive size argument");
+  if (d != 64 && d != 80 && d != 128) fail(FPDT_ERR_UNSUPPORTED, "head_dim must be 64, 80 or 128");
+  if (causal != 1) fail(FPDT_ERR_UNSUPPORTED, "only causal attention (causal=1) is supported");
+  if (dtype != FPDT_BF16 && dtype != FPDT_FP32) fail(FPDT_ERR_UNSUPPORTED, "dtype must be FPDT_BF16 or FPDT_FP32");
+  if (C % p) fail(FPDT_ERR_DIVISIBILITY, "chunk_size % world_size != 0");
+  c.c = C / p;
+  if (s_local % c.c) fail(FPDT_ERR_DIVISIBILITY, "s_local % (chunk_size / world_size) != 0 (S % C != 0)");
+  if (C % 256) fail(FPDT_ERR_DIVISIBILITY, "chunk_size must be a multiple of 256");
+  if (Hq % p || Hkv % p) fail(FPDT_ERR_DIVISIBILITY, "head counts must be divisible by world_size");
+  if (Hq % Hkv) fail(FPDT_ERR_DIVISIBILITY, "n_q_heads % n_kv_heads != 0");
+  c.u = s_local / c.c;
+  c.S = c.u * C;
+  c.hq = Hq / p;
+  c.hkv = Hkv / p;
+  c.G = Hq / Hkv;
+  c.eb = dtype == FPDT_BF16 ? 2 : 4;
+  return c;
+}
+
+// Host chunk store layout (offload=1): per chunk m, q_m [C][hq][d], kv_m [C][2hkv][d], dO_m [C][hq][d] (eb bytes),
+// dq_acc_m [C][hq][d] fp32.
+struct HostLayout {
+  size_t q_bytes, kv_bytes, do_bytes, dq_bytes, total;
+  size_t q(int64_t m) const { return (size_t)m * q_bytes; }
+  size_t kv(int64_t m, int64_t u) const { return (size_t)u * q_bytes + (size_t)m * kv_bytes; }
+  size_t dO(int64_t m, int64_t u) const { return (size_t)u * (q_bytes + kv_bytes) + (size_t)m * do_bytes; }
+  size_t dq(int64_t m, int64_t u) const { return (size_t)u * (q_bytes + kv_bytes + do_bytes) + (size_t)m * dq_bytes; }
+};
+HostLayout host_layout(const Config& c) {
+  HostLayout h;
+  h.q_bytes = (size_t)c.C * c.hq * c.d * c.eb;
+  h.kv_bytes = (size_t)c.C * 2 * c.hkv * c.d * c.eb;
+  h.do_bytes = h.q_bytes;
+  h.dq_bytes = (size_t)c.C * c.hq * c.d * 4;
+  h.total = (size_t)c.u * (h.q_bytes + h.kv_bytes + h.do_bytes + h.dq_bytes);
+  return h;
+}
+
+void ensure_host(fpdt_ctx* ctx, size_t bytes) {
+  if (ctx->host_bytes >= bytes) return;
+  if (ctx->host) {
+    FPDT_CHECK_CUDA(cudaDeviceSynchronize());
+    cudaFreeHost(ctx->host);
+    ctx->host = nullptr;
+    ctx->host_bytes = 0;
+  }
+  void* p = nullptr;
+  cudaError_t e = cudaHostAlloc(&p, bytes, cudaHostAllocDefault);
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    fail(FPDT_ERR_HOST_OOM, "pinned host store of " + std::to_string(bytes) + " bytes: " + cudaGetErrorString(e));
+  }
+  ctx->host = static_cast<uint8_t*>(p);
+  ctx->host_bytes = bytes;
+  ctx->stats.host_arena_bytes = (int64_t)bytes;
+}
+
+void h2d(fpdt_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  FPDT_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->s_h2d));
+  ctx->stats.bytes_h2d += (int64_t)bytes;
+}
+void d2h(fpdt_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  FPDT_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
+  ctx->stats.bytes_d2h += (int64_t)bytes;
+}
+void d2h_2d(fpdt_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows) {
+  FPDT_CHECK_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, ctx->s_d2h));
+  ctx->stats.bytes_d2h += (int64_t)(width * rows);
+}
+
+void alltoall(fpdt_ctx* ctx, const void* send, void* recv, size_t count_per_peer, int dtype) {
+  FPDT_CHECK_NCCL(ncclAlltoAll(send, recv, count_per_peer, dtype == FPDT_BF16 ? ncclBfloat16 : ncclFloat32, ctx->comm,
+                               ctx->s_comm));
+  ctx->stats.bytes_a2a += (int64_t)(count_per_peer * (ctx->p - 1) * (dtype == FPDT_BF16 ? 2 : 4));
+}
+
+struct TimedScope {
+  fpdt_ctx* ctx;
+  bool fwd;
+  cudaStream_t s;
+  std::pair<cudaEvent_t, cudaEvent_t>* ev = nullptr;
+  TimedScope(fpdt_ctx* c, bool f, cudaStream_t st) : ctx(c), fwd(f), s(st) {
+    if (!ctx->timing) return;
+    auto& v = fwd ? ctx->t_fwd : ctx->t_bwd;
+    size_t& n = fwd ? ctx->n_fwd : ctx->n_bwd;
+    if (v.size() <= n) {
+      cudaEvent_t a, b;
+      FPDT_CHECK_CUDA(cudaEventCreate(&a));
+      FPDT_CHECK_CUDA(cudaEventCreate(&b));
+      v.push_back({a, b});
+    }
+    ev = &v[n++];
+    rec(ev->first, s);
+  }
+  ~TimedScope() {
+    if (ev) cudaEventRecord(ev->second, s);
+  }
+};
+
+void launch_fwd(fpdt_ctx* ctx, const Config& c, const FwdArgs& a, cudaStream_t s) {
+  TimedScope t(ctx, true, s);
+  if (c.dtype == FPDT_BF16)
+    FPDT_CHECK_LAUNCH(launch_attn_fwd_bf16(a, c.d, s));
+  else
+    FPDT_CHECK_LAUNCH(launch_attn_fwd_f32(a, c.d, s));
+  ctx->stats.kernel_launches++;
+  ctx->stats.attn_launches++;
+}
+void launch_bwd(fpdt_ctx* ctx, const Config& c, const BwdArgs& a, cudaStream_t s) {
+  TimedScope t(ctx, false, s);
+  if (c.dtype == FPDT_BF16)
+    FPDT_CHECK_LAUNCH(launch_attn_bwd_bf16(a, c.d, s));
+  else
+    FPDT_CHECK_LAUNCH(launch_attn_bwd_f32(a, c.d, s));
+  ctx->stats.kernel_launches += c.dtype == FPDT_BF16 ? 1 : 2;
+  ctx->stats.attn_launches++;
+}
+
+// ------------------------------------------------------------------------------------------ forward
+void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const void* v, void* o, float* lse,
+             cudaStream_t cs) {
+  const int64_t C = c.C, u = c.u;
+  const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
+  const size_t row_q = (size_t)hq * d * eb, row_kv2 = (size_t)2 * hkv * d * eb;
+  const int hcomb = hq + 2 * hkv;  // combined head-layout buffer: q heads, k heads, v heads
+  const float sl2 = c.scale * 1.4426950408889634f;
+  float* lse_save = (float*)dev(ctx, B_LSESAVE, (size_t)hq * c.S * 4);
+  __nv_bfloat16* o_resid = c.dtype == FPDT_BF16 ? (__nv_bfloat16*)dev(ctx, B_ORESID, (size_t)c.S * hq * d * 2) : nullptr;
+  float* o_acc = nullptr;
+  float* lse_acc = nullptr;
+  if (c.offload) {
+    o_acc = (float*)dev(ctx, B_OACC, (size_t)C * hq * d * 4);
+    lse_acc = (float*)dev(ctx, B_LSEACC, (size_t)hq * C * 4);
+  }
+  ensure_events(ctx->ev_off, u);
+  ensure_events(ctx->ev_a2a, u);
+  rec(ctx->ev_enter, cs);
+  for (cudaStream_t s : {ctx->s_comm, ctx->s_h2d, ctx->s_d2h}) wait(s, ctx->ev_enter);
+  HostLayout hl{};
+  if (c.offload) {
+    hl = host_layout(c);
+    ensure_host(ctx, hl.total);
+  }
+  // device store for resident mode with p > 1: gathered [S][hcomb][d]
+  uint8_t* store = nullptr;
+  if (!c.offload && p > 1) store = (uint8_t*)dev(ctx, B_STORE, (size_t)c.S * hcomb * d * eb);
+  uint8_t* o_hat = p > 1 ? (uint8_t*)dev(ctx, B_OHAT, (size_t)C * hq * d * eb) : nullptr;
+  uint8_t* a2a_send[2] = {nullptr, nullptr};
+  uint8_t* a2a_recv[2] = {nullptr, nullptr};
+  if (p > 1) {
+    for (int b = 0; b < 2; ++b) {
+      a2a_send[b] = (uint8_t*)dev(ctx, B_A2A_SEND0 + b, (size_t)C * hcomb * d * eb);
+      if (c.offload) a2a_recv[b] = (uint8_t*)dev(ctx, B_A2A_RECV0 + b, (size_t)C * hcomb * d * eb);
+    }
+  }
+  uint8_t* kv_slot[2] = {nullptr, nullptr};
+  if (c.offload) {
+    kv_slot[0] = (uint8_t*)dev(ctx, B_KVSLOT0, (size_t)C * row_kv2);
+    kv_slot[1] = (uint8_t*)dev(ctx, B_KVSLOT1, (size_t)C * row_kv2);
+    for (int b = 0; b < 2; ++b) rec(ctx->ev_slot_free[b], cs);
+  }
+  for (int b = 0; b < 2; ++b) {
+    rec(ctx->ev_recv_used_c[b], cs);
+    rec(ctx->ev_recv_used_d[b], cs);
+  }
+  // p == 1 with offload: the head-layout chunk IS the caller's rows; offload all chunks up front
+  if (p == 1 && c.offload) {
+    for (int64_t m = 0; m < u; ++m) {
+      d2h(ctx, ctx->host + hl.q(m), (const uint8_t*)q + (size_t)m * C * row_q, (size_t)C * row_q);
+      const size_t wkv = (size_t)hkv * d * eb;
+      d2h_2d(ctx, ctx->host + hl.kv(m, u), row_kv2, (const uint8_t*)k + (size_t)m * C * wkv, wkv, wkv, C);
+      d2h_2d(ctx, ctx->host + hl.kv(m, u) + wkv, row_kv2, (const uint8_t*)v + (size_t)m * C * wkv, wkv, wkv, C);
+      rec(ctx->ev_off[m], ctx->s_d2h);
+    }
+  }
+  int fetch = 0;
+  int64_t high = 0;
+  for (int64_t m = 0; m < u; ++m) {
+    // ---- views of the current chunk's q, k, v in the head layout
+    HeadView qv, kv, vv;
+    int64_t q_row0, kv_row0_cur;
+    if (p == 1) {
+      qv = {q, c.S, hq, 0};
+      kv = {k, c.S, hkv, 0};
+      vv = {v, c.S, hkv, 0};
+      q_row0 = m * C;
+      kv_row0_cur = m * C;
+    } else {
+      // F3/F4: pack q,k,v rows of slot m and all-to-all (seq -> head)
+      const int b = (int)(m & 1);
+      uint8_t* recv = c.offload ? a2a_recv[b] : store + (size_t)m * C * hcomb * d * eb;
+      wait(ctx->s_comm, ctx->ev_recv_used_c[b]);
+      wait(ctx->s_comm, ctx->ev_recv_used_d[b]);
+      const size_t per_peer = (size_t)c.c * hcomb * d;
+      FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)q + (size_t)m * c.c * c.Hq * d * eb, c.c, c.Hq, d, p, eb,
+                                             a2a_send[b], per_peer, (int64_t)hcomb * d, 0, ctx->s_comm));
+      FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)k + (size_t)m * c.c * c.Hkv * d * eb, c.c, c.Hkv, d, p,
+                                             eb, a2a_send[b], per_peer, (int64_t)hcomb * d, hq, ctx->s_comm));
+      FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)v + (size_t)m * c.c * c.Hkv * d * eb, c.c, c.Hkv, d, p,
+                                             eb, a2a_send[b], per_peer, (int64_t)hcomb * d, hq + hkv, ctx->s_comm));
+      ctx->stats.kernel_launches += 3;
+      alltoall(ctx, a2a_send[b], recv, per_peer, c.dtype);
+      rec(ctx->ev_a2a[m], ctx->s_comm);
+      if (c.offload) {
+        // F5: offload q_m, kv_m from the receive buffer
+        wait(ctx->s_d2h, ctx->ev_a2a[m]);
+        const size_t pitch = (size_t)hcomb * d * eb;
+        d2h_2d(ctx, ctx->host + hl.q(m), row_q, recv, pitch, row_q, C);
+        d2h_2d(ctx, ctx->host + hl.kv(m, u), row_kv2, recv + row_q, pitch, row_kv2, C);
+        rec(ctx->ev_off[m], ctx->s_d2h);
+        rec(ctx->ev_recv_used_d[b], ctx->s_d2h);
+      }
+      wait(cs, ctx->ev_a2a[m]);
+      const uint8_t* base = c.offload ? recv : store;
+      qv = {base, c.offload ? C : c.S, hcomb, 0};
+      kv = {base, c.offload ? C : c.S, hcomb, hq};
+      vv = {base, c.offload ? C : c.S, hcomb, hq + hkv};
+      q_row0 = c.offload ? 0 : m * C;
+      kv_row0_cur = c.offload ? 0 : m * C;
+    }
+    FwdArgs a;
+    a.q = qv;
+    a.q_row0 = q_row0;
+    a.n_q_rows = (int)C;
+    a.q_pos0 = m * C;
+    a.causal = 1;
+    a.hq = hq;
+    a.G = c.G;
+    a.scale_log2 = sl2;
+    a.o_acc = o_acc;
+    a.lse_acc = lse_acc;
+    if (p == 1) {
+      a.o_out = (uint8_t*)o + (size_t)m * C * c.Hq * d * eb;
+      a.o_ld = (int64_t)c.Hq * d;
+      a.lse_user = lse ? lse + (size_t)m * C * c.Hq : nullptr;
+      a.lse_user_ld = c.Hq;
+    } else {
+      a.o_out = o_hat;
+      a.o_ld = (int64_t)hq * d;
+    }
+    a.lse_save = lse_save + m * C;
+    a.lse_save_ld = c.S;
+    a.o_resid = o_resid ? o_resid + (size_t)m * C * hq * d : nullptr;
+    a.o_resid_ld = (int64_t)hq * d;
+    if (!c.offload) {
+      // resident: one launch over keys [0, (m+1)C)
+      a.k = kv;
+      a.v = vv;
+      a.kv_row0 = 0;
+      a.n_kv_rows = (int)((m + 1) * C);
+      a.kv_pos0 = 0;
+      a.has_prev = 0;
+      a.is_final = 1;
+      launch_fwd(ctx, c, a, cs);
+    } else {
+      // F6: diagonal block with the resident chunk
+      a.k = kv;
+      a.v = vv;
+      a.kv_row0 = kv_row0_cur;
+      a.n_kv_rows = (int)C;
+      a.kv_pos0 = m * C;
+      a.has_prev = 0;
+      a.is_final = (m == 0);
+      launch_fwd(ctx, c, a, cs);
+      if (p > 1) rec(ctx->ev_recv_used_c[m & 1], cs);
+      // F7/F8: earlier chunks fetched from the host store, double-buffered
+      for (int64_t i = 0; i < m; ++i) {
+        const int sl = fetch & 1;
+        wait(ctx->s_h2d, ctx->ev_slot_free[sl]);
+        wait(ctx->s_h2d, ctx->ev_off[i]);
+        h2d(ctx, kv_slot[sl], ctx->host + hl.kv(i, u), (size_t)C * row_kv2);
+        rec(ctx->ev_slot_filled[sl], ctx->s_h2d);
+        high = std::max<int64_t>(high, std::min<int64_t>(fetch + 1, 2));  // slots 0/1 alternate
+        wait(cs, ctx->ev_slot_filled[sl]);
+        a.k = {kv_slot[sl], C, 2 * hkv, 0};
+        a.v = {kv_slot[sl], C, 2 * hkv, hkv};
+        a.kv_row0 = 0;
+        a.kv_pos0 = i * C;
+        a.has_prev = 1;
+        a.is_final = (i == m - 1);
+        launch_fwd(ctx, c, a, cs);
+        rec(ctx->ev_slot_free[sl], cs);
+        ++fetch;
+      }
+    }
+    if (p > 1) {
+      // F10: all-to-all of O_m back to the sequence layout, then unpack into the caller's rows of slot m
+      rec(ctx->ev_o_ready, cs);
+      wait(ctx->s_comm, ctx->ev_o_ready);
+      uint8_t* back = (uint8_t*)dev(ctx, B_BWD_RECV, (size_t)C * hq * d * eb);
+      alltoall(ctx, o_hat, back, (size_t)c.c * hq * d, c.dtype);
+      FPDT_CHECK_LAUNCH(launch_unpack_head2seq(back, (int64_t)c.c * hq * d, (int64_t)hq * d, 0, c.c, c.Hq, d, p, eb,
+                                               (uint8_t*)o + (size_t)m * c.c * c.Hq * d * eb, ctx->s_comm));
+      ctx->stats.kernel_launches++;
+      if (lse) {
+        // lse of this chunk: [hq][C] log2 -> [C][hq] natural, all-to-all (fp32), unpack to [c][Hq]
+        float* lt = (float*)dev(ctx, B_LSE_T, (size_t)C * hq * 4);
+        float* lr = (float*)dev(ctx, B_LSE_RECV, (size_t)C * hq * 4);
+        FPDT_CHECK_LAUNCH(launch_lse_to_user(lse_save + m * C, c.S, C, hq, lt, hq, 0, ctx->s_comm));
+        FPDT_CHECK_NCCL(ncclAlltoAll(lt, lr, (size_t)c.c * hq, ncclFloat32, ctx->comm, ctx->s_comm));
+        // unpack [p][c][hq] -> [c][Hq]: treat each row of hq floats as one head of hq*4 bytes... use 1-float heads
+        for (int r = 0; r < p; ++r)
+          FPDT_CHECK_CUDA(cudaMemcpy2DAsync(lse + (size_t)m * c.c * c.Hq + (size_t)r * hq, (size_t)c.Hq * 4,
+                                            lr + (size_t)r * c.c * hq, (size_t)hq * 4, (size_t)hq * 4, c.c,
+                                            cudaMemcpyDeviceToDevice, ctx->s_comm));
+        ctx->stats.kernel_launches++;
+      }
+      rec(ctx->ev_comm_done, ctx->s_comm);
+      wait(cs, ctx->ev_comm_done);  // o_hat reuse by the next chunk waits for the send
+    }
+  }
+  ctx->stats.fetch_slots_highwater = std::max(ctx->stats.fetch_slots_highwater, high);
+  // the caller may reuse q/k/v after the call: every offload must have read them
+  rec(ctx->ev_d2h_done, ctx->s_d2h);
+  wait(cs, ctx->ev_d2h_done);
+  rec(ctx->ev_comm_done, ctx->s_comm);
+  wait(cs, ctx->ev_comm_done);
+}
+
+// ------------------------------------------------------------------------------------------ backward
+void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, void* dq, void* dk, void* dv,
+              cudaStream_t cs) {
+  const int64_t C = c.C, u = c.u;
+  const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
+  const int hcomb = hq + 2 * hkv;
+  const size_t row_q = (size_t)hq * d * eb, row_kv2 = (size_t)2 * hkv * d * eb;
+  const float sl2 = c.scale * 1.4426950408889634f;
+  float* lse_save = (float*)ctx->bufs[B_LSESAVE].ptr;
+  float* Dh = (float*)dev(ctx, B_D, (size_t)hq * c.S * 4);
+  const __nv_bfloat16* o_resid = c.dtype == FPDT_BF16 ? (const __nv_bfloat16*)ctx->bufs[B_ORESID].ptr : nullptr;
+  ensure_events(ctx->ev_doff, u);
+  ensure_events(ctx->ev_dqoff, u);
+  ensure_events(ctx->ev_a2a, u);
+  rec(ctx->ev_enter, cs);
+  for (cudaStream_t s : {ctx->s_comm, ctx->s_h2d, ctx->s_d2h}) wait(s, ctx->ev_enter);
+  HostLayout hl{};
+  if (c.offload) hl = host_layout(c);
+  // ---- B1/B2: D and the head-layout dO
+  const void* do_h = dout;            // head-layout dO view base (p == 1: the caller's dO)
+  int64_t do_rows = c.S;
+  int do_heads = hq, do_head0 = 0;
+  uint8_t* gathered = nullptr;        // p > 1: [S or C][2hq][d] gathered (O, dO)
+  if (p == 1) {
+    FPDT_CHECK_LAUNCH(launch_bwd_preprocess_D(o, dout, c.dtype, c.S, hq, d, (int64_t)c.Hq * d, o_resid,
+                                              (int64_t)hq * d, Dh, c.S, cs));
+    ctx->stats.kernel_launches++;
+    if (c.offload) {
+      rec(ctx->ev_tmp, cs);
+      wait(ctx->s_d2h, ctx->ev_tmp);
+      for (int64_t m = 0; m < u; ++m) {
+        d2h(ctx, ctx->host + hl.dO(m, u), (const uint8_t*)dout + (size_t)m * C * row_q, (size_t)C * row_q);
+        rec(ctx->ev_doff[m], ctx->s_d2h);
+      }
+    }
+  } else {
+    // all-to-all of (O, dO) per chunk; D from the gathered head-layout chunks
+    const size_t per_peer = (size_t)c.c * 2 * hq * d;
+    uint8_t* send = (uint8_t*)dev(ctx, B_A2A_SEND0, (size_t)C * 2 * hq * d * eb);
+    gathered = (uint8_t*)dev(ctx, B_DOSTORE, (size_t)(c.offload ? 2 * C : c.S) * 2 * hq * d * eb);
+    for (int64_t m = 0; m < u; ++m) {
+      uint8_t* recv = c.offload ? gathered + (size_t)(m & 1) * C * 2 * hq * d * eb
+                                : gathered + (size_t)m * C * 2 * hq * d * eb;
+      if (c.offload && m >= 2) wait(ctx->s_comm, ctx->ev_doff[m - 2]);
+      FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)o + (size_t)m * c.c * c.Hq * d * eb, c.c, c.Hq, d, p, eb,
+                                             send, per_peer, (int64_t)2 * hq * d, 0, ctx->s_comm));
+      FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)dout + (size_t)m * c.c * c.Hq * d * eb, c.c, c.Hq, d, p,
+                                             eb, send, per_peer, (int64_t)2 * hq * d, hq, ctx->s_comm));
+      ctx->stats.kernel_launches += 2;
+      alltoall(ctx, send, recv, per_peer, c.dtype);
+      // D for rows [mC, (m+1)C) in the head layout (o = heads [0,hq), dO = heads [hq,2hq) of recv)
+      FPDT_CHECK_LAUNCH(launch_bwd_preprocess_D(recv, recv + row_q, c.dtype, C, hq, d, (int64_t)2 * hq * d,
+                                                o_resid ? o_resid + (size_t)m * C * hq * d : nullptr,
+                                                (int64_t)hq * d, Dh + m * C, c.S, ctx->s_comm));
+      ctx->stats.kernel_launches++;
+      rec(ctx->ev_a2a[m], ctx->s_comm);
+      if (c.offload) {
+        wait(ctx->s_d2h, ctx->ev_a2a[m]);
+        d2h_2d(ctx, ctx->host + hl.dO(m, u), row_q, recv + row_q, (size_t)2 * hq * d * eb, row_q, C);
+        rec(ctx->ev_doff[m], ctx->s_d2h);
+      }
+    }
+    rec(ctx->ev_comm_done, ctx->s_comm);
+    wait(cs, ctx->ev_comm_done);
+    do_h = gathered;
+    do_rows = c.S;
+    do_heads = 2 * hq;
+    do_head0 = hq;
+  }
+
+  float* dk_acc = (float*)dev(ctx, B_DKACC, (size_t)C * hkv * d * 4);
+  float* dv_acc = (float*)dev(ctx, B_DVACC, (size_t)C * hkv * d * 4);
+  uint8_t* bsend = p > 1 ? (uint8_t*)dev(ctx, B_BWD_SEND, (size_t)C * hcomb * d * eb) : nullptr;
+  uint8_t* brecv = p > 1 ? (uint8_t*)dev(ctx, B_BWD_RECV, (size_t)C * hcomb * d * eb) : nullptr;
+
+  // B6: dq_j final (fp32, already scaled) -> the caller's rows (p == 1) or the head-side send buffer (p > 1)
+  auto emit_dq = [&](int64_t j, const float* dq_final) {
+    if (p == 1)
+      FPDT_CHECK_LAUNCH(launch_convert_out(dq_final, C, hq, d, 1.f, (uint8_t*)dq + (size_t)j * C * c.Hq * d * eb,
+                                           c.dtype, (int64_t)c.Hq * d, 0, cs));
+    else
+      FPDT_CHECK_LAUNCH(launch_convert_out(dq_final, C, hq, d, 1.f, bsend, c.dtype, (int64_t)hcomb * d, 0, cs));
+    ctx->stats.kernel_launches++;
+  };
+  // B7: after outer iteration j, dq_j, dk_j, dv_j (in bsend) go back to their owner ranks (p > 1)
+  auto send_back = [&](int64_t j) {
+    if (p == 1) return;
+    rec(ctx->ev_o_ready, cs);
+    wait(ctx->s_comm, ctx->ev_o_ready);
+    alltoall(ctx, bsend, brecv, (size_t)c.c * hcomb * d, c.dtype);
+    const int64_t pst = (int64_t)c.c * hcomb * d, rld = (int64_t)hcomb * d;
+    FPDT_CHECK_LAUNCH(launch_unpack_head2seq(brecv, pst, rld, 0, c.c, c.Hq, d, p, eb,
+                                             (uint8_t*)dq + (size_t)j * c.c * c.Hq * d * eb, ctx->s_comm));
+    FPDT_CHECK_LAUNCH(launch_unpack_head2seq(brecv, pst, rld, hq, c.c, c.Hkv, d, p, eb,
+                                             (uint8_t*)dk + (size_t)j * c.c * c.Hkv * d * eb, ctx->s_comm));
+    FPDT_CHECK_LAUNCH(launch_unpack_head2seq(brecv, pst, rld, hq + hkv, c.c, c.Hkv, d, p, eb,
+                                             (uint8_t*)dv + (size_t)j * c.c * c.Hkv * d * eb, ctx->s_comm));
+    ctx->stats.kernel_launches += 3;
+    rec(ctx->ev_comm_done, ctx->s_comm);
+    wait(cs, ctx->ev_comm_done);  // bsend / brecv reuse by the next outer iteration
+  };
+  auto set_kv_out = [&](BwdArgs& a, int64_t j) {
+    if (p == 1) {
+      a.dk_out = (uint8_t*)dk + (size_t)j * C * c.Hkv * d * eb;
+      a.dv_out = (uint8_t*)dv + (size_t)j * C * c.Hkv * d * eb;
+      a.kv_out_ld = (int64_t)c.Hkv * d;
+      a.kv_out_head0 = 0;
+    } else {
+      a.dk_out = bsend;
+      a.dv_out = bsend + (size_t)hkv * d * eb;
+      a.kv_out_ld = (int64_t)hcomb * d;
+      a.kv_out_head0 = hq;  // heads [hq, hq+hkv) for dk; the dv pointer is pre-offset by hkv heads
+    }
+  };
+
+  if (!c.offload) {
+    // resident: one launch per outer j over the query range [jC, S)
+    float* dq_dev = (float*)dev(ctx, B_DQDEV, (size_t)c.S * hq * d * 4);
+    FPDT_CHECK_CUDA(cudaMemsetAsync(dq_dev, 0, (size_t)c.S * hq * d * 4, cs));
+    HeadView qv, kv, vv;
+    if (p == 1) {
+      qv = {ctx->saved_q, c.S, hq, 0};
+      kv = {ctx->saved_k, c.S, hkv, 0};
+      vv = {ctx->saved_v, c.S, hkv, 0};
+    } else {
+      uint8_t* store = (uint8_t*)ctx->bufs[B_STORE].ptr;
+      qv = {store, c.S, hcomb, 0};
+      kv = {store, c.S, hcomb, hq};
+      vv = {store, c.S, hcomb, hq + hkv};
+    }
+    for (int64_t j = 0; j < u; ++j) {
+      BwdArgs a;
+      a.q = qv; a.k = kv; a.v = vv;
+      a.dout = {do_h, do_rows, do_heads, do_head0};
+      a.q_row0 = j * C;
+      a.kv_row0 = j * C;
+      a.n_q_rows = (int)(c.S - j * C);
+      a.n_kv_rows = (int)C;
+      a.q_pos0 = j * C;
+      a.kv_pos0 = j * C;
+      a.causal = 1;
+      a.hq = hq;
+      a.G = c.G;
+      a.scale = c.scale;
+      a.scale_log2 = sl2;
+      a.lse2 = lse_save + j * C;
+      a.Dstat = Dh + j * C;
+      a.stat_ld = c.S;
+      a.dq_acc = dq_dev + (size_t)j * C * hq * d;
+      a.dk_acc = dk_acc;
+      a.dv_acc = dv_acc;
+      a.kv_acc_init = 1;
+      a.kv_final = 1;
+      set_kv_out(a, j);
+      launch_bwd(ctx, c, a, cs);
+      emit_dq(j, dq_dev + (size_t)j * C * hq * d);
+      send_back(j);
+    }
+  } else {
+    uint8_t* kvs[2] = {(uint8_t*)dev(ctx, B_KVSLOT0, (size_t)C * row_kv2), (uint8_t*)dev(ctx, B_KVSLOT1, (size_t)C * row_kv2)};
+    uint8_t* qs[2] = {(uint8_t*)dev(ctx, B_QSLOT0, (size_t)C * row_q), (uint8_t*)dev(ctx, B_QSLOT1, (size_t)C * row_q)};
+    uint8_t* dos[2] = {(uint8_t*)dev(ctx, B_DOSLOT0, (size_t)C * row_q), (uint8_t*)dev(ctx, B_DOSLOT1, (size_t)C * row_q)};
+    float* dqs[2] = {(float*)dev(ctx, B_DQSLOT0, (size_t)C * hq * d * 4), (float*)dev(ctx, B_DQSLOT1, (size_t)C * hq * d * 4)};
+    for (int b = 0; b < 2; ++b) {
+      rec(ctx->ev_kv_free[b], cs);
+      rec(ctx->ev_q_free[b], cs);
+    }
+    int step = 0;
+    for (int64_t j = 0; j < u; ++j) {
+      const int ks = (int)(j & 1);
+      // B3: fetch kv_j
+      wait(ctx->s_h2d, ctx->ev_kv_free[ks]);
+      h2d(ctx, kvs[ks], ctx->host + hl.kv(j, u), (size_t)C * row_kv2);
+      rec(ctx->ev_kv_filled[ks], ctx->s_h2d);
+      wait(cs, ctx->ev_kv_filled[ks]);
+      for (int64_t i = j; i < u; ++i, ++step) {
+        const int sl = step & 1;
+        // B4: fetch q_i, dO_i and (j > 0) the dq partial of chunk i
+        wait(ctx->s_h2d, ctx->ev_q_free[sl]);
+        wait(ctx->s_h2d, ctx->ev_doff[i]);
+        h2d(ctx, qs[sl], ctx->host + hl.q(i), (size_t)C * row_q);
+        h2d(ctx, dos[sl], ctx->host + hl.dO(i, u), (size_t)C * row_q);
+        if (j > 0) {
+          wait(ctx->s_h2d, ctx->ev_dqoff[i]);
+          h2d(ctx, dqs[sl], ctx->host + hl.dq(i, u), (size_t)C * hq * d * 4);
+        }
+        rec(ctx->ev_q_filled[sl], ctx->s_h2d);
+        wait(cs, ctx->ev_q_filled[sl]);
+        if (j == 0) FPDT_CHECK_CUDA(cudaMemsetAsync(dqs[sl], 0, (size_t)C * hq * d * 4, cs));
+        BwdArgs a;
+        a.q = {qs[sl], C, hq, 0};
+        a.dout = {dos[sl], C, hq, 0};
+        a.k = {kvs[ks], C, 2 * hkv, 0};
+        a.v = {kvs[ks], C, 2 * hkv, hkv};
+        a.q_row0 = 0;
+        a.kv_row0 = 0;
+        a.n_q_rows = (int)C;
+        a.n_kv_rows = (int)C;
+        a.q_pos0 = i * C;
+        a.kv_pos0 = j * C;
+        a.causal = 1;
+        a.hq = hq;
+        a.G = c.G;
+        a.scale = c.scale;
+        a.scale_log2 = sl2;
+        a.lse2 = lse_save + i * C;
+        a.Dstat = Dh + i * C;
+        a.stat_ld = c.S;
+        a.dq_acc = dqs[sl];
+        a.dk_acc = dk_acc;
+        a.dv_acc = dv_acc;
+        a.kv_acc_init = (i == j);
+        a.kv_final = (i == u - 1);
+        set_kv_out(a, j);
+        launch_bwd(ctx, c, a, cs);
+        if (i == j) {
+          // B6: dq_j is final after its last contribution (inner iteration i == j)
+          emit_dq(j, dqs[sl]);
+          rec(ctx->ev_q_free[sl], cs);
+        } else {
+          // B6: write the dq partial back to the host store
+          rec(ctx->ev_dq_ready[sl], cs);
+          wait(ctx->s_d2h, ctx->ev_dq_ready[sl]);
+          d2h(ctx, ctx->host + hl.dq(i, u), dqs[sl], (size_t)C * hq * d * 4);
+          rec(ctx->ev_dqoff[i], ctx->s_d2h);
+          rec(ctx->ev_q_free[sl], ctx->s_d2h);
+        }
+      }
+      send_back(j);  // dk_j, dv_j are final after the last inner iteration
+      rec(ctx->ev_kv_free[ks], cs);
+    }
+  }
+  rec(ctx->ev_d2h_done, ctx->s_d2h);
+  wait(cs, ctx->ev_d2h_done);
+  rec(ctx->ev_h2d_done, ctx->s_h2d);
+  wait(cs, ctx->ev_h2d_done);
+}
+
+}  // namespace
+
+// ============================================================================================ C ABI
+
+namespace {
+int run(const std::function<void()>& f) {
+  try {
+    f();
+    return FPDT_OK;
+  } catch (const Fail& e) {
+    return e.code;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return FPDT_ERR_CUDA;
+  }
+}
+}  // namespace
+
+extern "C" {
+
+const char* fpdt_last_error(void) { return g_last_error.c_str(); }
+
+int64_t fpdt_global_token(int64_t local_t, int64_t chunk_size, int world_size, int rank) {
+  const int64_t c = chunk_size / world_size;
+  return ((local_t / c) * world_size + rank) * c + (local_t % c);
+}
+
+int fpdt_get_unique_id(unsigned char id[128]) {
+  return run([&] {
+    if (!id) fail(FPDT_ERR_ARG, "null id");
+    ncclUniqueId u;
+    FPDT_CHECK_NCCL(ncclGetUniqueId(&u));
+    static_assert(sizeof(u.internal) == 128, "nccl id size");
+    std::memcpy(id, u.internal, 128);
+  });
+}
+
+int fpdt_ctx_create(int world_size, int rank, const unsigned char* nccl_id, int device, size_t host_arena_bytes,
+                    fpdt_ctx** out) {
+  return run([&] {
+    if (!out || world_size < 1 || rank < 0 || rank >= world_size) fail(FPDT_ERR_ARG, "bad world_size/rank/out");
+    if (world_size > 1 && !nccl_id) fail(FPDT_ERR_ARG, "nccl_id required for world_size > 1");
+    FPDT_CHECK_CUDA(cudaSetDevice(device));
+    fpdt_ctx* ctx = new fpdt_ctx();
+    ctx->p = world_size;
+    ctx->rank = rank;
+    ctx->device = device;
+    int lo = 0, hi = 0;
+    FPDT_CHECK_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    FPDT_CHECK_CUDA(cudaStreamCreateWithPriority(&ctx->s_comm, cudaStreamNonBlocking, hi));
+    FPDT_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
+    FPDT_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
+    cudaEvent_t* evs[] = {&ctx->ev_enter, &ctx->ev_o_ready, &ctx->ev_comm_done, &ctx->ev_d2h_done, &ctx->ev_h2d_done,
+                          &ctx->ev_tmp};
+    for (auto e : evs) FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (int b = 0; b < 2; ++b) {
+      cudaEvent_t* pe[] = {&ctx->ev_slot_free[b], &ctx->ev_slot_filled[b], &ctx->ev_q_free[b], &ctx->ev_q_filled[b],
+                           &ctx->ev_dq_ready[b], &ctx->ev_kv_free[b], &ctx->ev_kv_filled[b], &ctx->ev_recv_used_c[b],
+                           &ctx->ev_recv_used_d[b]};
+      for (auto e : pe) FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    }
+    if (world_size > 1) {
+      ncclUniqueId u;
+      std::memcpy(u.internal, nccl_id, 128);
+      FPDT_CHECK_NCCL(ncclCommInitRank(&ctx->comm, world_size, u, rank));
+    }
+    if (host_arena_bytes) ensure_host(ctx, host_arena_bytes);
+    *out = ctx;
+  });
+}
+
+int fpdt_ctx_destroy(fpdt_ctx* ctx) {
+  if (!ctx) return FPDT_OK;
+  int rc = run([&] {
+    cudaSetDevice(ctx->device);
+    cudaDeviceSynchronize();
+    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    for (auto& b : ctx->bufs)
+      if (b.ptr) cudaFree(b.ptr);
+    if (ctx->host) cudaFreeHost(ctx->host);
+    for (auto v : {&ctx->ev_off, &ctx->ev_doff, &ctx->ev_dqoff, &ctx->ev_a2a})
+      for (auto e : *v) cudaEventDestroy(e);
+    for (auto& pr : ctx->t_fwd) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
+    for (auto& pr : ctx->t_bwd) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
+    cudaStreamDestroy(ctx->s_comm);
+    cudaStreamDestroy(ctx->s_h2d);
+    cudaStreamDestroy(ctx->s_d2h);
+  });
+  delete ctx;
+  return rc;
+}
+
+int fpdt_attn_fwd(fpdt_ctx* ctx, const void* q, const void* k, const void* v, void* o, float* lse, int64_t s_local,
+                  int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
+                  int dtype, int offload, float softmax_scale, void* stream) {
+  return run([&] {
+    if (!ctx || !q || !k || !v || !o) fail(FPDT_ERR_ARG, "null pointer argument");
+    if (world_size != ctx->p) fail(FPDT_ERR_ARG, "world_size differs from the context's");
+    Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
+                           softmax_scale);
+    FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
+    ctx->fwd_done = false;
+    forward(ctx, c, q, k, v, o, lse, static_cast<cudaStream_t>(stream));
+    ctx->saved = c;
+    ctx->saved_q = q;
+    ctx->saved_k = k;
+    ctx->saved_v = v;
+    ctx->fwd_done = true;
+  });
+}
+
+int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void* dk, void* dv, int64_t s_local,
+                  int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
+                  int dtype, int offload, float softmax_scale, void* stream) {
+  return run([&] {
+    if (!ctx || !o || !dout || !dq || !dk || !dv) fail(FPDT_ERR_ARG, "null pointer argument");
+    if (world_size != ctx->p) fail(FPDT_ERR_ARG, "world_size differs from the context's");
+    Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
+                           softmax_scale);
+    if (!ctx->fwd_done) fail(FPDT_ERR_STATE, "fpdt_attn_bwd without a preceding fpdt_attn_fwd on this context");
+    if (!(c == ctx->saved)) fail(FPDT_ERR_STATE, "backward arguments differ from the saved forward's");
+    FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
+    backward(ctx, c, o, dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fpdt_get_stats(const fpdt_ctx* ctx, fpdt_stats* out) {
+  if (!ctx || !out) return FPDT_ERR_ARG;
+  *out = ctx->stats;
+  return FPDT_OK;
+}
+
+int fpdt_set_kernel_timing(fpdt_ctx* ctx, int enable) {
+  if (!ctx) return FPDT_ERR_ARG;
+  ctx->timing = enable != 0;
+  return FPDT_OK;
+}
+
+int fpdt_kernel_time(fpdt_ctx* ctx, double* fwd_ms, int64_t* fwd_launches, double* bwd_ms, int64_t* bwd_launches,
+                     int reset) {
+  return run([&] {
+    if (!ctx) fail(FPDT_ERR_ARG, "null ctx");
+    double f = 0, b = 0;
+    for (size_t i = 0; i < ctx->n_fwd; ++i) {
+      float ms = 0;
+      FPDT_CHECK_CUDA(cudaEventSynchronize(ctx->t_fwd[i].second));
+      FPDT_CHECK_CUDA(cudaEventElapsedTime(&ms, ctx->t_fwd[i].first, ctx->t_fwd[i].second));
+      f += ms;
+    }
+    for (size_t i = 0; i < ctx->n_bwd; ++i) {
+      float ms = 0;
+      FPDT_CHECK_CUDA(cudaEventSynchronize(ctx->t_bwd[i].second));
+      FPDT_CHECK_CUDA(cudaEventElapsedTime(&ms, ctx->t_bwd[i].first, ctx->t_bwd[i].second));
+      b += ms;
+    }
+    if (fwd_ms) *fwd_ms = f;
+    if (bwd_ms) *bwd_ms = b;
+    if (fwd_launches) *fwd_launches = (int64_t)ctx->n_fwd;
+    if (bwd_launches) *bwd_launches = (int64_t)ctx->n_bwd;
+    if (reset) ctx->n_fwd = ctx->n_bwd = 0;
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,160 @@
+"""Python binding of libfpdt (include/fpdt.h): argument marshalling only.
+
+Every step of the FPDT attention path runs inside libfpdt.so (CUDA kernels for sm_100a, NCCL,
+cudaMemcpyAsync); this module only turns torch tensors into device pointers and raises on a non-OK
+status.  There is no fallback: a missing library raises ``FpdtLibraryMissing``.
+"""
+from __future__ import annotations
+
+import ctypes
+
+from . import _lib
+from ._lib import c_float, c_int, c_int64, c_void_p
+
+FPDT_OK, FPDT_ERR_ARG, FPDT_ERR_DIVISIBILITY, FPDT_ERR_UNSUPPORTED, FPDT_ERR_HOST_OOM, FPDT_ERR_DEVICE_OOM, \
+    FPDT_ERR_STATE, FPDT_ERR_CUDA, FPDT_ERR_NCCL = range(9)
+FPDT_BF16, FPDT_FP32 = 0, 1
+STATUS_NAMES = {0: "FPDT_OK", 1: "FPDT_ERR_ARG", 2: "FPDT_ERR_DIVISIBILITY", 3: "FPDT_ERR_UNSUPPORTED",
+                4: "FPDT_ERR_HOST_OOM", 5: "FPDT_ERR_DEVICE_OOM", 6: "FPDT_ERR_STATE", 7: "FPDT_ERR_CUDA",
+                8: "FPDT_ERR_NCCL"}
+
+# names of every symbol include/fpdt.h declares (checked by the CPU tests against the built library)
+EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_attn_fwd", "fpdt_attn_bwd",
+            "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
+            "fpdt_selftest_umma")
+
+
+class FpdtError(RuntimeError):
+    def __init__(self, code: int, msg: str):
+        super().__init__(f"{STATUS_NAMES.get(code, code)}: {msg}")
+        self.code = code
+
+
+class Stats(ctypes.Structure):
+    _fields_ = [("bytes_h2d", c_int64), ("bytes_d2h", c_int64), ("bytes_a2a", c_int64),
+                ("kernel_launches", c_int64), ("attn_launches", c_int64), ("fetch_slots_highwater", c_int64),
+                ("host_arena_bytes", c_int64), ("device_bytes", c_int64)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
+def _declare(lib):
+    P = c_void_p
+    lib.fpdt_get_unique_id.argtypes = [ctypes.c_char_p]
+    lib.fpdt_get_unique_id.restype = c_int
+    lib.fpdt_ctx_create.argtypes = [c_int, c_int, ctypes.c_char_p, c_int, ctypes.c_size_t, ctypes.POINTER(P)]
+    lib.fpdt_ctx_create.restype = c_int
+    lib.fpdt_ctx_destroy.argtypes = [P]
+    lib.fpdt_ctx_destroy.restype = c_int
+    lib.fpdt_attn_fwd.argtypes = [P, P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int64, c_int, c_int, c_int,
+                                  c_float, P]
+    lib.fpdt_attn_fwd.restype = c_int
+    lib.fpdt_attn_bwd.argtypes = [P, P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int64, c_int, c_int, c_int,
+                                  c_float, P]
+    lib.fpdt_attn_bwd.restype = c_int
+    lib.fpdt_last_error.argtypes = []
+    lib.fpdt_last_error.restype = ctypes.c_char_p
+    lib.fpdt_global_token.argtypes = [c_int64, c_int64, c_int, c_int]
+    lib.fpdt_global_token.restype = c_int64
+    lib.fpdt_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
+    lib.fpdt_get_stats.restype = c_int
+    lib.fpdt_set_kernel_timing.argtypes = [P, c_int]
+    lib.fpdt_set_kernel_timing.restype = c_int
+    lib.fpdt_kernel_time.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int64),
+                                     ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int64), c_int]
+    lib.fpdt_kernel_time.restype = c_int
+    lib.fpdt_selftest_umma.argtypes = [c_int, c_int, P, P, c_int, c_int, P, P]
+    lib.fpdt_selftest_umma.restype = c_int
+
+
+def lib():
+    return _lib.load()
+
+
+def _check(rc: int):
+    if rc != FPDT_OK:
+        raise FpdtError(rc, lib().fpdt_last_error().decode())
+
+
+def _ptr(t):
+    return None if t is None else c_void_p(t.data_ptr())
+
+
+def _stream(stream):
+    if stream is None:
+        import torch
+        stream = torch.cuda.current_stream()
+    return c_void_p(stream.cuda_stream if hasattr(stream, "cuda_stream") else int(stream))
+
+
+def fpdt_get_unique_id() -> bytes:
+    buf = ctypes.create_string_buffer(128)
+    _check(lib().fpdt_get_unique_id(buf))
+    return buf.raw
+
+
+def fpdt_global_token(local_t: int, chunk_size: int, world_size: int, rank: int) -> int:
+    return lib().fpdt_global_token(local_t, chunk_size, world_size, rank)
+
+
+class FPDTContext:
+    """Owns one fpdt_ctx (NCCL comm, streams, pinned host chunk store, device slots, saved state)."""
+
+    def __init__(self, world_size: int = 1, rank: int = 0, nccl_id: bytes | None = None, device: int = 0,
+                 host_arena_bytes: int = 0):
+        self.world_size, self.rank = world_size, rank
+        h = c_void_p()
+        _check(lib().fpdt_ctx_create(world_size, rank, nccl_id, device, host_arena_bytes, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _check(lib().fpdt_ctx_destroy(self.handle))
+            self.handle = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def stats(self) -> dict:
+        s = Stats()
+        _check(lib().fpdt_get_stats(self.handle, ctypes.byref(s)))
+        return s.as_dict()
+
+    def set_kernel_timing(self, enable: bool):
+        _check(lib().fpdt_set_kernel_timing(self.handle, int(enable)))
+
+    def kernel_time(self, reset: bool = True):
+        f, b = ctypes.c_double(), ctypes.c_double()
+        nf, nb = c_int64(), c_int64()
+        _check(lib().fpdt_kernel_time(self.handle, ctypes.byref(f), ctypes.byref(nf), ctypes.byref(b),
+                                      ctypes.byref(nb), int(reset)))
+        return f.value, nf.value, b.value, nb.value
+
+
+def fpdt_attn_fwd(ctx: FPDTContext, q, k, v, o, lse, s_local: int, n_q_heads: int, n_kv_heads: int, head_dim: int,
+                  causal: int, chunk_size: int, world_size: int, dtype: int, offload: int,
+                  softmax_scale: float = 0.0, stream=None):
+    _check(lib().fpdt_attn_fwd(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), s_local, n_q_heads,
+                               n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload, softmax_scale,
+                               _stream(stream)))
+
+
+def fpdt_attn_bwd(ctx: FPDTContext, o, dout, dq, dk, dv, s_local: int, n_q_heads: int, n_kv_heads: int,
+                  head_dim: int, causal: int, chunk_size: int, world_size: int, dtype: int, offload: int,
+                  softmax_scale: float = 0.0, stream=None):
+    _check(lib().fpdt_attn_bwd(ctx.handle, _ptr(o), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), s_local, n_q_heads,
+                               n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload, softmax_scale,
+                               _stream(stream)))
+
+
+def dtype_code(torch_dtype) -> int:
+    import torch
+    if torch_dtype == torch.bfloat16:
+        return FPDT_BF16
+    if torch_dtype == torch.float32:
+        return FPDT_FP32
+    raise FpdtError(FPDT_ERR_UNSUPPORTED, f"dtype {torch_dtype}")

@@ -1,0 +1,54 @@
+"""Shared helpers for the GPU parity tests: run the CUDA path through the C-ABI binding, compare with the
+oracle by the normwise max relative error of SURVEY §8(c) c.4."""
+from __future__ import annotations
+
+import numpy as np
+import torch
+
+import fpdt_inputs as gen
+from oracle import attention
+
+TOL = {"bf16": 1e-2, "fp32": 1e-4}   # north_star: 1e-2 for bf16 I/O with fp32 accumulation, 1e-4 fp32 mode
+
+
+def rel_err(x, ref) -> float:
+    x = np.asarray(x, np.float64)
+    ref = np.asarray(ref, np.float64)
+    return float(np.abs(x - ref).max() / max(np.abs(ref).max(), 1e-30))
+
+
+def run_cuda(x: dict, chunk: int, dtype: str, offload: int, ctx=None, want_grad: bool = True):
+    """x: numpy q, k, v, do (bf16-representable fp32 values), sequence layout, world_size 1."""
+    from paper_2408_16978_b200 import fpdt
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    q, k, v, do = (torch.tensor(x[n]).to(tdt).cuda().contiguous() for n in ("q", "k", "v", "do"))
+    S, Hq, d = q.shape
+    Hkv = k.shape[1]
+    own = ctx is None
+    if own:
+        ctx = fpdt.FPDTContext()
+    o = torch.empty_like(q)
+    lse = torch.empty(S, Hq, dtype=torch.float32, device="cuda")
+    code = fpdt.dtype_code(tdt)
+    fpdt.fpdt_attn_fwd(ctx, q, k, v, o, lse, S, Hq, Hkv, d, 1, chunk, 1, code, offload)
+    out = {"o": o, "lse": lse}
+    if want_grad:
+        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+        fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, S, Hq, Hkv, d, 1, chunk, 1, code, offload)
+        out.update(dq=dq, dk=dk, dv=dv)
+    torch.cuda.synchronize()
+    res = {n: t.float().cpu().numpy() for n, t in out.items()}
+    res["stats"] = ctx.stats()
+    if own:
+        ctx.close()
+    return res
+
+
+def oracle_full(x: dict):
+    o, lse = attention.attention_forward(x["q"], x["k"], x["v"])
+    dq, dk, dv = attention.attention_backward(x["q"], x["k"], x["v"], o, lse, x["do"])
+    return {"o": o, "lse": lse, "dq": dq, "dk": dk, "dv": dv}
+
+
+def inputs(dist, seed, S, Hq, Hkv, d):
+    return gen.make_inputs(dist, seed, S, Hq, Hkv, d)
