@@ -1,0 +1,359 @@
+#!/usr/bin/env python
+"""FPDT chunked, sequence-parallel causal attention fwd+bwd on B200: the BASELINE.json headline.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference] [--offload 0|1]
+    torchrun --nproc-per-node N --master-addr 127.0.0.1 bench.py --gpus N ...     (N > 1)
+
+Workload (BASELINE.json configs[1]): GPT-2.7B-shaped attention layer, 32 heads, head_dim 80, global
+sequence S = 524,288 tokens, chunk 65,536 (u = 8 / p chunks per rank), bf16, causal, one process per GPU,
+Ulysses all-to-all per chunk for N > 1 (strong scaling: S fixed, s_local = S / N), KV chunks offloaded to
+pinned host memory and prefetched back double-buffered (the paper's FPDT with offloading).
+A step = fpdt_attn_fwd + fpdt_attn_bwd over the whole sequence.  Inputs are synthetic (the seeded
+counter-based generator, distribution "normal"), resident in HBM; every input tensor is 2.7 GB (> 126 MB
+L2), so no L2 flush is needed between steps.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md "Measurement" for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "chunked attn fwd+bwd TFLOPS/GPU & tokens/s at 1/2/4/8 B200 vs bf16 peak"
+WORKLOAD = dict(name="GPT-2.7B-shaped causal attention layer (BASELINE.json configs[1])", S=524288, Hq=32, Hkv=32,
+                d=80, C=65536, dtype="bf16")
+
+
+def flops_per_step(S, Hq, d):
+    pairs = S * (S + 1) / 2  # causal (query, key) pairs incl. the diagonal
+    return 4 * d * Hq * pairs, 10 * d * Hq * pairs  # fwd (QK^T, PV), bwd (recompute QK^T, dP, dV, dK, dQ)
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            p = json.load(f)
+        return p.get("bf16_tflops"), p.get("bf16_tflops_sustained"), p.get("hbm_gbs"), "measured (MEASURED_PEAKS.json)"
+    return 1590.0, 1400.0, 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled DURING the timed region (B200_PROFILING.md)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.samples = []
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except FileNotFoundError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) >= 7:
+                self.samples.append(parts)
+
+    def stop(self):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except Exception:
+                self.proc.kill()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        if not self.samples:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        sm = [float(s[0]) for s in self.samples if s[0].replace(".", "").isdigit()]
+        mx = [float(s[1]) for s in self.samples if s[1].replace(".", "").isdigit()]
+        reasons = sorted({names[i] for s in self.samples for i in range(4) if s[3 + i].lower() == "active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.samples)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+# ------------------------------------------------------------------------------------------------ CPU oracle
+def oracle_sample(S_sample=4096, heads=2, d=80, seed=0):
+    """One bounded sample of the workload through the fp64 oracle (plain definition, fwd + bwd):
+    the first S_sample tokens of `heads` heads.  Returns (seconds, algorithmic FLOPs of the sample)."""
+    import fpdt_inputs as gen
+    from oracle import attention
+    x = gen.make_inputs("normal", seed, S_sample, heads, heads, d)
+    t0 = time.perf_counter()
+    o, lse = attention.attention_forward(x["q"], x["k"], x["v"])
+    attention.attention_backward(x["q"], x["k"], x["v"], o, lse, x["do"])
+    dt = time.perf_counter() - t0
+    f, b = flops_per_step(S_sample, heads, d)
+    return dt, f + b
+
+
+def cpu_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count()
+
+
+def projected_tokens_per_s(dt, sample_flops, S, Hq, d):
+    f, b = flops_per_step(S, Hq, d)
+    return S / (dt * (f + b) / sample_flops)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    W = WORKLOAD
+    S, Hq, d = W["S"], W["Hq"], W["d"]
+    sample = dict(S_sample=4096, heads=2, d=d)
+    for _ in range(args.warmup):
+        oracle_sample(**sample)
+    times, fl = [], None
+    for _ in range(args.steps):
+        dt, fl = oracle_sample(**sample)
+        times.append(dt)
+    t = sum(times) / len(times)
+    value = projected_tokens_per_s(t, fl, S, Hq, d)
+    desc = (f"fp64 numpy oracle (oracle/attention.py), fwd+bwd of the first {sample['S_sample']} tokens x "
+            f"{sample['heads']} heads (d={d}) per step; projected to the full workload by algorithmic FLOPs")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": "tokens/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": t * 1e3, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "config": {"workload": W["name"], "S": S, "heads": Hq, "head_dim": d, "chunk": W["C"]},
+            "cpu_baseline": {"value": value, "unit": "tokens/s", "cores": cpu_cores(), "kind": "oracle",
+                             "sample": desc},
+            "e2e": {"value": value, "unit": "tokens/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ------------------------------------------------------------------------------------------------ ours
+def run_ours(args):
+    import ctypes
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2408_16978_b200 import _lib, fpdt
+    import fpdt_inputs as gen
+
+    rank, world, local = dist_env()
+    assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+    W = WORKLOAD
+    S, Hq, Hkv, d, C = W["S"], W["Hq"], W["Hkv"], W["d"], W["C"]
+    if args.seq:
+        S = args.seq
+    if args.chunk:
+        C = args.chunk
+    s_local = S // world
+    offload = args.offload
+
+    # NCCL id through torch.distributed (plumbing only)
+    nid = None
+    if world > 1:
+        obj = [fpdt.fpdt_get_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        nid = obj[0]
+    ctx = fpdt.FPDTContext(world, rank, nid, local)
+    genlib = _lib.load_generator()
+    bf = torch.bfloat16
+
+    def gen_tensor(name, H):
+        t = torch.empty(s_local, H, d, dtype=bf, device="cuda")
+        rc = genlib.fpdt_gen_fill(ctypes.c_void_p(t.data_ptr()), 0, gen.TENSOR_IDS[name], gen.DIST_IDS["normal"],
+                                  0, s_local, H, d, S, rank, world, C, ctypes.c_void_p(0))
+        assert rc == 0
+        return t
+
+    q, k, v, do = gen_tensor("q", Hq), gen_tensor("k", Hkv), gen_tensor("v", Hkv), gen_tensor("do", Hq)
+    o = torch.empty_like(q)
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        fpdt.fpdt_attn_fwd(ctx, q, k, v, o, None, s_local, Hq, Hkv, d, 1, C, world, fpdt.FPDT_BF16, offload,
+                           0.0, stream)
+        fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, s_local, Hq, Hkv, d, 1, C, world, fpdt.FPDT_BF16, offload,
+                           0.0, stream)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    def max_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([x], dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---------------------------------------------------------------- device-timed region
+    ctx.set_kernel_timing(True)
+    ctx.kernel_time(reset=True)
+    st0 = ctx.stats()
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.5)
+    torch.cuda.synchronize()
+    barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    wall0 = time.perf_counter()
+    e0.record(stream)
+    for _ in range(args.steps):
+        step()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    barrier()
+    wall = time.perf_counter() - wall0
+    clocks = sampler.stop()
+    st1 = ctx.stats()
+    fwd_ms, n_fwd, bwd_ms, n_bwd = ctx.kernel_time(reset=True)
+    ctx.set_kernel_timing(False)
+    ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
+    launches = (st1["kernel_launches"] - st0["kernel_launches"]) // args.steps
+    h2d_lib = (st1["bytes_h2d"] - st0["bytes_h2d"]) // args.steps
+    d2h_lib = (st1["bytes_d2h"] - st0["bytes_d2h"]) // args.steps
+
+    f_fwd, f_bwd = flops_per_step(S, Hq, d)
+    tokens_per_s = S / (ms / 1e3)
+    tflops_gpu = (f_fwd + f_bwd) / (world * ms / 1e3) / 1e12
+    burst, sustained, hbm, peak_src = load_peaks()
+
+    # dominant kernel = the backward pair kernel (10d of the 14d FLOPs per pair); algorithmic FLOPs per launch
+    # = (bwd FLOPs of a step / launches per step), timed by CUDA events on its launch stream inside the steps
+    bwd_launch_ms = bwd_ms / max(n_bwd, 1)
+    fwd_launch_ms = fwd_ms / max(n_fwd, 1)
+    bwd_flops_launch = f_bwd / world / max(n_bwd // args.steps, 1)
+    fwd_flops_launch = f_fwd / world / max(n_fwd // args.steps, 1)
+    ach_bwd = bwd_flops_launch / (bwd_launch_ms / 1e3) / 1e12
+    ach_fwd = fwd_flops_launch / (fwd_launch_ms / 1e3) / 1e12
+    traffic = None
+    prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("attn_bwd_kernel_bytes_per_launch")
+
+    # ---------------------------------------------------------------- end to end (host buffers)
+    e2e = None
+    if not args.no_e2e:
+        hq_ = [torch.empty(t.shape, dtype=bf, pin_memory=True) for t in (q, k, v, do)]
+        for h_, t in zip(hq_, (q, k, v, do)):
+            h_.copy_(t)
+        outs_h = [torch.empty(t.shape, dtype=bf, pin_memory=True) for t in (o, dq, dk, dv)]
+        h2d_b = sum(t.numel() * 2 for t in hq_)
+        d2h_b = sum(t.numel() * 2 for t in outs_h)
+
+        def e2e_step():
+            for h_, t in zip(hq_, (q, k, v, do)):
+                t.copy_(h_, non_blocking=True)
+            step()
+            for h_, t in zip(outs_h, (o, dq, dk, dv)):
+                h_.copy_(t, non_blocking=True)
+
+        e2e_step()
+        torch.cuda.synchronize()
+        barrier()
+        a0, a1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        a0.record(stream)
+        for _ in range(args.steps):
+            e2e_step()
+        a1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        e2e_ms = max_over_ranks(a0.elapsed_time(a1) / args.steps)
+        e2e = {"value": S / (e2e_ms / 1e3), "unit": "tokens/s", "ms_per_step": e2e_ms,
+               "h2d_bytes_per_step": h2d_b, "d2h_bytes_per_step": d2h_b,
+               "path": "pinned host q,k,v,dO -> device, fpdt_attn_fwd + fpdt_attn_bwd (C-ABI), o,dq,dk,dv -> host"}
+
+    cpu = None
+    if rank == 0 and not args.no_cpu_baseline:
+        dt, fl = oracle_sample(S_sample=8192)
+        cpu = {"value": projected_tokens_per_s(dt, fl, S, Hq, d), "unit": "tokens/s", "cores": cpu_cores(),
+               "kind": "oracle", "seconds": dt,
+               "sample": "fp64 numpy oracle (oracle/attention.py) fwd+bwd of the first 8192 tokens x 2 heads "
+                         "(d=80); tokens/s projected to the full workload by algorithmic FLOPs"}
+
+    line = {
+        "metric": METRIC, "value": tokens_per_s, "unit": "tokens/s", "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True, "scaling": "strong",
+        "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded counter-based generator, normal)",
+        "tflops_per_gpu": tflops_gpu,
+        "frac_of_peak": tflops_gpu / sustained,
+        "config": {"workload": W["name"], "S": S, "heads_q": Hq, "heads_kv": Hkv, "head_dim": d, "chunk": C,
+                   "chunks": S // C, "s_local": s_local, "offload": offload, "causal": 1,
+                   "parallelism": f"ulysses-sp{world}", "l2": "inputs 2.7 GB/tensor >> 126 MB L2, no flush",
+                   "flops_per_step": f_fwd + f_bwd, "flop_convention": "14*d per causal pair per q-head"},
+        "roofline": {"bound": "tensor", "kernel": "attn_bwd_kernel (tcgen05 pair backward)",
+                     "achieved": ach_bwd, "peak": sustained, "unit": "TFLOP/s", "frac": ach_bwd / sustained,
+                     "traffic": traffic, "peak_source": peak_src + ", sustained bf16 (kernel timed inside a long step)",
+                     "launch_ms": bwd_launch_ms, "launches_per_step": n_bwd // args.steps,
+                     "fwd_kernel": {"achieved": ach_fwd, "frac": ach_fwd / sustained, "launch_ms": fwd_launch_ms,
+                                    "launches_per_step": n_fwd // args.steps},
+                     "kernel_share_of_step": (fwd_ms + bwd_ms) / args.steps / ms},
+        "clocks": clocks,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "pcie_bytes_per_step": {"h2d": h2d_lib, "d2h": d2h_lib},
+        "wall_s_timed": wall,
+        "cpu_baseline": cpu,
+    }
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=3)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--offload", type=int, default=1)
+    ap.add_argument("--seq", type=int, default=0, help="override S (testing)")
+    ap.add_argument("--chunk", type=int, default=0, help="override the chunk size (testing)")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())
