@@ -1,20 +1,29 @@
 // Backward chunk-pair attention for sm_100a (KV-stationary; tcgen05 + TMEM + TMA).
 //
 // One launch = one (key/value chunk j, query chunk i) step of FPDT's nested backward loop
-// (fig:bw_db: "The outer loop is on key and value, while the inner one is on query").
+// (fig:bw_db: "The outer loop is on key and value, while the inner one is on query"),
+// or, in the resident mode, key/value chunk j against the whole query range [jC, S).
 // A CTA owns one 128-row key/value tile of one KV head and walks the query tiles of the range and the
 // G query heads of its group; per (query tile, head) it computes:
 //   S^T  = K Q^T            P^T  = exp2(S^T*scale*log2e - lse2)       (recompute, no stored P)
 //   dP^T = V dO^T           dS^T = P^T o (dP^T - D)
-//   dV  += P^T dO           dK  += dS^T Q          dQ_partial = dS K  (added to fp32 dq_acc)
+//   dV  += P^T dO           dK  += dS^T Q          dQ_partial = dS K  (reduced into fp32 dq_acc)
 // dK/dV accumulate in TMEM across the whole walk and leave once per launch (accumulated across the
-// inner loop in fp32 HBM; final bf16 at the last inner step).
+// inner loop of the offloaded schedule in fp32 HBM; final bf16 at the last inner step).
 //
-// Warps: 0-3 softmax-gradient (thread = key row = TMEM lane), then dQ read-out (thread = query row)
-//        and the final dK/dV write; 4 TMA producer; 5 TMEM allocator + MMA issuer.
-// TMEM: S^T [0,128) -> P^T bf16 [0,64) + dS^T bf16 [64,128);  dP^T [128,256) -> dQ [128,128+D);
-//       dK [256,256+D);  dV [384,384+D).
-// smem: K, V (stationary), QS stages of {Q, dO, lse2[128], D[128]}, dS (MN-major 128B-swizzled, A of dQ).
+// Warps (448 threads):
+//   0-3   softmax-gradient, query columns [0,64)   (thread = key row = TMEM lane); final dK
+//   4-7   softmax-gradient, query columns [64,128)                                ; final dV
+//   8-11  dQ read-out (thread = query row) and reduction into dq_acc: TMA bulk reduce-add (D <= 80)
+//         or vector atomics (D = 128)
+//   12    TMA producer;  13  TMEM allocator + single-thread MMA issuer
+// TMEM: S^T [0,128) -> P^T bf16 [0,64) + dS^T bf16 [64,128);  dP^T [128,256);
+//       D <= 80: dQ [256,256+D), dK, dV next (496 columns at D = 80)  -> dP^T of the next tile can be
+//                issued before the current dQ is read out;
+//       D = 128: dQ aliases dP^T; dK [256,384); dV [384,512).
+// MMA issue order per tile n: dV_n, dK_n, S^T_{n+1}, dQ_n, dP^T_{n+1}: S^T_{n+1} overwrites P^T_n/dS^T_n
+// only after dV_n/dK_n in issue order (tcgen05 MMAs of one thread execute in order), so the next
+// tile's exponentials overlap the dQ_n/dP^T_{n+1} MMAs.
 #include "attn_tile.cuh"
 #include "kernels.h"
 #include "smem_layout.cuh"
@@ -25,24 +34,34 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 192;
+constexpr int kThreads = 448;
 
 template <int D>
 struct BwdCfg {
   using T = Tile<D>;
+  static constexpr bool kSepDQ = (D <= 80);
+  static constexpr bool kTmaDQ = (D <= 80);
   static constexpr int QS = 2;
-  static constexpr int kKV = 2 * T::kBytes;
-  static constexpr int kStage = 2 * T::kBytes;
+  static constexpr int kStage = 2 * T::kBytes;                 // Q + dO
   static constexpr int kDS = 128 * 128 * 2;
-  static constexpr int kStats = 2 * 512;
-  static constexpr int oK = 0, oV = T::kBytes, oStage = kKV, oDS = kKV + QS * kStage, oStats = oDS + kDS;
+  static constexpr int kDQ = kTmaDQ ? 128 * D * 4 : 0;
+  static constexpr int kStats = 1024;                          // lse2[128] + D[128]
+  static constexpr int oK = 0, oV = T::kBytes, oStage = 2 * T::kBytes;
+  static constexpr int oDS = oStage + QS * kStage;
+  static constexpr int oDQ = oDS + kDS;
+  static constexpr int oStats = oDQ + kDQ;
   static constexpr int oBars = oStats + QS * kStats;
-  static constexpr int kBars = 16 * 8;
-  static constexpr int kSmem = oBars + kBars + 16;
+  static constexpr int kSmem = oBars + 256;
+  // TMEM columns
+  static constexpr uint32_t tS = 0, tdP = 128;
+  static constexpr uint32_t tdQ = kSepDQ ? 256 : 128;
+  static constexpr uint32_t tdK = kSepDQ ? 256 + D : 256;
+  static constexpr uint32_t tdV = kSepDQ ? 256 + 2 * D : 384;
+  static_assert(!kSepDQ || 256 + 3 * D <= 512, "TMEM budget");
 };
 
 struct TmapSet {
-  CUtensorMap q_main, q_tail, k_main, k_tail, v_main, v_tail, o_main, o_tail;
+  CUtensorMap q_main, q_tail, k_main, k_tail, v_main, v_tail, o_main, o_tail, dq;
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -56,6 +75,16 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
                : "memory");
 }
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
@@ -66,16 +95,15 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
   extern __shared__ __align__(1024) uint8_t smem[];
   if ((smem_u32(smem) & 1023) != 0) __trap();
   const uint32_t base = smem_u32(smem);
-  const uint32_t sK = base + C::oK, sV = base + C::oV, sDS = base + C::oDS;
+  const uint32_t sK = base + C::oK, sV = base + C::oV, sDS = base + C::oDS, sDQ = base + C::oDQ;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::oBars);
-  // barrier slots
   const uint32_t b_kv = smem_u32(&bars[0]);
   auto b_qfull = [&](int s) { return smem_u32(&bars[1 + s]); };
   auto b_qempty = [&](int s) { return smem_u32(&bars[3 + s]); };
   const uint32_t b_s = smem_u32(&bars[5]), b_dp = smem_u32(&bars[6]), b_p = smem_u32(&bars[7]),
                  b_ds = smem_u32(&bars[8]), b_dsfree = smem_u32(&bars[9]), b_dqfull = smem_u32(&bars[10]),
                  b_dqempty = smem_u32(&bars[11]), b_kvdone = smem_u32(&bars[12]);
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::oBars + C::kBars);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::oBars + 16 * 8);
 
   const uint32_t warp = warp_id(), lane = lane_id();
   const int kt = blockIdx.x;
@@ -91,8 +119,8 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
   }
   const int n_iter = (n_qt_total - qt_first) * G;
 
-  if (warp == 5) tmem_alloc<512>(smem_u32(tmem_slot));
-  if (warp == 4 && lane == 0) {
+  if (warp == 13) tmem_alloc<512>(smem_u32(tmem_slot));
+  if (warp == 12 && lane == 0) {
     mbar_init(b_kv, 1);
     for (int s = 0; s < QS; ++s) {
       mbar_init(b_qfull(s), 1);
@@ -100,8 +128,8 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
     }
     mbar_init(b_s, 1);
     mbar_init(b_dp, 1);
-    mbar_init(b_p, 128);
-    mbar_init(b_ds, 128);
+    mbar_init(b_p, 256);
+    mbar_init(b_ds, 256);
     mbar_init(b_dsfree, 1);
     mbar_init(b_dqfull, 1);
     mbar_init(b_dqempty, 128);
@@ -113,7 +141,7 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 4) {
+  if (warp == 12) {
     // ------------------------------------------------------------------ producer
     if (elect_one() && n_iter > 0) {
       const uint64_t pol_kv = policy_evict_first(), pol_q = policy_evict_last();
@@ -136,7 +164,7 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
         bulk_load(stats + 512, a.Dstat + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, b_qfull(s));
       }
     }
-  } else if (warp == 5) {
+  } else if (warp == 13) {
     // ------------------------------------------------------------------ MMA issuer
     if (elect_one() && n_iter > 0) {
       const uint32_t idS = idesc_bf16(128, 128, 0, 0);           // S^T, dP^T: A,B K-major
@@ -144,25 +172,29 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
       const uint32_t idGt = idesc_bf16(128, 16, 0, 1);
       const uint32_t idQm = idesc_bf16(128, T::kMainN, 1, 1);    // dQ: A = dS MN-major smem, B = K MN-major
       const uint32_t idQt = idesc_bf16(128, 16, 1, 1);
-      const uint32_t tS = tmem, tdP = tmem + 128, tdK = tmem + 256, tdV = tmem + 384;
-      mbar_wait(b_kv, 0);
-      tc_fence_after();
-      for (int n = 0; n < n_iter; ++n) {
-        const int s = n % QS;
-        const uint32_t st = base + C::oStage + s * C::kStage;
-        const uint32_t sQ = st, sO = st + T::kBytes;
-        mbar_wait(b_qfull(s), (n / QS) & 1);
-        tc_fence_after();
+      const uint32_t tS = tmem + C::tS, tdP = tmem + C::tdP, tdQ = tmem + C::tdQ, tdK = tmem + C::tdK,
+                     tdV = tmem + C::tdV;
+      auto stage_q = [&](int n) { return base + C::oStage + (n % QS) * C::kStage; };
+      auto issue_S = [&](int n) {
+        const uint32_t sQ = stage_q(n);
 #pragma unroll
         for (int kk = 0; kk < T::kKSteps; ++kk) mma_ss(tS, T::desc_kmajor(sK, kk), T::desc_kmajor(sQ, kk), idS, kk > 0);
         mma_commit(b_s);
-        if (n > 0) {
-          mbar_wait(b_dqempty, (n - 1) & 1);
-          tc_fence_after();
-        }
+      };
+      auto issue_dP = [&](int n) {
+        const uint32_t sO = stage_q(n) + T::kBytes;
 #pragma unroll
         for (int kk = 0; kk < T::kKSteps; ++kk) mma_ss(tdP, T::desc_kmajor(sV, kk), T::desc_kmajor(sO, kk), idS, kk > 0);
         mma_commit(b_dp);
+      };
+      mbar_wait(b_kv, 0);
+      mbar_wait(b_qfull(0), 0);
+      tc_fence_after();
+      issue_S(0);
+      issue_dP(0);
+      for (int n = 0; n < n_iter; ++n) {
+        const int s = n % QS;
+        const uint32_t sQ = stage_q(n), sO = sQ + T::kBytes;
         // dV += P^T dO
         mbar_wait(b_p, n & 1);
         tc_fence_after();
@@ -173,7 +205,7 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
           for (int kk = 0; kk < 8; ++kk)
             mma_ts(tdV + T::kMainN, tS + kk * 8, T::desc_mn_tail(sO, kk), idGt, (n > 0 || kk > 0));
         }
-        // dK += dS^T Q ; dQ = dS K
+        // dK += dS^T Q
         mbar_wait(b_ds, n & 1);
         tc_fence_after();
 #pragma unroll
@@ -183,53 +215,69 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
           for (int kk = 0; kk < 8; ++kk)
             mma_ts(tdK + T::kMainN, tS + 64 + kk * 8, T::desc_mn_tail(sQ, kk), idGt, (n > 0 || kk > 0));
         }
+        mma_commit(b_qempty(s));  // Q_n / dO_n consumed (dQ reads dS and K only)
+        const bool more = n + 1 < n_iter;
+        if (more) {
+          mbar_wait(b_qfull((n + 1) % QS), ((n + 1) / QS) & 1);
+          tc_fence_after();
+          issue_S(n + 1);
+        }
+        // dQ_n = dS K  (its TMEM columns must have been read out for n-1)
+        if (n > 0) {
+          mbar_wait(b_dqempty, (n - 1) & 1);
+          tc_fence_after();
+        }
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_ss(tdP, desc_a_mn_sw128(sDS, kk), T::desc_mn_main(sK, kk), idQm, kk > 0);
+        for (int kk = 0; kk < 8; ++kk) mma_ss(tdQ, desc_a_mn_sw128(sDS, kk), T::desc_mn_main(sK, kk), idQm, kk > 0);
         if constexpr (T::kTail) {
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
-            mma_ss(tdP + T::kMainN, desc_a_mn_sw128(sDS, kk), T::desc_mn_tail(sK, kk), idQt, kk > 0);
+            mma_ss(tdQ + T::kMainN, desc_a_mn_sw128(sDS, kk), T::desc_mn_tail(sK, kk), idQt, kk > 0);
         }
         mma_commit(b_dqfull);
         mma_commit(b_dsfree);
-        mma_commit(b_qempty(s));
+        if (more) {
+          if constexpr (!C::kSepDQ) {  // dP^T aliases dQ: wait until dQ_n has been read out
+            mbar_wait(b_dqempty, n & 1);
+            tc_fence_after();
+          }
+          issue_dP(n + 1);
+        }
       }
       mma_commit(b_kvdone);
     }
-  } else {
+  } else if (warp < 8) {
     // ------------------------------------------------------------------ softmax gradient (key rows)
-    const int r = warp * 32 + lane;
-    const uint32_t lane_off = (warp * 32) << 16;
-    const uint32_t tS = tmem + lane_off, tdP = tmem + 128 + lane_off;
+    const int half = warp >> 2;  // query columns [64*half, 64*half+64)
+    const int r = (warp & 3) * 32 + lane;
+    const uint32_t lane_off = ((warp & 3) * 32) << 16;
+    const uint32_t tS = tmem + C::tS + lane_off, tdP = tmem + C::tdP + lane_off;
     const int64_t kpos = kv_base + r;
     const float sl2 = a.scale_log2;
     for (int n = 0; n < n_iter; ++n) {
       const int s = n % QS;
       const int qt = qt_first + n / G;
-      const float* lse2 = reinterpret_cast<const float*>(smem + C::oStats + s * C::kStats);
+      const float* lse2 = reinterpret_cast<const float*>(smem + C::oStats + s * C::kStats) + 64 * half;
       const float* Dq = lse2 + 128;
       mbar_wait(b_s, n & 1);
       tc_fence_after();
-      float p[128];
-      tmem_ld32(tS + 0, reinterpret_cast<uint32_t*>(p));
-      tmem_ld32(tS + 32, reinterpret_cast<uint32_t*>(p) + 32);
-      tmem_ld32(tS + 64, reinterpret_cast<uint32_t*>(p) + 64);
-      tmem_ld32(tS + 96, reinterpret_cast<uint32_t*>(p) + 96);
+      float p[64];
+      tmem_ld32(tS + 64 * half, reinterpret_cast<uint32_t*>(p));
+      tmem_ld32(tS + 64 * half + 32, reinterpret_cast<uint32_t*>(p) + 32);
       tmem_wait_ld();
-      // stats of this stage were delivered with the Q tile (bar_qfull), which the MMA warp waited on
-      // before issuing S^T; bar_s completing therefore implies they are in smem.
-      const int64_t lim = a.causal ? (kpos - (a.q_pos0 + (int64_t)qt * 128)) : -1;  // q index < lim masked
+      // query column index (within the tile) < lim is masked (query position < key position)
+      const int64_t lim = (a.causal ? (kpos - (a.q_pos0 + (int64_t)qt * 128)) : -1) - 64 * half;
 #pragma unroll
-      for (int i = 0; i < 128; ++i) {
+      for (int i = 0; i < 64; ++i) {
         const float v = ex2(fmaf(p[i], sl2, -lse2[i]));
         p[i] = (i < lim) ? 0.f : v;
       }
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) {
+      for (int c = 0; c < 64; c += 32) {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) pk[i / 2] = pack_bf16x2(p[c + i], p[c + i + 1]);
-        tmem_st16(tS + c / 2, pk);
+        tmem_st16(tS + 32 * half + c / 2, pk);
       }
       tmem_wait_st();
       tc_fence_before();
@@ -238,9 +286,9 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
       if (n > 0) mbar_wait(b_dsfree, (n - 1) & 1);
       tc_fence_after();
 #pragma unroll
-      for (int c = 0; c < 128; c += 32) {
+      for (int c = 0; c < 64; c += 32) {
         float dp[32];
-        tmem_ld32(tdP + c, reinterpret_cast<uint32_t*>(dp));
+        tmem_ld32(tdP + 64 * half + c, reinterpret_cast<uint32_t*>(dp));
         tmem_wait_ld();
         uint32_t pk[16];
 #pragma unroll
@@ -249,87 +297,121 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
           const float d1 = p[c + i + 1] * (dp[i + 1] - Dq[c + i + 1]);
           pk[i / 2] = pack_bf16x2(d0, d1);
         }
-        tmem_st16(tS + 64 + c / 2, pk);
+        tmem_st16(tS + 64 + 32 * half + c / 2, pk);
 #pragma unroll
         for (int m8 = 0; m8 < 4; ++m8) {
           const uint32_t w[4] = {pk[m8 * 4], pk[m8 * 4 + 1], pk[m8 * 4 + 2], pk[m8 * 4 + 3]};
-          st_shared_v4(sDS + mn_sw128_offset(c + m8 * 8, r), w);
+          st_shared_v4(sDS + mn_sw128_offset(64 * half + c + m8 * 8, r), w);
         }
       }
       tmem_wait_st();
       fence_async_shared();
       tc_fence_before();
       mbar_arrive(b_ds);
-      // dQ read-out: TMEM lane r = query row r of this tile
-      {
-        const int h = g * G + n % G;
-        mbar_wait(b_dqfull, n & 1);
-        tc_fence_after();
-        float v[D];
-#pragma unroll
-        for (int c = 0; c < D; c += 16) tmem_ld16(tdP + c, reinterpret_cast<uint32_t(&)[16]>(v[c]));
-        tmem_wait_ld();
-        tc_fence_before();
-        mbar_arrive(b_dqempty);
-        const int64_t qrow = (int64_t)qt * 128 + r;
-        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (qrow * a.hq + h) * D);
-#pragma unroll
-        for (int c = 0; c < D; c += 4)
-          atomicAdd(dst + c / 4, make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale, v[c + 3] * a.scale));
-      }
     }
-    // ---- dK / dV out (thread = key row)
+    // ---- final dK (half 0) / dV (half 1), thread = key row
     const int64_t row = (int64_t)kt * 128 + r;  // row within the launch's key range
-    float* dk_acc = a.dk_acc + (row * (a.hq / G) + g) * D;
-    float* dv_acc = a.dv_acc + (row * (a.hq / G) + g) * D;
+    const int hkv = a.hq / G;
+    float* acc = (half ? a.dv_acc : a.dk_acc) + (row * hkv + g) * D;
+    const float sc = half ? 1.f : a.scale;
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(half ? a.dv_out : a.dk_out);
+    if (a.kv_final) out += row * a.kv_out_ld + (int64_t)(a.kv_out_head0 + g) * D;
     if (n_iter > 0) {
       mbar_wait(b_kvdone, 0);
       tc_fence_after();
     }
 #pragma unroll
-    for (int which = 0; which < 2; ++which) {
-      float* acc = which ? dv_acc : dk_acc;
-      const float sc = which ? 1.f : a.scale;
-      __nv_bfloat16* out = which ? reinterpret_cast<__nv_bfloat16*>(a.dv_out) : reinterpret_cast<__nv_bfloat16*>(a.dk_out);
-      if (a.kv_final) out += row * a.kv_out_ld + (int64_t)(a.kv_out_head0 + g) * D;
+    for (int c = 0; c < D; c += 16) {
+      float v[16];
+      if (n_iter > 0) {
+        tmem_ld16(tmem + (half ? C::tdV : C::tdK) + lane_off + c, reinterpret_cast<uint32_t(&)[16]>(v));
+        tmem_wait_ld();
 #pragma unroll
-      for (int c = 0; c < D; c += 16) {
-        float v[16];
-        if (n_iter > 0) {
-          tmem_ld16(tmem + (which ? 384 : 256) + lane_off + c, reinterpret_cast<uint32_t(&)[16]>(v));
-          tmem_wait_ld();
+        for (int i = 0; i < 16; ++i) v[i] *= sc;
+      } else {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] *= sc;
-        } else {
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      }
+      if (!a.kv_acc_init) {
 #pragma unroll
-          for (int i = 0; i < 16; ++i) v[i] = 0.f;
-        }
-        if (!a.kv_acc_init) {
-#pragma unroll
-          for (int i = 0; i < 16; i += 4) {
-            const float4 x = *reinterpret_cast<const float4*>(acc + c + i);
-            v[i] += x.x; v[i + 1] += x.y; v[i + 2] += x.z; v[i + 3] += x.w;
-          }
-        }
-        if (a.kv_final) {
-#pragma unroll
-          for (int i = 0; i < 16; i += 8) {
-            uint4 w;
-            w.x = pack_bf16x2(v[i], v[i + 1]); w.y = pack_bf16x2(v[i + 2], v[i + 3]);
-            w.z = pack_bf16x2(v[i + 4], v[i + 5]); w.w = pack_bf16x2(v[i + 6], v[i + 7]);
-            *reinterpret_cast<uint4*>(out + c + i) = w;
-          }
-        } else {
-#pragma unroll
-          for (int i = 0; i < 16; i += 4)
-            *reinterpret_cast<float4*>(acc + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+        for (int i = 0; i < 16; i += 4) {
+          const float4 x = *reinterpret_cast<const float4*>(acc + c + i);
+          v[i] += x.x; v[i + 1] += x.y; v[i + 2] += x.z; v[i + 3] += x.w;
         }
       }
+      if (a.kv_final) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 8) {
+          uint4 w;
+          w.x = pack_bf16x2(v[i], v[i + 1]); w.y = pack_bf16x2(v[i + 2], v[i + 3]);
+          w.z = pack_bf16x2(v[i + 4], v[i + 5]); w.w = pack_bf16x2(v[i + 6], v[i + 7]);
+          *reinterpret_cast<uint4*>(out + c + i) = w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(acc + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+    }
+  } else {
+    // ------------------------------------------------------------------ dQ read-out (query rows)
+    const int r = (warp - 8) * 32 + lane;
+    const int t128 = threadIdx.x - 256;
+    const uint32_t lane_off = ((warp & 3) * 32) << 16;
+    const uint32_t tdQ = tmem + C::tdQ + lane_off;
+    for (int n = 0; n < n_iter; ++n) {
+      const int qt = qt_first + n / G, hh = n % G;
+      const int h = g * G + hh;
+      mbar_wait(b_dqfull, n & 1);
+      tc_fence_after();
+      if constexpr (C::kTmaDQ) {
+        float v[D];
+#pragma unroll
+        for (int c = 0; c < D; c += 16) tmem_ld16(tdQ + c, reinterpret_cast<uint32_t(&)[16]>(v[c]));
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(b_dqempty);
+        // the previous bulk reduce must have finished reading the staging tile
+        if (t128 == 0) bulk_wait_read0();
+        named_bar(1, 128);
+        float* dst = reinterpret_cast<float*>(smem + C::oDQ) + r * D;
+#pragma unroll
+        for (int c = 0; c < D; c += 4)
+          *reinterpret_cast<float4*>(dst + c) = make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale,
+                                                            v[c + 3] * a.scale);
+        fence_async_shared();
+        named_bar(1, 128);
+        if (t128 == 0) {
+          tma_reduce_add_3d(&tm.dq, sDQ, 0, h, qt * 128);
+          bulk_commit();
+        }
+      } else {
+        const int64_t qrow = (int64_t)qt * 128 + r;
+        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (qrow * a.hq + h) * D);
+#pragma unroll
+        for (int hf = 0; hf < D; hf += 64) {
+          float v[64];
+#pragma unroll
+          for (int c = 0; c < 64; c += 16) tmem_ld16(tdQ + hf + c, reinterpret_cast<uint32_t(&)[16]>(v[c]));
+          tmem_wait_ld();
+          if (hf + 64 >= D) {
+            tc_fence_before();
+            mbar_arrive(b_dqempty);
+          }
+#pragma unroll
+          for (int c = 0; c < 64; c += 4)
+            atomicAdd(dst + (hf + c) / 4,
+                      make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale, v[c + 3] * a.scale));
+        }
+      }
+    }
+    if constexpr (C::kTmaDQ) {
+      if (t128 == 0) bulk_wait0();
     }
   }
   tc_fence_before();
   __syncthreads();
-  if (warp == 5) tmem_dealloc<512>(tmem);
+  if (warp == 13) tmem_dealloc<512>(tmem);
 }
 
 template <int D>
@@ -346,6 +428,8 @@ int launch_bwd(const BwdArgs& a, cudaStream_t s) {
   ok &= make_tmap_rows_heads_dim(&tm.v_tail, a.v.base, a.v.rows, a.v.heads, D, 16, 128, s32);
   ok &= make_tmap_rows_heads_dim(&tm.o_main, a.dout.base, a.dout.rows, a.dout.heads, D, 64, 128, s128);
   ok &= make_tmap_rows_heads_dim(&tm.o_tail, a.dout.base, a.dout.rows, a.dout.heads, D, 16, 128, s32);
+  if constexpr (C::kTmaDQ)
+    ok &= make_tmap_f32_rows_heads_dim(&tm.dq, a.dq_acc, a.n_q_rows, a.hq, D, D, 128);
   if (!ok) return -1;
   static bool attr_set = false;
   if (!attr_set) {
