@@ -138,6 +138,24 @@ int fpdt_kernel_time(fpdt_ctx* ctx, double* fwd_ms, int64_t* fwd_launches, doubl
 int fpdt_selftest_umma(int variant, int head_dim, const void* a, const void* b, int n_heads, int rows, void* out,
                        void* stream);
 
+/* Diagnostic micro-benchmark (one CTA of 128 threads per SM, 148 CTAs): what = 0 SS tcgen05.mma
+ * M=128 N=n K=16, 1 TS tcgen05.mma, 2 MUFU ex2 per thread, 3 tcgen05.ld 32x32b.x32 per warp, 4 FMA
+ * polynomial exp2 per thread.  Writes SM cycles per operation (CTA 0) to out[0] (device fp32).
+ * Returns 0 or a CUDA error code. */
+int fpdt_selftest_perf(int what, int n, int iters, float* out, void* stream);
+
+/* Diagnostic: launch ONE bf16 chunk-pair kernel directly (no scheduler) on caller device buffers, rows
+ * [0, n_rows) of q/k/v/dout against each other (the diagonal pair when causal = 1).
+ *   which 0 (forward):  out0 = o bf16 [n_rows][n_q_heads][head_dim], out1 = log2-domain lse fp32 [n_q_heads][n_rows]
+ *   which 1 (backward): lse2 / Dstat fp32 [n_q_heads][n_rows] (log2-domain lse, rowsum(dO o O)),
+ *                       out0 = dq accumulator fp32 [n_rows][n_q_heads][head_dim] (zeroed by the caller; scaled
+ *                       dQ is added), out1 / out2 = dK / dV bf16 [n_rows][n_kv_heads][head_dim]
+ * trace (nullable): device int64 [16][4096] receiving SM-clock timestamps of warp-role protocol events of
+ * CTA (trace_cta, 0).  Returns FPDT_OK or a status. */
+int fpdt_debug_pair(int which, int head_dim, int causal, const void* q, const void* k, const void* v, const void* dout,
+                    const float* lse2, const float* Dstat, void* out0, void* out1, void* out2, int64_t n_rows,
+                    int n_q_heads, int n_kv_heads, long long* trace, int trace_cta, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

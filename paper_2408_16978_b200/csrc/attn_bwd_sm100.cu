@@ -17,13 +17,15 @@
 //   8-11  dQ read-out (thread = query row) and reduction into dq_acc: TMA bulk reduce-add (D <= 80)
 //         or vector atomics (D = 128)
 //   12    TMA producer;  13  TMEM allocator + single-thread MMA issuer
-// TMEM: S^T [0,128) -> P^T bf16 [0,64) + dS^T bf16 [64,128);  dP^T [128,256);
+// TMEM: S^T [0,128) -> P^T bf16 [0,64) + dS^T bf16 [64,128) (A operands of dV, dK);  dP^T [128,256);
+//       dS is also stored to smem (MN-major 128B-swizzled) as the A operand of dQ = dS K;
 //       D <= 80: dQ [256,256+D), dK, dV next (496 columns at D = 80)  -> dP^T of the next tile can be
 //                issued before the current dQ is read out;
 //       D = 128: dQ aliases dP^T; dK [256,384); dV [384,512).
-// MMA issue order per tile n: dV_n, dK_n, S^T_{n+1}, dQ_n, dP^T_{n+1}: S^T_{n+1} overwrites P^T_n/dS^T_n
-// only after dV_n/dK_n in issue order (tcgen05 MMAs of one thread execute in order), so the next
-// tile's exponentials overlap the dQ_n/dP^T_{n+1} MMAs.
+// MMA issue order per tile n: dV_n, dK_n, S^T_{n+1}, dQ_n, dP^T_{n+1}: S^T_{n+1} overwrites P^T_n/dS^T_n only
+// after dV_n/dK_n in issue order (tcgen05 MMAs of one thread execute in order), so the next tile's
+// exponentials overlap the dQ_n and dP^T_{n+1} MMAs.  dV, dK, dQ are single N = D instructions per
+// 16-row contraction step (attn_tile.cuh), the minimum tcgen05 instruction count.
 #include "attn_tile.cuh"
 #include "kernels.h"
 #include "smem_layout.cuh"
@@ -35,12 +37,15 @@ namespace {
 using namespace ptx;
 
 constexpr int kThreads = 448;
+#ifndef FPDT_BWD_TMA_DQ
+#define FPDT_BWD_TMA_DQ 1
+#endif
 
 template <int D>
 struct BwdCfg {
   using T = Tile<D>;
   static constexpr bool kSepDQ = (D <= 80);
-  static constexpr bool kTmaDQ = (D <= 80);
+  static constexpr bool kTmaDQ = FPDT_BWD_TMA_DQ && (D <= 80);
   static constexpr int QS = 2;
   static constexpr int kStage = 2 * T::kBytes;                 // Q + dO
   static constexpr int kDS = 128 * 128 * 2;
@@ -61,13 +66,24 @@ struct BwdCfg {
 };
 
 struct TmapSet {
-  CUtensorMap q_main, q_tail, k_main, k_tail, v_main, v_tail, o_main, o_tail, dq;
+  CUtensorMap q, k, v, o, dq;
 };
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe (see attn_fwd_sm100.cu): degree-3 minimax, max rel. error 7.5e-5; -127 <= x <= 127.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float j = __fadd_rn(x, 12582912.f);
+  const float f = __fsub_rn(x, __fsub_rn(j, 12582912.f));
+  float p = fmaf(f, 0.055169348f, 0.24260798f);
+  p = fmaf(p, f, 0.69326115f);
+  p = fmaf(p, f, 0.9999283f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
 }
 
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
@@ -118,6 +134,12 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
     if (qt_first > n_qt_total) qt_first = n_qt_total;
   }
   const int n_iter = (n_qt_total - qt_first) * G;
+  // debug timeline (a.trace != nullptr): SM clock of protocol events of CTA (trace_cta, 0)
+  const bool tracing = a.trace != nullptr && blockIdx.x == a.trace_cta && blockIdx.y == 0;
+#define TRACE(ev, n)                                                        \
+  do {                                                                      \
+    if (tracing && (n) < 4096) a.trace[(ev) * 4096 + (n)] = clock64();      \
+  } while (0)
 
   if (warp == 13) tmem_alloc<512>(smem_u32(tmem_slot));
   if (warp == 12 && lane == 0) {
@@ -147,19 +169,20 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
       const uint64_t pol_kv = policy_evict_first(), pol_q = policy_evict_last();
       mbar_expect_tx(b_kv, 2 * T::kBytes);
       const int krow = (int)(a.kv_row0 + (int64_t)kt * 128);
-      T::load(sK, &tm.k_main, &tm.k_tail, b_kv, a.k.head0 + g, krow, pol_kv);
-      T::load(sV, &tm.v_main, &tm.v_tail, b_kv, a.v.head0 + g, krow, pol_kv);
+      T::load(sK, &tm.k, b_kv, a.k.head0 + g, krow, pol_kv);
+      T::load(sV, &tm.v, b_kv, a.v.head0 + g, krow, pol_kv);
       for (int n = 0; n < n_iter; ++n) {
         const int s = n % QS;
         if (n >= QS) mbar_wait(b_qempty(s), ((n / QS) - 1) & 1);
+        TRACE(12, n);
         const int qt = qt_first + n / G, hh = n % G;
         const int h = g * G + hh;
         const uint32_t st = base + C::oStage + s * C::kStage;
         const uint32_t stats = base + C::oStats + s * C::kStats;
         const int qrow = (int)(a.q_row0 + (int64_t)qt * 128);
         mbar_expect_tx(b_qfull(s), 2 * T::kBytes + 1024);
-        T::load(st, &tm.q_main, &tm.q_tail, b_qfull(s), a.q.head0 + h, qrow, pol_q);
-        T::load(st + T::kBytes, &tm.o_main, &tm.o_tail, b_qfull(s), a.dout.head0 + h, qrow, pol_q);
+        T::load(st, &tm.q, b_qfull(s), a.q.head0 + h, qrow, pol_q);
+        T::load(st + T::kBytes, &tm.o, b_qfull(s), a.dout.head0 + h, qrow, pol_q);
         bulk_load(stats, a.lse2 + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, b_qfull(s));
         bulk_load(stats + 512, a.Dstat + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, b_qfull(s));
       }
@@ -168,10 +191,8 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
     // ------------------------------------------------------------------ MMA issuer
     if (elect_one() && n_iter > 0) {
       const uint32_t idS = idesc_bf16(128, 128, 0, 0);           // S^T, dP^T: A,B K-major
-      const uint32_t idGm = idesc_bf16(128, T::kMainN, 0, 1);    // dV, dK: A = TMEM, B MN-major
-      const uint32_t idGt = idesc_bf16(128, 16, 0, 1);
-      const uint32_t idQm = idesc_bf16(128, T::kMainN, 1, 1);    // dQ: A = dS MN-major smem, B = K MN-major
-      const uint32_t idQt = idesc_bf16(128, 16, 1, 1);
+      const uint32_t idG = idesc_bf16(128, D, 0, 1);             // dV, dK: A = TMEM, B MN-major
+      const uint32_t idQ = idesc_bf16(128, D, 1, 1);             // dQ: A = dS MN-major smem, B = K MN-major
       const uint32_t tS = tmem + C::tS, tdP = tmem + C::tdP, tdQ = tmem + C::tdQ, tdK = tmem + C::tdK,
                      tdV = tmem + C::tdV;
       auto stage_q = [&](int n) { return base + C::oStage + (n % QS) * C::kStage; };
@@ -195,45 +216,35 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
       for (int n = 0; n < n_iter; ++n) {
         const int s = n % QS;
         const uint32_t sQ = stage_q(n), sO = sQ + T::kBytes;
-        // dV += P^T dO
+        // dV += P^T dO   (A = P^T from TMEM)
         mbar_wait(b_p, n & 1);
+        TRACE(4, n);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_ts(tdV, tS + kk * 8, T::desc_mn_main(sO, kk), idGm, (n > 0 || kk > 0));
-        if constexpr (T::kTail) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            mma_ts(tdV + T::kMainN, tS + kk * 8, T::desc_mn_tail(sO, kk), idGt, (n > 0 || kk > 0));
-        }
-        // dK += dS^T Q
+        for (int kk = 0; kk < 8; ++kk) mma_ts(tdV, tS + kk * 8, T::desc_mn(sO, kk), idG, (n > 0 || kk > 0));
+        // dK += dS^T Q   (A = dS^T from TMEM)
         mbar_wait(b_ds, n & 1);
+        TRACE(5, n);
         tc_fence_after();
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_ts(tdK, tS + 64 + kk * 8, T::desc_mn_main(sQ, kk), idGm, (n > 0 || kk > 0));
-        if constexpr (T::kTail) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            mma_ts(tdK + T::kMainN, tS + 64 + kk * 8, T::desc_mn_tail(sQ, kk), idGt, (n > 0 || kk > 0));
-        }
+        for (int kk = 0; kk < 8; ++kk) mma_ts(tdK, tS + 64 + kk * 8, T::desc_mn(sQ, kk), idG, (n > 0 || kk > 0));
         mma_commit(b_qempty(s));  // Q_n / dO_n consumed (dQ reads dS and K only)
+        // S^T_{n+1} may overwrite P^T_n / dS^T_n now (dV_n, dK_n precede it in issue order)
         const bool more = n + 1 < n_iter;
         if (more) {
           mbar_wait(b_qfull((n + 1) % QS), ((n + 1) / QS) & 1);
           tc_fence_after();
           issue_S(n + 1);
+          TRACE(6, n);
         }
-        // dQ_n = dS K  (its TMEM columns must have been read out for n-1)
+        // dQ_n = dS K  (A = dS from smem, MN-major; its TMEM columns must be read out for n-1)
         if (n > 0) {
           mbar_wait(b_dqempty, (n - 1) & 1);
+          TRACE(7, n);
           tc_fence_after();
         }
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk) mma_ss(tdQ, desc_a_mn_sw128(sDS, kk), T::desc_mn_main(sK, kk), idQm, kk > 0);
-        if constexpr (T::kTail) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            mma_ss(tdQ + T::kMainN, desc_a_mn_sw128(sDS, kk), T::desc_mn_tail(sK, kk), idQt, kk > 0);
-        }
+        for (int kk = 0; kk < 8; ++kk) mma_ss(tdQ, desc_a_mn_sw128(sDS, kk), T::desc_mn(sK, kk), idQ, kk > 0);
         mma_commit(b_dqfull);
         mma_commit(b_dsfree);
         if (more) {
@@ -242,6 +253,7 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
             tc_fence_after();
           }
           issue_dP(n + 1);
+          TRACE(8, n);
         }
       }
       mma_commit(b_kvdone);
@@ -260,18 +272,34 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
       const float* lse2 = reinterpret_cast<const float*>(smem + C::oStats + s * C::kStats) + 64 * half;
       const float* Dq = lse2 + 128;
       mbar_wait(b_s, n & 1);
+      if (warp == 0 && lane == 0) TRACE(0, n);
       tc_fence_after();
       float p[64];
       tmem_ld32(tS + 64 * half, reinterpret_cast<uint32_t*>(p));
       tmem_ld32(tS + 64 * half + 32, reinterpret_cast<uint32_t*>(p) + 32);
       tmem_wait_ld();
+      if (warp == 0 && lane == 0) TRACE(13, n);
       // query column index (within the tile) < lim is masked (query position < key position)
-      const int64_t lim = (a.causal ? (kpos - (a.q_pos0 + (int64_t)qt * 128)) : -1) - 64 * half;
+      int64_t lim64 = (a.causal ? (kpos - (a.q_pos0 + (int64_t)qt * 128)) : -1) - 64 * half;
+      const int lim = (int)(lim64 < -1 ? -1 : (lim64 > 64 ? 64 : lim64));
+      if (__any_sync(0xffffffffu, lim > 0)) {
+        // tile straddling the diagonal: MUFU only (maps to exact zeros under the mask)
 #pragma unroll
-      for (int i = 0; i < 64; ++i) {
-        const float v = ex2(fmaf(p[i], sl2, -lse2[i]));
-        p[i] = (i < lim) ? 0.f : v;
+        for (int i = 0; i < 64; ++i) {
+          const float v = ex2(fmaf(p[i], sl2, -lse2[i]));
+          p[i] = (i < lim) ? 0.f : v;
+        }
+      } else {
+        // every 4th exponential on the FMA pipe (exp2_poly), the rest on MUFU
+#pragma unroll
+        for (int i = 0; i < 64; i += 4) {
+          p[i] = ex2(fmaf(p[i], sl2, -lse2[i]));
+          p[i + 1] = ex2(fmaf(p[i + 1], sl2, -lse2[i + 1]));
+          p[i + 2] = ex2(fmaf(p[i + 2], sl2, -lse2[i + 2]));
+          p[i + 3] = exp2_poly(fmaf(p[i + 3], sl2, -lse2[i + 3]));
+        }
       }
+      if (warp == 0 && lane == 0) TRACE(14, n);
 #pragma unroll
       for (int c = 0; c < 64; c += 32) {
         uint32_t pk[16];
@@ -280,13 +308,17 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
         tmem_st16(tS + 32 * half + c / 2, pk);
       }
       tmem_wait_st();
+      if (warp == 0 && lane == 0) TRACE(15, n);
       tc_fence_before();
       mbar_arrive(b_p);
+      if (warp == 0 && lane == 0) TRACE(1, n);
       mbar_wait(b_dp, n & 1);
+      if (warp == 0 && lane == 0) TRACE(2, n);
       if (n > 0) mbar_wait(b_dsfree, (n - 1) & 1);
       tc_fence_after();
 #pragma unroll
       for (int c = 0; c < 64; c += 32) {
+        // dS = P o (dP - D)
         float dp[32];
         tmem_ld32(tdP + 64 * half + c, reinterpret_cast<uint32_t*>(dp));
         tmem_wait_ld();
@@ -308,6 +340,7 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
       fence_async_shared();
       tc_fence_before();
       mbar_arrive(b_ds);
+      if (warp == 0 && lane == 0) TRACE(3, n);
     }
     // ---- final dK (half 0) / dV (half 1), thread = key row
     const int64_t row = (int64_t)kt * 128 + r;  // row within the launch's key range
@@ -363,6 +396,7 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
       const int qt = qt_first + n / G, hh = n % G;
       const int h = g * G + hh;
       mbar_wait(b_dqfull, n & 1);
+      TRACE(9, n);
       tc_fence_after();
       if constexpr (C::kTmaDQ) {
         float v[D];
@@ -371,6 +405,7 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(b_dqempty);
+        TRACE(10, n);
         // the previous bulk reduce must have finished reading the staging tile
         if (t128 == 0) bulk_wait_read0();
         named_bar(1, 128);
@@ -384,6 +419,7 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
         if (t128 == 0) {
           tma_reduce_add_3d(&tm.dq, sDQ, 0, h, qt * 128);
           bulk_commit();
+          TRACE(11, n);
         }
       } else {
         const int64_t qrow = (int64_t)qt * 128 + r;
@@ -418,16 +454,10 @@ template <int D>
 int launch_bwd(const BwdArgs& a, cudaStream_t s) {
   using C = BwdCfg<D>;
   TmapSet tm;
-  const CUtensorMapSwizzle s128 = CU_TENSOR_MAP_SWIZZLE_128B, s32 = CU_TENSOR_MAP_SWIZZLE_32B;
-  bool ok = true;
-  ok &= make_tmap_rows_heads_dim(&tm.q_main, a.q.base, a.q.rows, a.q.heads, D, 64, 128, s128);
-  ok &= make_tmap_rows_heads_dim(&tm.q_tail, a.q.base, a.q.rows, a.q.heads, D, 16, 128, s32);
-  ok &= make_tmap_rows_heads_dim(&tm.k_main, a.k.base, a.k.rows, a.k.heads, D, 64, 128, s128);
-  ok &= make_tmap_rows_heads_dim(&tm.k_tail, a.k.base, a.k.rows, a.k.heads, D, 16, 128, s32);
-  ok &= make_tmap_rows_heads_dim(&tm.v_main, a.v.base, a.v.rows, a.v.heads, D, 64, 128, s128);
-  ok &= make_tmap_rows_heads_dim(&tm.v_tail, a.v.base, a.v.rows, a.v.heads, D, 16, 128, s32);
-  ok &= make_tmap_rows_heads_dim(&tm.o_main, a.dout.base, a.dout.rows, a.dout.heads, D, 64, 128, s128);
-  ok &= make_tmap_rows_heads_dim(&tm.o_tail, a.dout.base, a.dout.rows, a.dout.heads, D, 16, 128, s32);
+  bool ok = make_tile_tmap<D>(&tm.q, a.q.base, a.q.rows, a.q.heads);
+  ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
+  ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
+  ok &= make_tile_tmap<D>(&tm.o, a.dout.base, a.dout.rows, a.dout.heads);
   if constexpr (C::kTmaDQ)
     ok &= make_tmap_f32_rows_heads_dim(&tm.dq, a.dq_acc, a.n_q_rows, a.hq, D, D, 128);
   if (!ok) return -1;

@@ -27,6 +27,10 @@ using namespace ptx;
 
 constexpr int kThreads = 320;
 constexpr float kRescaleThreshold = 8.0f;
+#ifndef FPDT_FWD_POLY
+#define FPDT_FWD_POLY 0
+#endif
+constexpr bool kFwdPoly = FPDT_FWD_POLY != 0;  // FMA-pipe exp2 for every 4th element (issue-bound here: off)
 
 template <int D>
 struct FwdCfg {
@@ -38,7 +42,7 @@ struct FwdCfg {
 };
 
 struct TmapSet {
-  CUtensorMap q_main, q_tail, k_main, k_tail, v_main, v_tail;
+  CUtensorMap q, k, v;
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -50,6 +54,46 @@ __device__ __forceinline__ float lg2(float x) {
   float y;
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
+}
+
+// 2^x on the FMA pipe (FA4-style MUFU offload): round-to-nearest split x = k + f, f in [-1/2, 1/2],
+// degree-3 minimax polynomial for 2^f (max rel. error 7.5e-5 << bf16's 2^-9), exponent added as an integer.
+// Valid for -127 <= x <= 127; callers use it only where x is finite.
+__device__ __forceinline__ float exp2_poly(float x) {
+  x = fmaxf(x, -127.f);
+  const float j = __fadd_rn(x, 12582912.f);  // 1.5 * 2^23: integer part lands in the low mantissa bits
+  const float f = __fsub_rn(x, __fsub_rn(j, 12582912.f));
+  float p = fmaf(f, 0.055169348f, 0.24260798f);
+  p = fmaf(p, f, 0.69326115f);
+  p = fmaf(p, f, 0.9999283f);
+  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
+}
+
+// exp2(x*sl2 - mb) for one 128-column row, packed to bf16 and stored to TMEM columns [tS, tS+64); returns the
+// row sum of the fp32 values.  kPoly: every 4th exponential on the FMA pipe.
+template <bool kPoly>
+__device__ __forceinline__ float exp_pack_store(const float* x, float sl2, float mb, uint32_t tS) {
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+#pragma unroll
+  for (int c = 0; c < 128; c += 32) {
+    uint32_t pk[16];
+#pragma unroll
+    for (int i = 0; i < 32; i += 4) {
+      const float p0 = ex2(fmaf(x[c + i], sl2, -mb));
+      const float p1 = ex2(fmaf(x[c + i + 1], sl2, -mb));
+      const float p2 = ex2(fmaf(x[c + i + 2], sl2, -mb));
+      const float e3 = fmaf(x[c + i + 3], sl2, -mb);
+      const float p3 = kPoly ? exp2_poly(e3) : ex2(e3);
+      s0 += p0;
+      s1 += p1;
+      s2 += p2;
+      s3 += p3;
+      pk[i / 2] = pack_bf16x2(p0, p1);
+      pk[i / 2 + 1] = pack_bf16x2(p2, p3);
+    }
+    tmem_st16(tS + c / 2, pk);
+  }
+  return (s0 + s1) + (s2 + s3);
 }
 
 template <int D>
@@ -77,6 +121,11 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
     const int64_t need = (reach + 127) / 128;
     n_tiles = (int)(need < n_tiles ? need : n_tiles);
   }
+  const bool tracing = a.trace != nullptr && blockIdx.x == a.trace_cta && blockIdx.y == 0;
+#define TRACE(ev, n)                                                        \
+  do {                                                                      \
+    if (tracing && (n) < 4096) a.trace[(ev) * 4096 + (n)] = clock64();      \
+  } while (0)
 
   if (warp == 9) tmem_alloc<512>(smem_u32(&tmem_slot));
   if (warp == 8 && lane == 0) {
@@ -101,32 +150,32 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
   if (warp == 8) {
     // ------------------------------------------------------------------ TMA producer
     if (elect_one()) {
-      tma_prefetch_desc(&tm.q_main);
-      tma_prefetch_desc(&tm.k_main);
-      tma_prefetch_desc(&tm.v_main);
+      tma_prefetch_desc(&tm.q);
+      tma_prefetch_desc(&tm.k);
+      tma_prefetch_desc(&tm.v);
       const uint64_t pol_q = policy_evict_first(), pol_kv = policy_evict_last();
       const uint32_t bq = smem_u32(&bar_q);
       mbar_expect_tx(bq, C::kQBytes);
       const int qrow = (int)(a.q_row0 + (int64_t)pair * 256);
-      T::load(sQ, &tm.q_main, &tm.q_tail, bq, a.q.head0 + h, qrow, pol_q);
-      T::load(sQ + T::kBytes, &tm.q_main, &tm.q_tail, bq, a.q.head0 + h, qrow + 128, pol_q);
+      T::load(sQ, &tm.q, bq, a.q.head0 + h, qrow, pol_q);
+      T::load(sQ + T::kBytes, &tm.q, bq, a.q.head0 + h, qrow + 128, pol_q);
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j % ST;
         if (j >= ST) mbar_wait(smem_u32(&bar_kv_empty[s]), ((j / ST) - 1) & 1);
+        TRACE(7, j);
         const uint32_t sk = sKV + s * C::kStageBytes, sv = sk + T::kBytes;
         const int krow = (int)(a.kv_row0 + (int64_t)j * 128);
         mbar_expect_tx(smem_u32(&bar_k[s]), T::kBytes);
-        T::load(sk, &tm.k_main, &tm.k_tail, smem_u32(&bar_k[s]), a.k.head0 + g, krow, pol_kv);
+        T::load(sk, &tm.k, smem_u32(&bar_k[s]), a.k.head0 + g, krow, pol_kv);
         mbar_expect_tx(smem_u32(&bar_v[s]), T::kBytes);
-        T::load(sv, &tm.v_main, &tm.v_tail, smem_u32(&bar_v[s]), a.v.head0 + g, krow, pol_kv);
+        T::load(sv, &tm.v, smem_u32(&bar_v[s]), a.v.head0 + g, krow, pol_kv);
       }
     }
   } else if (warp == 9) {
     // ------------------------------------------------------------------ MMA issuer
     if (elect_one()) {
       const uint32_t idS = idesc_bf16(128, 128, 0, 0);
-      const uint32_t idPVm = idesc_bf16(128, T::kMainN, 0, 1);
-      const uint32_t idPVt = idesc_bf16(128, 16, 0, 1);
+      const uint32_t idPV = idesc_bf16(128, D, 0, 1);
       const uint32_t tS[2] = {tmem, tmem + 128};
       const uint32_t tO[2] = {tmem + 256, tmem + 384};
       auto issue_S = [&](int t, int s) {
@@ -139,12 +188,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         const uint32_t sv = sKV + s * C::kStageBytes + T::kBytes;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tO[t], tS[t] + kk * 8, T::desc_mn_main(sv, kk), idPVm, (j > 0 || kk > 0) ? 1u : 0u);
-        if constexpr (T::kTail) {
-#pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            mma_ts(tO[t] + T::kMainN, tS[t] + kk * 8, T::desc_mn_tail(sv, kk), idPVt, (j > 0 || kk > 0) ? 1u : 0u);
-        }
+          mma_ts(tO[t], tS[t] + kk * 8, T::desc_mn(sv, kk), idPV, (j > 0 || kk > 0) ? 1u : 0u);
       };
       mbar_wait(smem_u32(&bar_q), 0);
       tc_fence_after();
@@ -161,12 +205,14 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         }
         mbar_wait(smem_u32(&bar_v[s]), ph);
         mbar_wait(smem_u32(&bar_p[0]), j & 1);
+        TRACE(4, j);
         tc_fence_after();
         issue_PV(0, s, j);
         const bool more = j + 1 < n_tiles;
         const int s2 = (j + 1) % ST;
         if (more) {
           mbar_wait(smem_u32(&bar_k[s2]), ((j + 1) / ST) & 1);
+          TRACE(6, j);
           tc_fence_after();
           issue_S(0, s2);
           mma_commit(smem_u32(&bar_s[0]));
@@ -174,6 +220,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
           mma_commit(smem_u32(&bar_o[0]));
         }
         mbar_wait(smem_u32(&bar_p[1]), j & 1);
+        TRACE(5, j);
         tc_fence_after();
         issue_PV(1, s, j);
         mma_commit(smem_u32(&bar_kv_empty[s]));
@@ -197,6 +244,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
     float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_tiles; ++j) {
       mbar_wait(smem_u32(&bar_s[t]), j & 1);
+      if ((warp & 3) == 0 && lane == 0) TRACE(0 + 2 * t, j);
       tc_fence_after();
       float x[128];
       tmem_ld32(tS + 0, reinterpret_cast<uint32_t*>(x));
@@ -204,18 +252,28 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
       tmem_ld32(tS + 64, reinterpret_cast<uint32_t*>(x) + 64);
       tmem_ld32(tS + 96, reinterpret_cast<uint32_t*>(x) + 96);
       tmem_wait_ld();
-      if (a.causal) {
-        const int64_t lim = qpos - (a.kv_pos0 + (int64_t)j * 128);
-        if (lim < 127) {
+      if ((warp & 3) == 0 && lane == 0) TRACE(8 + 4 * t, j);
+      // causal mask: only on the tile(s) that straddle the diagonal (warp-uniform fast path otherwise)
+      const int64_t lim64 = qpos - (a.kv_pos0 + (int64_t)j * 128);
+      const bool masked = a.causal && lim64 < 127;
+      const bool any_masked = __any_sync(0xffffffffu, masked);
+      if (masked) {
+        const int lim = (int)(lim64 < -1 ? -1 : lim64);
 #pragma unroll
-          for (int i = 0; i < 128; ++i)
-            if (i > lim) x[i] = -INFINITY;
-        }
+        for (int i = 0; i < 128; ++i)
+          if (i > lim) x[i] = -INFINITY;
       }
-      float mx = x[0];
+      float m8[8];
 #pragma unroll
-      for (int i = 1; i < 128; ++i) mx = fmaxf(mx, x[i]);
+      for (int k = 0; k < 8; ++k) m8[k] = x[k];
+#pragma unroll
+      for (int i = 8; i < 128; i += 8) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], x[i + k]);
+      }
+      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
       mx *= sl2;
+      if ((warp & 3) == 0 && lane == 0) TRACE(9 + 4 * t, j);
       const bool need = mx > m_run + kRescaleThreshold;
       if (__any_sync(0xffffffffu, need)) {
         const float m_new = need ? mx : m_run;
@@ -235,23 +293,16 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         m_run = m_new;
       }
       const float mb = (m_run == -INFINITY) ? 0.f : m_run;
-      float sum = 0.f;
-#pragma unroll
-      for (int c = 0; c < 128; c += 32) {
-        uint32_t pk[16];
-#pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float p0 = ex2(fmaf(x[c + i], sl2, -mb));
-          const float p1 = ex2(fmaf(x[c + i + 1], sl2, -mb));
-          sum += p0 + p1;
-          pk[i / 2] = pack_bf16x2(p0, p1);
-        }
-        tmem_st16(tS + c / 2, pk);
-      }
+      // P = exp2(S*scale*log2e - m): a quarter of the exponentials on the FMA pipe (exp2_poly), the rest on
+      // MUFU, except on masked tiles (MUFU maps -inf to exactly 0)
+      const float sum = any_masked ? exp_pack_store<false>(x, sl2, mb, tS) : exp_pack_store<kFwdPoly>(x, sl2, mb, tS);
       l_run += sum;
+      if ((warp & 3) == 0 && lane == 0) TRACE(10 + 4 * t, j);
       tmem_wait_st();
+      if ((warp & 3) == 0 && lane == 0) TRACE(11 + 4 * t, j);
       tc_fence_before();
       mbar_arrive(smem_u32(&bar_p[t]));
+      if ((warp & 3) == 0 && lane == 0) TRACE(1 + 2 * t, j);
     }
     // epilogue: normalise, merge with the running partial result, write
     mbar_wait(smem_u32(&bar_o[t]), 0);
@@ -325,14 +376,9 @@ template <int D>
 int launch_fwd(const FwdArgs& a, cudaStream_t s) {
   using C = FwdCfg<D>;
   TmapSet tm;
-  const CUtensorMapSwizzle s128 = CU_TENSOR_MAP_SWIZZLE_128B, s32 = CU_TENSOR_MAP_SWIZZLE_32B;
-  bool ok = true;
-  ok &= make_tmap_rows_heads_dim(&tm.q_main, a.q.base, a.q.rows, a.q.heads, D, 64, 128, s128);
-  ok &= make_tmap_rows_heads_dim(&tm.q_tail, a.q.base, a.q.rows, a.q.heads, D, 16, 128, s32);
-  ok &= make_tmap_rows_heads_dim(&tm.k_main, a.k.base, a.k.rows, a.k.heads, D, 64, 128, s128);
-  ok &= make_tmap_rows_heads_dim(&tm.k_tail, a.k.base, a.k.rows, a.k.heads, D, 16, 128, s32);
-  ok &= make_tmap_rows_heads_dim(&tm.v_main, a.v.base, a.v.rows, a.v.heads, D, 64, 128, s128);
-  ok &= make_tmap_rows_heads_dim(&tm.v_tail, a.v.base, a.v.rows, a.v.heads, D, 16, 128, s32);
+  bool ok = make_tile_tmap<D>(&tm.q, a.q.base, a.q.rows, a.q.heads);
+  ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
+  ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
   if (!ok) return -1;
   static bool attr_set = false;
   if (!attr_set) {

@@ -1,0 +1,63 @@
+// Diagnostic entry point: one chunk-pair attention kernel launched directly on caller buffers, with an
+// optional per-CTA SM-clock timeline (kernels.h FwdArgs/BwdArgs::trace).  Not used by the FPDT schedule;
+// it exists so a single pair kernel can be timed and its warp-role protocol inspected in isolation.
+#include <cmath>
+
+#include "fpdt.h"
+#include "kernels.h"
+
+using namespace fpdt;
+
+extern "C" int fpdt_debug_pair(int which, int head_dim, int causal, const void* q, const void* k, const void* v,
+                               const void* dout, const float* lse2, const float* Dstat, void* out0, void* out1,
+                               void* out2, int64_t n_rows, int n_q_heads, int n_kv_heads, long long* trace,
+                               int trace_cta, void* stream) {
+  if (head_dim != 64 && head_dim != 80 && head_dim != 128) return FPDT_ERR_UNSUPPORTED;
+  if (n_rows % 256 || n_q_heads % n_kv_heads) return FPDT_ERR_DIVISIBILITY;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const float scale = (float)(1.0 / std::sqrt((double)head_dim));
+  if (which == 0) {
+    FwdArgs a;
+    a.q = {q, n_rows, n_q_heads, 0};
+    a.k = {k, n_rows, n_kv_heads, 0};
+    a.v = {v, n_rows, n_kv_heads, 0};
+    a.n_q_rows = (int)n_rows;
+    a.n_kv_rows = (int)n_rows;
+    a.causal = causal;
+    a.hq = n_q_heads;
+    a.G = n_q_heads / n_kv_heads;
+    a.scale_log2 = scale * 1.4426950408889634f;
+    a.is_final = 1;
+    a.o_out = out0;
+    a.o_ld = (int64_t)n_q_heads * head_dim;
+    a.lse_save = static_cast<float*>(out1);
+    a.lse_save_ld = n_rows;
+    a.trace = trace;
+    a.trace_cta = trace_cta;
+    return launch_attn_fwd_bf16(a, head_dim, s) == 0 ? FPDT_OK : FPDT_ERR_CUDA;
+  }
+  BwdArgs a;
+  a.q = {q, n_rows, n_q_heads, 0};
+  a.k = {k, n_rows, n_kv_heads, 0};
+  a.v = {v, n_rows, n_kv_heads, 0};
+  a.dout = {dout, n_rows, n_q_heads, 0};
+  a.n_q_rows = (int)n_rows;
+  a.n_kv_rows = (int)n_rows;
+  a.causal = causal;
+  a.hq = n_q_heads;
+  a.G = n_q_heads / n_kv_heads;
+  a.scale = scale;
+  a.scale_log2 = scale * 1.4426950408889634f;
+  a.lse2 = lse2;
+  a.Dstat = Dstat;
+  a.stat_ld = n_rows;
+  a.dq_acc = static_cast<float*>(out0);
+  a.kv_acc_init = 1;
+  a.kv_final = 1;
+  a.dk_out = out1;
+  a.dv_out = out2;
+  a.kv_out_ld = (int64_t)n_kv_heads * head_dim;
+  a.trace = trace;
+  a.trace_cta = trace_cta;
+  return launch_attn_bwd_bf16(a, head_dim, s) == 0 ? FPDT_OK : FPDT_ERR_CUDA;
+}

@@ -43,6 +43,8 @@ struct FwdArgs {
   // D = rowsum(dO o O) is formed from the fp32 output (R9); nullptr = not saved.
   __nv_bfloat16* o_resid = nullptr;
   int64_t o_resid_ld = 0;
+  long long* trace = nullptr;       // debug timeline (fpdt_debug_pair), [16][4096] SM clocks
+  int trace_cta = 0;
 };
 
 // Backward chunk-pair attention (KV-stationary): keys/values [kv_row0, +n_kv_rows) against queries
@@ -68,6 +70,8 @@ struct BwdArgs {
   void* dv_out = nullptr;
   int64_t kv_out_ld = 0;            // elements per row of dk_out/dv_out
   int kv_out_head0 = 0;
+  long long* trace = nullptr;       // debug timeline (fpdt_debug_pair), [16][4096] SM clocks
+  int trace_cta = 0;
 };
 
 int launch_attn_fwd_bf16(const FwdArgs& a, int head_dim, cudaStream_t s);

@@ -1,0 +1,111 @@
+// Micro-benchmarks of the sm_100a units the attention kernels lean on (diagnostic, not on the hot path):
+// tcgen05.mma issue cost per instruction shape, MUFU ex2 throughput, TMEM load throughput.
+// Each runs one CTA per SM (148 CTAs) and reports the median SM-cycles per operation of CTA 0.
+#include "attn_tile.cuh"
+#include "fpdt.h"
+
+namespace fpdt {
+namespace {
+
+using namespace ptx;
+
+// what: 0 = SS MMA M=128 N=n K=16, 1 = TS MMA (A in TMEM) M=128 N=n K=16, 2 = MUFU.EX2 per thread (128 thr),
+//       3 = tcgen05.ld 32x32b.x32 per warp (4 warps), 4 = FFMA-poly exp2 per thread
+__global__ void __launch_bounds__(1024, 1) perf_kernel(int what, int n, int iters, float* out) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  __shared__ uint64_t bar;
+  __shared__ uint32_t slot;
+  const uint32_t warp = warp_id();
+  if (warp == 0) tmem_alloc<512>(smem_u32(&slot));
+  if (threadIdx.x == 0) {
+    mbar_init(smem_u32(&bar), 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = slot;
+  const uint32_t s0 = smem_u32(smem);
+  long long t0 = 0, t1 = 0;
+  float sink = 0.f;
+  if (what <= 1) {
+    if (threadIdx.x == 0) {
+      const uint32_t id = idesc_bf16(128, n, 0, 0);
+      const uint64_t da = smem_desc(s0, 16, 1024, kSw128), db = smem_desc(s0 + 32768, 16, 1024, kSw128);
+      const int chains = (iters & 7) ? (iters & 7) : 1;
+      const uint32_t stride = n <= 128 ? 128 : 256;
+      const uint32_t acc0 = tmem, acc1 = tmem + (chains > 1 ? stride : 0);
+      t0 = clock64();
+      if (what == 0) {
+        for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mma_ss((u & 1) ? acc1 : acc0, da + 2 * u, db + 2 * u, id, 1);
+        }
+      } else {
+        for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) mma_ts((u & 1) ? acc1 : acc0, tmem + 256 + 8 * u, db + 2 * u, id, 1);
+        }
+      }
+      mma_commit(smem_u32(&bar));
+      mbar_wait(smem_u32(&bar), 0);
+      t1 = clock64();
+    }
+  } else if (what == 2 || what == 4) {
+    float x[8];
+#pragma unroll
+    for (int c = 0; c < 8; ++c) x[c] = -0.001f * threadIdx.x - 0.1f * c;
+    t0 = clock64();
+    for (int i = 0; i < iters; i += 8) {
+#pragma unroll
+      for (int c = 0; c < 8; ++c) {
+        float y;
+        if (what == 2) {
+          asm volatile("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x[c]));
+        } else {
+          const float xc = fmaxf(x[c], -127.f);
+          const float fl = floorf(xc);
+          const float f = xc - fl;
+          float p = fmaf(f, 0.0790393f, 0.2261766f);
+          p = fmaf(p, f, 0.6951474f);
+          p = fmaf(p, f, 1.0f);
+          y = __int_as_float(__float_as_int(p) + ((int)fl << 23));
+        }
+        x[c] = x[c] + y * 1e-9f;
+      }
+    }
+    t1 = clock64();
+#pragma unroll
+    for (int c = 0; c < 8; ++c) sink += x[c];
+  } else if (what == 3) {
+    const uint32_t lane_off = ((warp & 3) * 32) << 16;
+    uint32_t r[32];
+    t0 = clock64();
+    uint32_t r2[32], r3[32], r4[32];
+    for (int i = 0; i < iters; i += 4) {
+      tmem_ld32(tmem + lane_off + 0, r);
+      tmem_ld32(tmem + lane_off + 32, r2);
+      tmem_ld32(tmem + lane_off + 64, r3);
+      tmem_ld32(tmem + lane_off + 96, r4);
+      tmem_wait_ld();
+      sink += __uint_as_float(r[3]) + __uint_as_float(r2[7]) + __uint_as_float(r3[11]) + __uint_as_float(r4[31]);
+    }
+    t1 = clock64();
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = (float)(t1 - t0) / iters;
+  if (sink == 12345.f) out[1] = sink;
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) tmem_dealloc<512>(tmem);
+}
+
+}  // namespace
+}  // namespace fpdt
+
+extern "C" int fpdt_selftest_perf(int what, int n, int iters, float* out, void* stream) {
+  const int smem = 65536 + 1024;
+  cudaFuncSetAttribute(fpdt::perf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int threads = ((what == 2 || what == 4) && n > 0) ? n : 128;  // n = threads per CTA for the ALU tests
+  fpdt::perf_kernel<<<148, threads, smem, static_cast<cudaStream_t>(stream)>>>(what, n, iters, out);
+  return (int)cudaGetLastError();
+}

@@ -23,8 +23,7 @@ __device__ __forceinline__ uint8_t* align1024(uint8_t* p) {
 
 template <int D>
 __global__ void __launch_bounds__(128, 1)
-probe_kernel(int variant, const __grid_constant__ CUtensorMap a_main, const __grid_constant__ CUtensorMap a_tail,
-             const __grid_constant__ CUtensorMap b_main, const __grid_constant__ CUtensorMap b_tail,
+probe_kernel(int variant, const __grid_constant__ CUtensorMap a_map, const __grid_constant__ CUtensorMap b_map,
              const __nv_bfloat16* __restrict__ a_plain, int ha, int hb, float* __restrict__ out) {
   using T = Tile<D>;
   extern __shared__ uint8_t smem_raw[];
@@ -81,11 +80,11 @@ probe_kernel(int variant, const __grid_constant__ CUtensorMap a_main, const __gr
     const uint64_t pol = policy_evict_first();
     if (variant == 0) {
       mbar_expect_tx(bar_load, 2 * T::kBytes);
-      T::load(sA, &a_main, &a_tail, bar_load, ha, 0, pol);
-      T::load(sB, &b_main, &b_tail, bar_load, hb, 0, pol);
+      T::load(sA, &a_map, bar_load, ha, 0, pol);
+      T::load(sB, &b_map, bar_load, hb, 0, pol);
     } else {
       mbar_expect_tx(bar_load, T::kBytes);
-      T::load(sB, &b_main, &b_tail, bar_load, hb, 0, pol);
+      T::load(sB, &b_map, bar_load, hb, 0, pol);
     }
     mbar_wait(bar_load, 0);
     tc_fence_after();
@@ -93,21 +92,11 @@ probe_kernel(int variant, const __grid_constant__ CUtensorMap a_main, const __gr
       const uint32_t id = idesc_bf16(128, 128, 0, 0);
       for (int kk = 0; kk < T::kKSteps; ++kk) mma_ss(tmem, T::desc_kmajor(sA, kk), T::desc_kmajor(sB, kk), id, kk > 0);
     } else if (variant == 1) {
-      const uint32_t idm = idesc_bf16(128, T::kMainN, 0, 1);
-      for (int kk = 0; kk < 8; ++kk) mma_ts(tmem, tmem + 128 + kk * 8, T::desc_mn_main(sB, kk), idm, kk > 0);
-      if constexpr (T::kTail) {
-        const uint32_t idt = idesc_bf16(128, 16, 0, 1);
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tmem + T::kMainN, tmem + 128 + kk * 8, T::desc_mn_tail(sB, kk), idt, kk > 0);
-      }
+      const uint32_t idm = idesc_bf16(128, D, 0, 1);
+      for (int kk = 0; kk < 8; ++kk) mma_ts(tmem, tmem + 128 + kk * 8, T::desc_mn(sB, kk), idm, kk > 0);
     } else {
-      const uint32_t idm = idesc_bf16(128, T::kMainN, 1, 1);
-      for (int kk = 0; kk < 8; ++kk) mma_ss(tmem, desc_a_mn_sw128(sA, kk), T::desc_mn_main(sB, kk), idm, kk > 0);
-      if constexpr (T::kTail) {
-        const uint32_t idt = idesc_bf16(128, 16, 1, 1);
-        for (int kk = 0; kk < 8; ++kk)
-          mma_ss(tmem + T::kMainN, desc_a_mn_sw128(sA, kk), T::desc_mn_tail(sB, kk), idt, kk > 0);
-      }
+      const uint32_t idm = idesc_bf16(128, D, 1, 1);
+      for (int kk = 0; kk < 8; ++kk) mma_ss(tmem, desc_a_mn_sw128(sA, kk), T::desc_mn(sB, kk), idm, kk > 0);
     }
     mma_commit(bar_mma);
   }
@@ -129,18 +118,13 @@ probe_kernel(int variant, const __grid_constant__ CUtensorMap a_main, const __gr
 
 template <int D>
 int run_probe(int variant, const void* a, const void* b, int H, int rows, void* out, cudaStream_t stream) {
-  CUtensorMap am{}, at{}, bm{}, bt{};
-  const CUtensorMapSwizzle s128 = CU_TENSOR_MAP_SWIZZLE_128B, s32 = CU_TENSOR_MAP_SWIZZLE_32B;
-  if (variant == 0) {
-    if (!make_tmap_rows_heads_dim(&am, a, rows, H, D, 64, 128, s128)) return 1;
-    if (!make_tmap_rows_heads_dim(&at, a, rows, H, D, 16, 128, s32)) return 1;
-  }
-  if (!make_tmap_rows_heads_dim(&bm, b, rows, H, D, 64, 128, s128)) return 1;
-  if (!make_tmap_rows_heads_dim(&bt, b, rows, H, D, 16, 128, s32)) return 1;
-  if (variant != 0) am = bm, at = bt;
+  CUtensorMap am{}, bm{};
+  if (variant == 0 && !make_tile_tmap<D>(&am, a, rows, H)) return 1;
+  if (!make_tile_tmap<D>(&bm, b, rows, H)) return 1;
+  if (variant != 0) am = bm;
   const int smem = 32768 * 2 + 1024;
   cudaFuncSetAttribute(probe_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  probe_kernel<D><<<1, 128, smem, stream>>>(variant, am, at, bm, bt, (const __nv_bfloat16*)a, H - 1, H - 1,
+  probe_kernel<D><<<1, 128, smem, stream>>>(variant, am, bm, (const __nv_bfloat16*)a, H - 1, H - 1,
                                             (float*)out);
   return (int)cudaGetLastError();
 }

@@ -17,6 +17,11 @@ __device__ __forceinline__ uint32_t mn_sw128_offset(int m, int k) {
 __device__ __forceinline__ uint64_t desc_a_mn_sw128(uint32_t base, int kk) {
   return ptx::smem_desc(base + kk * 2048, 16384, 1024, ptx::kSw128);
 }
+// The same bytes read as a K-major A operand [128 (M) x 128 (K)] with M = the former K index (rows of 128 B,
+// 8-row groups 1 KB apart, the two 64-element K atoms 16 KB apart): contraction step kk = 16 elements.
+__device__ __forceinline__ uint64_t desc_a_kmajor_sw128(uint32_t base, int kk) {
+  return ptx::smem_desc(base + (kk >> 2) * 16384 + (kk & 3) * 32, 16, 1024, ptx::kSw128);
+}
 __device__ __forceinline__ void st_shared_v4(uint32_t addr, const uint32_t (&w)[4]) {
   asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(addr), "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3])
                : "memory");

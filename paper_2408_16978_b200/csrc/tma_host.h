@@ -40,6 +40,13 @@ inline bool make_tmap_rows_heads_dim(CUtensorMap* m, const void* base, uint64_t 
   return r == CUDA_SUCCESS;
 }
 
+// Tensor map of the attention operand tiles (attn_tile.cuh): box = one swizzle atom of 128 rows.
+template <int D>
+inline bool make_tile_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint32_t heads) {
+  if (D == 80) return make_tmap_rows_heads_dim(m, base, rows, heads, D, 16, 128, CU_TENSOR_MAP_SWIZZLE_32B);
+  return make_tmap_rows_heads_dim(m, base, rows, heads, D, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+}
+
 // Tensor map over an fp32 tensor [rows][heads][head_dim] without swizzle (used for TMA reduce-add into
 // the dq accumulator).  Box = {box_cols, 1, box_rows}.
 inline bool make_tmap_f32_rows_heads_dim(CUtensorMap* m, const void* base, uint64_t rows, uint32_t heads,
