@@ -159,14 +159,13 @@ def run_ours(args):
     import torch
     import torch.distributed as dist
 
-    from paper_2408_16978_b200 import _lib, fpdt
+    from paper_2408_16978_b200 import _lib, distributed, fpdt
     import fpdt_inputs as gen
 
     rank, world, local = dist_env()
     assert world == args.gpus, f"--gpus {args.gpus} but WORLD_SIZE={world}"
     torch.cuda.set_device(local)
-    if world > 1:
-        dist.init_process_group("gloo", rank=rank, world_size=world)
+    distributed.init_process_group(rank, world, "gloo")
     W = WORKLOAD
     S, Hq, Hkv, d, C = W["S"], W["Hq"], W["Hkv"], W["d"], W["C"]
     if args.seq:
@@ -177,11 +176,7 @@ def run_ours(args):
     offload = args.offload
 
     # NCCL id through torch.distributed (plumbing only)
-    nid = None
-    if world > 1:
-        obj = [fpdt.fpdt_get_unique_id() if rank == 0 else None]
-        dist.broadcast_object_list(obj, src=0)
-        nid = obj[0]
+    nid = distributed.broadcast_nccl_id(rank, world, fpdt.fpdt_get_unique_id)
     ctx = fpdt.FPDTContext(world, rank, nid, local)
     genlib = _lib.load_generator()
     bf = torch.bfloat16
@@ -205,15 +200,10 @@ def run_ours(args):
                            0.0, stream)
 
     def barrier():
-        if world > 1:
-            dist.barrier()
+        distributed.barrier(world)
 
     def max_over_ranks(x):
-        if world == 1:
-            return x
-        t = torch.tensor([x], dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        return float(t.item())
+        return distributed.max_over_ranks(x, world)
 
     for _ in range(args.warmup):
         step()

@@ -75,6 +75,18 @@ int fpdt_get_unique_id(unsigned char id[128]);
 int fpdt_ctx_create(int world_size, int rank, const unsigned char* nccl_id, int device, size_t host_arena_bytes,
                     fpdt_ctx** out);
 
+/* In-process group: world_size ranks living in ONE process on ONE device `device`, one host thread per rank
+ * (single-GPU multi-rank testing of the p > 1 path; SURVEY §8(e) "fallback if only 1 GPU is granted").
+ * Contexts made with fpdt_ctx_create_local replace NCCL's all-to-all by a copy-engine exchange with exactly
+ * ncclAlltoAll's layout (receive block q = rank q's send block r); packing, scheduling, offload and the reverse
+ * all-to-alls are the same code as the NCCL path.  Rules: every rank's calls run on their own host thread and
+ * their own `stream` (sharing one stream across ranks can deadlock the device), all ranks make the same calls;
+ * a failing rank leaves the others blocked in the group barrier.  The group must outlive its contexts. */
+typedef struct fpdt_group fpdt_group;
+int fpdt_group_create(int world_size, int device, fpdt_group** out);
+int fpdt_group_destroy(fpdt_group* group);
+int fpdt_ctx_create_local(fpdt_group* group, int rank, int device, size_t host_arena_bytes, fpdt_ctx** out);
+
 /* Release everything the context owns (synchronises the context's streams first). */
 int fpdt_ctx_destroy(fpdt_ctx* ctx);
 

@@ -17,9 +17,11 @@
 #include <nccl.h>
 
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
 #include <functional>
+#include <mutex>
 #include <string>
 #include <vector>
 
@@ -97,9 +99,34 @@ enum BufId {
 
 }  // namespace
 
+// In-process group (fpdt_group_create): world_size ranks in ONE process on ONE device, one host thread per
+// rank.  Its all-to-all is a copy-engine exchange with NCCL's send/recv layout (recv block q = rank q's send
+// block r); everything else is the code the NCCL path runs.  For single-GPU multi-rank tests.
+struct fpdt_group {
+  int p = 1;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  int64_t generation = 0;
+  std::vector<const void*> send;
+  std::vector<cudaEvent_t> ev_sent, ev_read;
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const int64_t gen = generation;
+    if (++arrived == p) {
+      arrived = 0;
+      ++generation;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return generation != gen; });
+    }
+  }
+};
+
 struct fpdt_ctx {
   int p = 1, rank = 0, device = 0;
   ncclComm_t comm = nullptr;
+  fpdt_group* group = nullptr;  // non-null: in-process group instead of NCCL
   cudaStream_t s_comm = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   uint8_t* host = nullptr;
   size_t host_bytes = 0;
@@ -232,10 +259,33 @@ void d2h_2d(fpdt_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spi
   ctx->stats.bytes_d2h += (int64_t)(width * rows);
 }
 
+// All-to-all on the comm stream: send [p][count] -> recv [p][count], recv block q = rank q's send block `rank`.
 void alltoall(fpdt_ctx* ctx, const void* send, void* recv, size_t count_per_peer, int dtype) {
-  FPDT_CHECK_NCCL(ncclAlltoAll(send, recv, count_per_peer, dtype == FPDT_BF16 ? ncclBfloat16 : ncclFloat32, ctx->comm,
-                               ctx->s_comm));
-  ctx->stats.bytes_a2a += (int64_t)(count_per_peer * (ctx->p - 1) * (dtype == FPDT_BF16 ? 2 : 4));
+  const size_t eb = dtype == FPDT_BF16 ? 2 : 4;
+  if (!ctx->group) {
+    FPDT_CHECK_NCCL(ncclAlltoAll(send, recv, count_per_peer, dtype == FPDT_BF16 ? ncclBfloat16 : ncclFloat32,
+                                 ctx->comm, ctx->s_comm));
+  } else {
+    // local group: publish the send buffer and its ready event, pull every peer's block, then hold the
+    // comm stream until every peer has read ours (a send buffer is rewritten only after that).
+    fpdt_group* g = ctx->group;
+    const int r = ctx->rank, p = ctx->p;
+    const size_t bytes = count_per_peer * eb;
+    g->send[r] = send;
+    FPDT_CHECK_CUDA(cudaEventRecord(g->ev_sent[r], ctx->s_comm));
+    g->barrier();
+    for (int q = 0; q < p; ++q) {
+      FPDT_CHECK_CUDA(cudaStreamWaitEvent(ctx->s_comm, g->ev_sent[q], 0));
+      FPDT_CHECK_CUDA(cudaMemcpyAsync(static_cast<uint8_t*>(recv) + q * bytes,
+                                      static_cast<const uint8_t*>(g->send[q]) + r * bytes, bytes,
+                                      cudaMemcpyDeviceToDevice, ctx->s_comm));
+    }
+    FPDT_CHECK_CUDA(cudaEventRecord(g->ev_read[r], ctx->s_comm));
+    g->barrier();
+    for (int q = 0; q < p; ++q) FPDT_CHECK_CUDA(cudaStreamWaitEvent(ctx->s_comm, g->ev_read[q], 0));
+    g->barrier();  // nobody re-records ev_sent / ev_read before every rank has enqueued its waits
+  }
+  ctx->stats.bytes_a2a += (int64_t)(count_per_peer * (ctx->p - 1) * eb);
 }
 
 struct TimedScope {
@@ -461,7 +511,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
         float* lt = (float*)dev(ctx, B_LSE_T, (size_t)C * hq * 4);
         float* lr = (float*)dev(ctx, B_LSE_RECV, (size_t)C * hq * 4);
         FPDT_CHECK_LAUNCH(launch_lse_to_user(lse_save + m * C, c.S, C, hq, lt, hq, 0, ctx->s_comm));
-        FPDT_CHECK_NCCL(ncclAlltoAll(lt, lr, (size_t)c.c * hq, ncclFloat32, ctx->comm, ctx->s_comm));
+        alltoall(ctx, lt, lr, (size_t)c.c * hq, FPDT_FP32);
         // unpack [p][c][hq] -> [c][Hq]: treat each row of hq floats as one head of hq*4 bytes... use 1-float heads
         for (int r = 0; r < p; ++r)
           FPDT_CHECK_CUDA(cudaMemcpy2DAsync(lse + (size_t)m * c.c * c.Hq + (size_t)r * hq, (size_t)c.Hq * 4,
@@ -756,13 +806,12 @@ int fpdt_get_unique_id(unsigned char id[128]) {
   });
 }
 
-int fpdt_ctx_create(int world_size, int rank, const unsigned char* nccl_id, int device, size_t host_arena_bytes,
-                    fpdt_ctx** out) {
-  return run([&] {
-    if (!out || world_size < 1 || rank < 0 || rank >= world_size) fail(FPDT_ERR_ARG, "bad world_size/rank/out");
-    if (world_size > 1 && !nccl_id) fail(FPDT_ERR_ARG, "nccl_id required for world_size > 1");
+namespace {
+fpdt_ctx* create_ctx(int world_size, int rank, const unsigned char* nccl_id, fpdt_group* group, int device,
+                     size_t host_arena_bytes) {
     FPDT_CHECK_CUDA(cudaSetDevice(device));
     fpdt_ctx* ctx = new fpdt_ctx();
+    ctx->group = group;
     ctx->p = world_size;
     ctx->rank = rank;
     ctx->device = device;
@@ -780,13 +829,56 @@ int fpdt_ctx_create(int world_size, int rank, const unsigned char* nccl_id, int 
                            &ctx->ev_recv_used_d[b]};
       for (auto e : pe) FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
-    if (world_size > 1) {
+    if (world_size > 1 && !group) {
       ncclUniqueId u;
       std::memcpy(u.internal, nccl_id, 128);
       FPDT_CHECK_NCCL(ncclCommInitRank(&ctx->comm, world_size, u, rank));
     }
     if (host_arena_bytes) ensure_host(ctx, host_arena_bytes);
-    *out = ctx;
+    return ctx;
+}
+}  // namespace
+
+int fpdt_ctx_create(int world_size, int rank, const unsigned char* nccl_id, int device, size_t host_arena_bytes,
+                    fpdt_ctx** out) {
+  return run([&] {
+    if (!out || world_size < 1 || rank < 0 || rank >= world_size) fail(FPDT_ERR_ARG, "bad world_size/rank/out");
+    if (world_size > 1 && !nccl_id) fail(FPDT_ERR_ARG, "nccl_id required for world_size > 1");
+    *out = create_ctx(world_size, rank, nccl_id, nullptr, device, host_arena_bytes);
+  });
+}
+
+int fpdt_group_create(int world_size, int device, fpdt_group** out) {
+  return run([&] {
+    if (!out || world_size < 1) fail(FPDT_ERR_ARG, "bad world_size/out");
+    FPDT_CHECK_CUDA(cudaSetDevice(device));
+    fpdt_group* g = new fpdt_group();
+    g->p = world_size;
+    g->send.assign(world_size, nullptr);
+    g->ev_sent.assign(world_size, nullptr);
+    g->ev_read.assign(world_size, nullptr);
+    for (int r = 0; r < world_size; ++r) {
+      FPDT_CHECK_CUDA(cudaEventCreateWithFlags(&g->ev_sent[r], cudaEventDisableTiming));
+      FPDT_CHECK_CUDA(cudaEventCreateWithFlags(&g->ev_read[r], cudaEventDisableTiming));
+    }
+    *out = g;
+  });
+}
+
+int fpdt_group_destroy(fpdt_group* g) {
+  if (!g) return FPDT_OK;
+  for (auto e : g->ev_sent)
+    if (e) cudaEventDestroy(e);
+  for (auto e : g->ev_read)
+    if (e) cudaEventDestroy(e);
+  delete g;
+  return FPDT_OK;
+}
+
+int fpdt_ctx_create_local(fpdt_group* group, int rank, int device, size_t host_arena_bytes, fpdt_ctx** out) {
+  return run([&] {
+    if (!out || !group || rank < 0 || rank >= group->p) fail(FPDT_ERR_ARG, "bad group/rank/out");
+    *out = create_ctx(group->p, rank, nullptr, group, device, host_arena_bytes);
   });
 }
 

@@ -21,7 +21,8 @@ STATUS_NAMES = {0: "FPDT_OK", 1: "FPDT_ERR_ARG", 2: "FPDT_ERR_DIVISIBILITY", 3: 
 # names of every symbol include/fpdt.h declares (checked by the CPU tests against the built library)
 EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_attn_fwd", "fpdt_attn_bwd",
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
-            "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair")
+            "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair", "fpdt_group_create",
+            "fpdt_group_destroy", "fpdt_ctx_create_local")
 
 
 class FpdtError(RuntimeError):
@@ -45,6 +46,12 @@ def _declare(lib):
     lib.fpdt_get_unique_id.restype = c_int
     lib.fpdt_ctx_create.argtypes = [c_int, c_int, ctypes.c_char_p, c_int, ctypes.c_size_t, ctypes.POINTER(P)]
     lib.fpdt_ctx_create.restype = c_int
+    lib.fpdt_group_create.argtypes = [c_int, c_int, ctypes.POINTER(P)]
+    lib.fpdt_group_create.restype = c_int
+    lib.fpdt_group_destroy.argtypes = [P]
+    lib.fpdt_group_destroy.restype = c_int
+    lib.fpdt_ctx_create_local.argtypes = [P, c_int, c_int, ctypes.c_size_t, ctypes.POINTER(P)]
+    lib.fpdt_ctx_create_local.restype = c_int
     lib.fpdt_ctx_destroy.argtypes = [P]
     lib.fpdt_ctx_destroy.restype = c_int
     lib.fpdt_attn_fwd.argtypes = [P, P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int64, c_int, c_int, c_int,
@@ -102,14 +109,34 @@ def fpdt_global_token(local_t: int, chunk_size: int, world_size: int, rank: int)
     return lib().fpdt_global_token(local_t, chunk_size, world_size, rank)
 
 
+class LocalGroup:
+    """fpdt_group: world_size ranks in this process on one device (single-GPU multi-rank tests)."""
+
+    def __init__(self, world_size: int, device: int = 0):
+        self.world_size = world_size
+        h = c_void_p()
+        _check(lib().fpdt_group_create(world_size, device, ctypes.byref(h)))
+        self.handle = h
+
+    def close(self):
+        if self.handle:
+            _check(lib().fpdt_group_destroy(self.handle))
+            self.handle = None
+
+
 class FPDTContext:
-    """Owns one fpdt_ctx (NCCL comm, streams, pinned host chunk store, device slots, saved state)."""
+    """Owns one fpdt_ctx (NCCL comm or local group, streams, pinned host chunk store, device slots, saved
+    state)."""
 
     def __init__(self, world_size: int = 1, rank: int = 0, nccl_id: bytes | None = None, device: int = 0,
-                 host_arena_bytes: int = 0):
+                 host_arena_bytes: int = 0, group: LocalGroup | None = None):
         self.world_size, self.rank = world_size, rank
         h = c_void_p()
-        _check(lib().fpdt_ctx_create(world_size, rank, nccl_id, device, host_arena_bytes, ctypes.byref(h)))
+        if group is not None:
+            assert group.world_size == world_size
+            _check(lib().fpdt_ctx_create_local(group.handle, rank, device, host_arena_bytes, ctypes.byref(h)))
+        else:
+            _check(lib().fpdt_ctx_create(world_size, rank, nccl_id, device, host_arena_bytes, ctypes.byref(h)))
         self.handle = h
 
     def close(self):

@@ -1,0 +1,96 @@
+"""The p > 1 path (all-to-all pack/unpack, per-chunk exchange, head-sharded attention, reverse exchange) on ONE
+GPU: p ranks of an in-process group (fpdt_group_create), one host thread and one stream per rank.
+
+Checks (SURVEY §8(c) c.3 "invariances", c.5): world-size invariance against the p = 1 run of the same GLOBAL
+inputs — bitwise for O, lse, dK, dV (per-head arithmetic is identical and there are no atomics on them),
+within tolerance for dQ (its fp32 reduce-add order varies) — and oracle parity at p > 1."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import fpdt_inputs as gen
+from fpdt_testlib import TOL, oracle_full, rel_err
+
+pytestmark = pytest.mark.gpu
+
+
+def run_group(x: dict, p: int, C: int, dtype: str, offload: int) -> dict:
+    """Shard the global inputs x by the rank-ordinal contract, run fwd+bwd on p local ranks, unshard."""
+    from paper_2408_16978_b200 import fpdt
+    S, Hq, d = x["q"].shape
+    Hkv = x["k"].shape[1]
+    s_local = S // p
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    code = fpdt.dtype_code(tdt)
+    group = fpdt.LocalGroup(p) if p > 1 else None
+    rows = [gen.global_tokens_of_rank(r, p, s_local, C) for r in range(p)]
+    out = {n: np.zeros(x[m].shape, np.float32) for n, m in (("o", "q"), ("dq", "q"), ("dk", "k"), ("dv", "v"))}
+    out["lse"] = np.zeros((S, Hq), np.float32)
+    errors = []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                q, k, v, do = (torch.tensor(x[n][rows[r]]).to(tdt).cuda().contiguous() for n in ("q", "k", "v", "do"))
+                o = torch.empty_like(q)
+                lse = torch.empty(s_local, Hq, dtype=torch.float32, device="cuda")
+                dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+            stream.synchronize()
+            ctx = fpdt.FPDTContext(p, r, group=group) if p > 1 else fpdt.FPDTContext()
+            fpdt.fpdt_attn_fwd(ctx, q, k, v, o, lse, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
+            fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
+            stream.synchronize()
+            for n, t in (("o", o), ("lse", lse), ("dq", dq), ("dk", dk), ("dv", dv)):
+                out[n][rows[r]] = t.float().cpu().numpy()
+            ctx.close()
+        except Exception as e:  # surfaced in the main thread
+            errors.append((r, e))
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(p)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in threads), "a rank hung"
+    if group is not None:
+        group.close()
+    assert not errors, errors
+    return out
+
+
+@pytest.mark.parametrize("p", [2, 4])
+@pytest.mark.parametrize("offload", [1, 0])
+def test_world_size_invariance_bf16(p, offload):
+    S, Hq, Hkv, d, C = 2048, 8, 4, 80, 512      # u = 4 chunks, GQA G = 2, head_dim of GPT-2.7B
+    x = gen.make_inputs("drift", 7, S, Hq, Hkv, d)
+    ref = run_group(x, 1, C, "bf16", offload)
+    got = run_group(x, p, C, "bf16", offload)
+    for n in ("o", "lse", "dk", "dv"):
+        assert np.array_equal(got[n], ref[n]), (n, rel_err(got[n], ref[n]))
+    assert rel_err(got["dq"], ref["dq"]) < 1e-3
+
+
+@pytest.mark.parametrize("p,S,Hq,Hkv,d,C", [
+    (2, 2048, 4, 4, 64, 512),      # MHA, u = 4
+    (4, 2048, 8, 4, 128, 1024),    # GQA G = 2, u = 2, c = 256 rows per rank
+    (2, 1024, 8, 2, 128, 256),     # GQA G = 4 (Llama-3 8B ratio), smallest chunk
+])
+def test_oracle_parity_multirank_bf16(p, S, Hq, Hkv, d, C):
+    x = gen.make_inputs("normal", 8, S, Hq, Hkv, d)
+    ref = oracle_full(x)
+    got = run_group(x, p, C, "bf16", 1)
+    errs = {n: rel_err(got[n], ref[n]) for n in ("o", "lse", "dq", "dk", "dv")}
+    assert all(e <= TOL["bf16"] for e in errs.values()), errs
+
+
+def test_oracle_parity_multirank_fp32():
+    S, Hq, Hkv, d, C = 1024, 4, 2, 64, 512
+    x = gen.make_inputs("sink", 9, S, Hq, Hkv, d)
+    ref = oracle_full(x)
+    got = run_group(x, 2, C, "fp32", 1)
+    errs = {n: rel_err(got[n], ref[n]) for n in ("o", "lse", "dq", "dk", "dv")}
+    assert all(e <= TOL["fp32"] for e in errs.values()), errs
