@@ -18,6 +18,8 @@ NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 COMMON = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "-Xcompiler", "-O2",
                  "--expt-relaxed-constexpr", "-cudart", "static"]
+# experiment knobs (e.g. FPDT_NVCC_DEFINES="-DFPDT_BWD_EXP=1"); empty for every product build
+COMMON += os.environ.get("FPDT_NVCC_DEFINES", "").split()
 
 
 def _nccl_dirs():

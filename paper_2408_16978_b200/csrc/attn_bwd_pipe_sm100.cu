@@ -1,0 +1,538 @@
+// Backward chunk-pair attention for sm_100a, head_dim 64 / 80: software-pipelined across query tiles.
+//
+// Same operation as attn_bwd_sm100.cu (one (key/value chunk j, query chunk i) step of FPDT's nested backward
+// loop, fig:bw_db; KV-stationary CTA = one 128-row key/value tile of one KV head walking the
+// query tiles of the range and the G query heads of its group):
+//   S^T  = K Q^T            P^T  = exp2(S^T*scale*log2e - lse2)       (recompute)
+//   dP^T = V dO^T           dS^T = P^T o (dP^T - D)
+//   dV  += P^T dO           dK  += dS^T Q          dQ_partial = dS K  (TMA bulk reduce-add into fp32 dq_acc)
+//
+// What differs from the non-pipelined kernel: P^T_n and dS^T_n (bf16) are written into the dP^T TMEM columns
+// once the softmax warps hold dP^T_n in registers, so the S^T columns hold nothing but S^T and S^T_{n+1} is
+// issued as soon as S^T_n has been read out — it runs during the exponentials of tile n, and the softmax warps go
+// straight from dS_n to the exponentials of tile n+1.  dV and dK are TS-MMAs (A from TMEM): shared memory, not
+// the tensor pipe, is the scarce resource here (128 B/clk/SM; an SS-MMA with M = 128, N <= 128 already needs all
+// of it), so per query tile only dQ = dS K (A = the dS smem tile) reads two smem operands.  Shared-memory bytes per
+// tile (d = 80): TMA Q, dO 40K + MMA operands 172K + dS 32K + dQ staging 80K.
+// Element-wise math uses packed f32x2 FMA-pipe instructions (FFMA2/FADD2/FMUL2); a fraction of the
+// exponentials run as a polynomial on the FMA pipe (FA4-style MUFU offload).
+//
+// Warps (512 threads = 4 warpgroups, registers rebalanced with setmaxnreg):
+//   WG0 (0-3)   softmax-gradient, query columns [0,64)   (thread = key row = TMEM lane); final dK    168 regs
+//   WG1 (4-7)   softmax-gradient, query columns [64,128)                                ; final dV    168 regs
+//   WG2 (8-11)  dQ read-out (thread = query row) -> smem staging -> TMA bulk reduce-add              104 regs
+//   WG3 (12)    TMA producer; (13) TMEM allocator + single-thread MMA issuer; (14, 15) idle          72 regs
+// Shared memory (d = 80: 215 KB): K, V | 3 Q stages (+ lse2/D rows) | 2 dO stages | dS | dQ staging.
+// TMEM: S^T [0,128) | dP^T [128,256), then per query half h: P^T [128+64h, +32), dS^T [160+64h, +32) (bf16) |
+//       dQ [256,256+D) | dK | dV  (496 columns at d = 80).
+#include "attn_tile.cuh"
+#include "kernels.h"
+#include "smem_layout.cuh"
+#include "tma_host.h"
+
+#include <cstdlib>
+#include <cstring>
+
+namespace fpdt {
+namespace {
+
+using namespace ptx;
+
+constexpr int kThreads = 512;
+#ifndef FPDT_BWD_EXP
+#define FPDT_BWD_EXP 0  // timing experiments only (wrong results): 1 no dQ reduce, 2 no dQ staging/reduce,
+                       // 3 no stats loads, 4 = 2 + 3
+#endif
+#ifndef FPDT_BWD_POLY_EVERY
+#define FPDT_BWD_POLY_EVERY 4  // one exponential pair in FPDT_BWD_POLY_EVERY goes to the FMA-pipe polynomial
+#endif
+
+template <int D>
+struct PipeCfg {
+  using T = Tile<D>;
+  static constexpr int QS = 3, OS = 2;
+  static constexpr int TB = T::kBytes;
+  static constexpr int kDS = 128 * 128 * 2;  // dS (bf16)
+  static constexpr int kDQ = 128 * D * 4;
+  static constexpr int kStats = 1024;  // lse2[128] + D[128] fp32
+  static constexpr int oK = 0, oV = TB, oQ = 2 * TB, oO = oQ + QS * TB;
+  static constexpr int oDS = ((oO + OS * TB + 1023) / 1024) * 1024;
+  static constexpr int oDQ = oDS + kDS;
+  static constexpr int oStats = oDQ + kDQ;
+  static constexpr int oBars = oStats + QS * kStats;
+  static constexpr int kSmem = oBars + 256;
+  static_assert(kSmem <= 227 * 1024, "shared memory budget");
+  static constexpr uint32_t tS = 0, tdP = 128, tdQ = 256, tdK = 256 + D, tdV = 256 + 2 * D;
+  static_assert(256 + 3 * D <= 512, "TMEM budget");
+};
+
+struct TmapSet {
+  CUtensorMap q, k, v, o, dq32, dq16;  // dq32: 32-column fp32 boxes, 128B swizzle; dq16: 16 columns, 64B swizzle
+};
+
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
+// 2^x for a pair on the FMA pipe: x = j + f, j = rint(x), f in [-1/2, 1/2]; degree-3 minimax for 2^f (max rel.
+// error 7.5e-5, far below bf16's 2^-9); the exponent is added as an integer.  x is clamped to >= -127.
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 kRnd = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 j = __fadd2_rn(x, kRnd);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(kRnd, make_float2(-j.x, -j.y)));
+  float2 p = __ffma2_rn(f, make_float2(0.055169348f, 0.055169348f), make_float2(0.24260798f, 0.24260798f));
+  p = __ffma2_rn(p, f, make_float2(0.69326115f, 0.69326115f));
+  p = __ffma2_rn(p, f, make_float2(0.9999283f, 0.9999283f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
+
+__device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2) {
+  asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
+                   reinterpret_cast<uint64_t>(m)),
+               "r"(src), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ float4 lds4(const float* p) {
+  if (FPDT_BWD_EXP >= 3) return make_float4(1.f, 2.f, 3.f, 4.f);
+  return *reinterpret_cast<const float4*>(p);
+}
+
+template <int D, bool kRedDQ>
+__global__ void __launch_bounds__(kThreads, 1)
+attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdArgs a) {
+  using T = Tile<D>;
+  using C = PipeCfg<D>;
+  constexpr int QS = C::QS, OS = C::OS;
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const uint32_t base = smem_u32(smem);
+  const uint32_t sK = base + C::oK, sV = base + C::oV, sDS = base + C::oDS, sDQ = base + C::oDQ;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::oBars);
+  auto bar = [&](int i) { return smem_u32(&bars[i]); };
+  // barrier indices
+  constexpr int B_KV = 0, B_QF = 1, B_QE = B_QF + QS, B_OF = B_QE + QS, B_OE = B_OF + OS, B_S = B_OE + OS,
+                B_SFREE = B_S + 1, B_DP = B_SFREE + 1, B_P = B_DP + 1, B_DS = B_P + 1,
+                B_DSFREE = B_DS + 1, B_DQF = B_DSFREE + 1, B_DQE = B_DQF + 1, B_KVDONE = B_DQE + 1,
+                B_NUM = B_KVDONE + 1;
+  static_assert(B_NUM <= 30, "barrier area");
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::oBars + 30 * 8);
+
+  const uint32_t warp = warp_id(), lane = lane_id();
+  const int kt = blockIdx.x;
+  const int g = blockIdx.y;
+  const int G = a.G;
+  const int64_t kv_base = a.kv_pos0 + (int64_t)kt * 128;
+  int qt_first = 0;
+  const int n_qt_total = a.n_q_rows / 128;
+  if (a.causal) {
+    const int64_t rel = kv_base - a.q_pos0;  // first query tile that can see this key tile
+    if (rel > 0) qt_first = (int)(rel / 128);
+    if (qt_first > n_qt_total) qt_first = n_qt_total;
+  }
+  const int n_iter = (n_qt_total - qt_first) * G;
+  const bool tracing = a.trace != nullptr && blockIdx.x == a.trace_cta && blockIdx.y == 0;
+#define TRACE(ev, n)                                                        \
+  do {                                                                      \
+    if (tracing && (n) < 4096) a.trace[(ev) * 4096 + (n)] = clock64();      \
+  } while (0)
+
+  if (warp == 13) tmem_alloc<512>(smem_u32(tmem_slot));
+  if (warp == 12 && lane == 0) {
+    mbar_init(bar(B_KV), 1);
+    for (int s = 0; s < QS; ++s) {
+      mbar_init(bar(B_QF + s), 1);
+      mbar_init(bar(B_QE + s), 1);
+    }
+    for (int s = 0; s < OS; ++s) {
+      mbar_init(bar(B_OF + s), 1);
+      mbar_init(bar(B_OE + s), 1);
+    }
+    mbar_init(bar(B_S), 1);
+    mbar_init(bar(B_SFREE), 256);
+    mbar_init(bar(B_DP), 1);
+    mbar_init(bar(B_P), 256);
+    mbar_init(bar(B_DS), 256);
+    mbar_init(bar(B_DSFREE), 1);
+    mbar_init(bar(B_DQF), 1);
+    mbar_init(bar(B_DQE), 128);
+    mbar_init(bar(B_KVDONE), 1);
+    fence_mbar_init();
+  }
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  const uint32_t tmem = *tmem_slot;
+
+  if (warp >= 12) {
+    setmaxnreg_dec<72>();
+    if (warp == 12) {
+      // ---------------------------------------------------------------- TMA producer
+      if (elect_one() && n_iter > 0) {
+        const uint64_t pol_kv = policy_evict_first(), pol_q = policy_evict_last();
+        mbar_expect_tx(bar(B_KV), 2 * C::TB);
+        const int krow = (int)(a.kv_row0 + (int64_t)kt * 128);
+        T::load(sK, &tm.k, bar(B_KV), a.k.head0 + g, krow, pol_kv);
+        T::load(sV, &tm.v, bar(B_KV), a.v.head0 + g, krow, pol_kv);
+        for (int n = 0; n < n_iter; ++n) {
+          const int qs = n % QS, os = n % OS;
+          const int qt = qt_first + n / G, h = g * G + n % G;
+          const int qrow = (int)(a.q_row0 + (int64_t)qt * 128);
+          if (n >= QS) mbar_wait(bar(B_QE + qs), ((n / QS) - 1) & 1);
+          TRACE(12, n);
+          const uint32_t fq = bar(B_QF + qs);
+          const uint32_t stats = base + C::oStats + qs * C::kStats;
+          mbar_expect_tx(fq, C::TB + 1024);
+          T::load(base + C::oQ + qs * C::TB, &tm.q, fq, a.q.head0 + h, qrow, pol_q);
+          bulk_load(stats, a.lse2 + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, fq);
+          bulk_load(stats + 512, a.Dstat + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, fq);
+          if (n >= OS) mbar_wait(bar(B_OE + os), ((n / OS) - 1) & 1);
+          mbar_expect_tx(bar(B_OF + os), C::TB);
+          T::load(base + C::oO + os * C::TB, &tm.o, bar(B_OF + os), a.dout.head0 + h, qrow, pol_q);
+        }
+      }
+    } else if (warp == 13) {
+      // ---------------------------------------------------------------- MMA issuer
+      if (elect_one() && n_iter > 0) {
+        const uint32_t idS = idesc_bf16(128, 128, 0, 0);  // S^T, dP^T: A (K or V rows), B (Q or dO rows) K-major
+        const uint32_t idG = idesc_bf16(128, D, 0, 1);    // dV, dK: A = P^T / dS^T K-major smem, B MN-major
+        const uint32_t idQ = idesc_bf16(128, D, 1, 1);    // dQ: A = dS MN-major smem, B = K MN-major
+        const uint32_t tS = tmem + C::tS, tdP = tmem + C::tdP, tdQ = tmem + C::tdQ, tdK = tmem + C::tdK,
+                       tdV = tmem + C::tdV;
+        auto sQ = [&](int n) { return base + C::oQ + (n % QS) * C::TB; };
+        auto sO = [&](int n) { return base + C::oO + (n % OS) * C::TB; };
+        auto issue_S = [&](int n) {
+          mbar_wait(bar(B_QF + n % QS), (n / QS) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < T::kKSteps; ++kk)
+            mma_ss(tS, T::desc_kmajor(sK, kk), T::desc_kmajor(sQ(n), kk), idS, kk > 0);
+          mma_commit(bar(B_S));
+        };
+        auto issue_dP = [&](int n) {
+          mbar_wait(bar(B_OF + n % OS), (n / OS) & 1);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < T::kKSteps; ++kk)
+            mma_ss(tdP, T::desc_kmajor(sV, kk), T::desc_kmajor(sO(n), kk), idS, kk > 0);
+          mma_commit(bar(B_DP));
+        };
+        mbar_wait(bar(B_KV), 0);
+        issue_S(0);
+        issue_dP(0);
+        // Issue order per query tile n (blocking waits: a spinning probe loop would steal the shared-memory pipe
+        // the tensor core reads its operands through):
+        //   S^T_{n+1}  after SFREE(n) (S^T_n read out) and Q_{n+1} loaded
+        //   dV_n       after P^T_n in TMEM
+        //   group n    dK_n, dP^T_{n+1}, dQ_n after dS^T_n in TMEM and dS_n in smem; dP^T_{n+1} overwrites P^T_n /
+        //              dS^T_n after dV_n and dK_n in issue order; dQ_n after dQ_{n-1} has been read out
+        for (int n = 0; n < n_iter; ++n) {
+          const bool more = n + 1 < n_iter;
+          if (more) {
+            mbar_wait(bar(B_SFREE), n & 1);
+            TRACE(6, n);
+            issue_S(n + 1);
+          }
+          // dV += P^T dO_n   (A = P^T in TMEM)
+          mbar_wait(bar(B_P), n & 1);
+          TRACE(4, n);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ts(tdV, tdP + 64 * (kk >> 2) + (kk & 3) * 8, T::desc_mn(sO(n), kk), idG, (n > 0 || kk > 0));
+          mma_commit(bar(B_OE + n % OS));  // dO_n consumed (dP_n precedes dV_n)
+          // dK += dS^T Q_n   (A = dS^T in TMEM); first, so that Q_n is released early
+          mbar_wait(bar(B_DS), n & 1);
+          TRACE(5, n);
+          tc_fence_after();
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk)
+            mma_ts(tdK, tdP + 64 * (kk >> 2) + 32 + (kk & 3) * 8, T::desc_mn(sQ(n), kk), idG, (n > 0 || kk > 0));
+          mma_commit(bar(B_QE + n % QS));  // Q_n consumed
+          if (more) issue_dP(n + 1);
+          // dQ_n = dS K   (A = the dS smem tile, MN-major)
+          if (n > 0) {
+            mbar_wait(bar(B_DQE), (n - 1) & 1);
+            tc_fence_after();
+          }
+#pragma unroll
+          for (int kk = 0; kk < 8; ++kk) mma_ss(tdQ, desc_a_mn_sw128(sDS, kk), T::desc_mn(sK, kk), idQ, kk > 0);
+          mma_commit(bar(B_DQF));
+          mma_commit(bar(B_DSFREE));
+          TRACE(8, n);
+        }
+        mma_commit(bar(B_KVDONE));
+      }
+    }
+  } else if (warp < 8) {
+    setmaxnreg_inc<168>();
+    // ------------------------------------------------------------------ softmax gradient (key rows)
+    const int half = warp >> 2;  // query columns [64*half, 64*half+64)
+    const int r = (warp & 3) * 32 + lane;
+    // TMEM addresses of this warp's lanes; the empty asm keeps them in registers (no per-iteration S2R)
+    uint32_t tS = tmem + C::tS + (((warp & 3) * 32) << 16) + 64 * half;
+    uint32_t tdP = tS + (C::tdP - C::tS);
+    asm volatile("" : "+r"(tS), "+r"(tdP));
+    // row r's 128-byte line in the SW128 tiles; the 16-byte chunk m8 of it lives at chunk m8 ^ (r & 7)
+    const uint32_t xr = (uint32_t)(r & 7) << 4;
+    const uint32_t sDSr = sDS + mn_sw128_offset(64 * half, r) - xr;
+    const int64_t kpos = kv_base + r;
+    const float sl2 = a.scale_log2;
+    for (int n = 0; n < n_iter; ++n) {
+      const int qt = qt_first + n / G;
+      const float* st = reinterpret_cast<const float*>(smem + C::oStats + (n % QS) * C::kStats) + 64 * half;
+      mbar_wait(bar(B_S), n & 1);
+      if (warp == 0 && lane == 0) TRACE(0, n);
+      tc_fence_after();
+      float p[64];
+      tmem_ld32(tS, reinterpret_cast<uint32_t*>(p));
+      tmem_ld32(tS + 32, reinterpret_cast<uint32_t*>(p) + 32);
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(bar(B_SFREE));
+      if (warp == 0 && lane == 0) TRACE(13, n);
+      // query column (within this half) < lim is masked: its query position is before the key position
+      const int64_t lim64 = (a.causal ? (kpos - (a.q_pos0 + (int64_t)qt * 128)) : -1) - 64 * half;
+      const int lim = (int)(lim64 < 0 ? 0 : (lim64 > 64 ? 64 : lim64));
+      if (__any_sync(0xffffffffu, lim > 0)) {
+        // tile straddling the diagonal: MUFU only (exact zeros under the mask)
+#pragma unroll
+        for (int i = 0; i < 64; i += 4) {
+          const float4 l = lds4(st + i);
+          const float2 x0 = __ffma2_rn(make_float2(p[i], p[i + 1]), make_float2(sl2, sl2), make_float2(-l.x, -l.y));
+          const float2 x1 =
+              __ffma2_rn(make_float2(p[i + 2], p[i + 3]), make_float2(sl2, sl2), make_float2(-l.z, -l.w));
+          p[i] = i < lim ? 0.f : ex2(x0.x);
+          p[i + 1] = i + 1 < lim ? 0.f : ex2(x0.y);
+          p[i + 2] = i + 2 < lim ? 0.f : ex2(x1.x);
+          p[i + 3] = i + 3 < lim ? 0.f : ex2(x1.y);
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; i += 4) {
+          const float4 l = lds4(st + i);
+          const float2 x0 = __ffma2_rn(make_float2(p[i], p[i + 1]), make_float2(sl2, sl2), make_float2(-l.x, -l.y));
+          const float2 x1 =
+              __ffma2_rn(make_float2(p[i + 2], p[i + 3]), make_float2(sl2, sl2), make_float2(-l.z, -l.w));
+          p[i] = ex2(x0.x);
+          p[i + 1] = ex2(x0.y);
+          if ((i / 4) % (FPDT_BWD_POLY_EVERY / 2) == (FPDT_BWD_POLY_EVERY / 2) - 1) {
+            const float2 e = ex2_poly2(x1);
+            p[i + 2] = e.x;
+            p[i + 3] = e.y;
+          } else {
+            p[i + 2] = ex2(x1.x);
+            p[i + 3] = ex2(x1.y);
+          }
+        }
+      }
+      if (warp == 0 && lane == 0) TRACE(14, n);
+      // dP^T_n -> registers; its TMEM columns then receive P^T_n and dS^T_n (bf16), the A operands of dV and dK
+      mbar_wait(bar(B_DP), n & 1);
+      if (warp == 0 && lane == 0) TRACE(2, n);
+      tc_fence_after();
+      float dp[64];
+      tmem_ld32(tdP, reinterpret_cast<uint32_t*>(dp));
+      tmem_ld32(tdP + 32, reinterpret_cast<uint32_t*>(dp) + 32);
+      tmem_wait_ld();
+      if (warp == 0 && lane == 0) TRACE(15, n);
+#pragma unroll
+      for (int c = 0; c < 64; c += 32) {
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) pk[i / 2] = pack_bf16x2(p[c + i], p[c + i + 1]);
+        tmem_st16(tdP + c / 2, pk);
+      }
+      tmem_wait_st();
+      tc_fence_before();
+      mbar_arrive(bar(B_P));
+      if (warp == 0 && lane == 0) TRACE(1, n);
+      // dS = P o (dP - D) -> TMEM (dS^T, A of dK) and smem (MN-major dS tile, A of dQ)
+      uint32_t pk[32];
+#pragma unroll
+      for (int i = 0; i < 64; i += 4) {
+        const float4 dd = lds4(st + 128 + i);
+        const float2 a0 = __fmul2_rn(make_float2(p[i], p[i + 1]),
+                                     __fadd2_rn(make_float2(dp[i], dp[i + 1]), make_float2(-dd.x, -dd.y)));
+        const float2 a1 = __fmul2_rn(make_float2(p[i + 2], p[i + 3]),
+                                     __fadd2_rn(make_float2(dp[i + 2], dp[i + 3]), make_float2(-dd.z, -dd.w)));
+        pk[i / 2] = pack_bf16x2(a0.x, a0.y);
+        pk[i / 2 + 1] = pack_bf16x2(a1.x, a1.y);
+      }
+      tmem_st16(tdP + 32, pk);
+      tmem_st16(tdP + 48, pk + 16);
+      if (n > 0) mbar_wait(bar(B_DSFREE), (n - 1) & 1);
+      if (warp == 0 && lane == 0) TRACE(10, n);
+#pragma unroll
+      for (int m8 = 0; m8 < 8; ++m8) {
+        const uint32_t w[4] = {pk[m8 * 4], pk[m8 * 4 + 1], pk[m8 * 4 + 2], pk[m8 * 4 + 3]};
+        st_shared_v4(sDSr + (((uint32_t)m8 << 4) ^ xr), w);
+      }
+      tmem_wait_st();
+      fence_async_shared();
+      tc_fence_before();
+      mbar_arrive(bar(B_DS));
+      if (warp == 0 && lane == 0) TRACE(3, n);
+    }
+    // ---- final dK (half 0) / dV (half 1), thread = key row
+    const int64_t row = (int64_t)kt * 128 + r;  // row within the launch's key range
+    const int hkv = a.hq / G;
+    float* acc = (half ? a.dv_acc : a.dk_acc) + (row * hkv + g) * D;
+    const float sc = half ? 1.f : a.scale;
+    __nv_bfloat16* out = reinterpret_cast<__nv_bfloat16*>(half ? a.dv_out : a.dk_out);
+    if (a.kv_final) out += row * a.kv_out_ld + (int64_t)(a.kv_out_head0 + g) * D;
+    if (n_iter > 0) {
+      mbar_wait(bar(B_KVDONE), 0);
+      tc_fence_after();
+    }
+    const uint32_t tacc = tmem + (half ? C::tdV : C::tdK) + (((warp & 3) * 32) << 16);
+#pragma unroll
+    for (int c = 0; c < D; c += 16) {
+      float v[16];
+      if (n_iter > 0) {
+        tmem_ld16(tacc + c, reinterpret_cast<uint32_t(&)[16]>(v));
+        tmem_wait_ld();
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] *= sc;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; ++i) v[i] = 0.f;
+      }
+      if (!a.kv_acc_init) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4) {
+          const float4 x = *reinterpret_cast<const float4*>(acc + c + i);
+          v[i] += x.x; v[i + 1] += x.y; v[i + 2] += x.z; v[i + 3] += x.w;
+        }
+      }
+      if (a.kv_final) {
+#pragma unroll
+        for (int i = 0; i < 16; i += 8) {
+          uint4 w;
+          w.x = pack_bf16x2(v[i], v[i + 1]); w.y = pack_bf16x2(v[i + 2], v[i + 3]);
+          w.z = pack_bf16x2(v[i + 4], v[i + 5]); w.w = pack_bf16x2(v[i + 6], v[i + 7]);
+          *reinterpret_cast<uint4*>(out + c + i) = w;
+        }
+      } else {
+#pragma unroll
+        for (int i = 0; i < 16; i += 4)
+          *reinterpret_cast<float4*>(acc + c + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+      }
+    }
+  } else {
+    setmaxnreg_dec<104>();
+    // ------------------------------------------------------------------ dQ read-out (query rows)
+    const int r = (warp - 8) * 32 + lane;
+    const int t128 = threadIdx.x - 256;
+    uint32_t tdQ = tmem + C::tdQ + (((warp & 3) * 32) << 16);
+    asm volatile("" : "+r"(tdQ));
+    for (int n = 0; n < n_iter; ++n) {
+      const int qt = qt_first + n / G, h = g * G + n % G;
+      mbar_wait(bar(B_DQF), n & 1);
+      TRACE(9, n);
+      tc_fence_after();
+      float v[D];
+#pragma unroll
+      for (int c = 0; c < D; c += 16) tmem_ld16(tdQ + c, reinterpret_cast<uint32_t(&)[16]>(v[c]));
+      tmem_wait_ld();
+      tc_fence_before();
+      mbar_arrive(bar(B_DQE));
+      if (FPDT_BWD_EXP == 2 || FPDT_BWD_EXP == 4) continue;
+      if constexpr (kRedDQ) {
+        // vector reductions straight from registers into the fp32 dq accumulator (no shared-memory staging)
+        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (((int64_t)qt * 128 + r) * a.hq + h) * D);
+#pragma unroll
+        for (int c = 0; c < D; c += 4)
+          atomicAdd(dst + c / 4, make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale, v[c + 3] * a.scale));
+        continue;
+      }
+      // the previous bulk reduce must have finished reading the staging tile
+      if (t128 == 0) bulk_wait_read0();
+      named_bar(1, 128);
+      // staging = D/32 column chunks [128 rows][32 fp32] (128B-swizzled) + a [128][16] chunk (64B-swizzled) when
+      // D % 32 == 16: the 16-byte piece j of row r lives at piece j ^ (r & 7) (resp. j ^ ((r >> 1) & 3)), so the
+      // 32 rows of a warp hit all 32 banks (an unswizzled 320-byte row pitch would be a 16-way bank conflict)
+      const float2 sc = make_float2(a.scale, a.scale);
+      uint8_t* stg = smem + C::oDQ;
+#pragma unroll
+      for (int c = 0; c < D; c += 4) {
+        const float2 x0 = __fmul2_rn(make_float2(v[c], v[c + 1]), sc);
+        const float2 x1 = __fmul2_rn(make_float2(v[c + 2], v[c + 3]), sc);
+        const int j = (c & 31) >> 2;
+        uint32_t off;
+        if (c < (D / 32) * 32)
+          off = (c >> 5) * 16384 + r * 128 + ((j ^ (r & 7)) << 4);
+        else
+          off = (D / 32) * 16384 + r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+        *reinterpret_cast<float4*>(stg + off) = make_float4(x0.x, x0.y, x1.x, x1.y);
+      }
+      fence_async_shared();
+      named_bar(1, 128);
+      if (FPDT_BWD_EXP != 1 && t128 == 0) {
+#pragma unroll
+        for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_3d(&tm.dq32, sDQ + cc * 16384, cc * 32, h, qt * 128);
+        if (D % 32) tma_reduce_add_3d(&tm.dq16, sDQ + (D / 32) * 16384, (D / 32) * 32, h, qt * 128);
+        bulk_commit();
+        TRACE(11, n);
+      }
+    }
+    if (!kRedDQ && t128 == 0) bulk_wait0();
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 13) tmem_dealloc<512>(tmem);
+#undef TRACE
+}
+
+template <int D>
+int launch_pipe(const BwdArgs& a, cudaStream_t s) {
+  using C = PipeCfg<D>;
+  // FPDT_BWD_DQ=red: dQ partials by vector atomics from registers; default: TMA bulk reduce-add from smem staging
+  static const bool red = [] {
+    const char* e = getenv("FPDT_BWD_DQ");
+    return e && strcmp(e, "red") == 0;
+  }();
+  TmapSet tm;
+  bool ok = make_tile_tmap<D>(&tm.q, a.q.base, a.q.rows, a.q.heads);
+  ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
+  ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
+  ok &= make_tile_tmap<D>(&tm.o, a.dout.base, a.dout.rows, a.dout.heads);
+  ok &= make_tmap_f32_rows_heads_dim(&tm.dq32, a.dq_acc, a.n_q_rows, a.hq, D, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_tmap_f32_rows_heads_dim(&tm.dq16, a.dq_acc, a.n_q_rows, a.hq, D, 16, 128, CU_TENSOR_MAP_SWIZZLE_64B);
+  if (!ok) return -1;
+  auto kern = red ? attn_bwd_pipe_kernel<D, true> : attn_bwd_pipe_kernel<D, false>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[red]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr_set[red] = true;
+  }
+  dim3 grid(a.n_kv_rows / 128, a.hq / a.G);
+  kern<<<grid, kThreads, C::kSmem, s>>>(tm, a);
+  return (int)cudaGetLastError();
+}
+
+}  // namespace
+
+// head_dim 64 / 80 (the pipelined kernel); head_dim 128 stays on attn_bwd_sm100.cu (its TMEM/smem budget has no
+// room for the extra Q stage and the separate dQ columns)
+int launch_attn_bwd_pipe_bf16(const BwdArgs& a, int head_dim, cudaStream_t s) {
+  switch (head_dim) {
+    case 64: return launch_pipe<64>(a, s);
+    case 80: return launch_pipe<80>(a, s);
+  }
+  return -2;
+}
+
+}  // namespace fpdt

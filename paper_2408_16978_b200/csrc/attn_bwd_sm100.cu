@@ -31,6 +31,9 @@
 #include "smem_layout.cuh"
 #include "tma_host.h"
 
+#include <cstdlib>
+#include <cstring>
+
 namespace fpdt {
 namespace {
 
@@ -473,7 +476,14 @@ int launch_bwd(const BwdArgs& a, cudaStream_t s) {
 
 }  // namespace
 
+// head_dim 64 / 80 run the software-pipelined kernel (attn_bwd_pipe_sm100.cu) unless FPDT_BWD_KERNEL=v2 selects
+// this one (A/B measurements); head_dim 128 always runs this one.
 int launch_attn_bwd_bf16(const BwdArgs& a, int head_dim, cudaStream_t s) {
+  static const bool use_v2 = [] {
+    const char* e = getenv("FPDT_BWD_KERNEL");
+    return e && strcmp(e, "v2") == 0;
+  }();
+  if (head_dim != 128 && !use_v2) return launch_attn_bwd_pipe_bf16(a, head_dim, s);
   switch (head_dim) {
     case 64: return launch_bwd<64>(a, s);
     case 80: return launch_bwd<80>(a, s);

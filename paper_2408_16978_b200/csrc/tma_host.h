@@ -47,10 +47,11 @@ inline bool make_tile_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint
   return make_tmap_rows_heads_dim(m, base, rows, heads, D, 64, 128, CU_TENSOR_MAP_SWIZZLE_128B);
 }
 
-// Tensor map over an fp32 tensor [rows][heads][head_dim] without swizzle (used for TMA reduce-add into
-// the dq accumulator).  Box = {box_cols, 1, box_rows}.
+// Tensor map over an fp32 tensor [rows][heads][head_dim] (used for TMA reduce-add into the dq accumulator);
+// swizzled boxes let threads that own one row each stage a tile without shared-memory bank conflicts.  Box = {box_cols, 1, box_rows}.
 inline bool make_tmap_f32_rows_heads_dim(CUtensorMap* m, const void* base, uint64_t rows, uint32_t heads,
-                                         uint32_t head_dim, uint32_t box_cols, uint32_t box_rows) {
+                                         uint32_t head_dim, uint32_t box_cols, uint32_t box_rows,
+                                         CUtensorMapSwizzle swizzle = CU_TENSOR_MAP_SWIZZLE_NONE) {
   EncodeTiledFn fn = get_encode_fn();
   if (!fn) return false;
   cuuint64_t dims[3] = {head_dim, heads, rows};
@@ -58,7 +59,7 @@ inline bool make_tmap_f32_rows_heads_dim(CUtensorMap* m, const void* base, uint6
   cuuint32_t box[3] = {box_cols, 1, box_rows};
   cuuint32_t estr[3] = {1, 1, 1};
   CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }

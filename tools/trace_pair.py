@@ -54,8 +54,8 @@ launch(ctypes.c_void_p(trace.data_ptr()))
 torch.cuda.synchronize()
 t = trace.cpu().numpy()
 names = {"bwd": ["sm:got_S", "sm:arr_P", "sm:got_dP", "sm:arr_dS", "mma:got_P", "mma:got_dS", "mma:iss_S+1",
-                 "mma:got_dqempty", "mma:iss_dP+1", "dq:got_full", "dq:arr_empty", "dq:reduce", "prod:got_qempty",
-                 "sm:S_loaded", "sm:exp_done", "sm:P_stored"],
+                 "mma:got_dqempty", "mma:iss_dP+1", "dq:got_full", "sm:got_dsfree", "dq:reduce", "prod:got_qempty",
+                 "sm:S_loaded", "sm:exp_done", "sm:dP_loaded"],
          "fwd": ["sm0:got_S", "sm0:arr_P", "sm1:got_S", "sm1:arr_P", "mma:got_P0", "mma:got_P1", "mma:got_K+1",
                  "prod:got_kvempty", "sm0:S_loaded", "sm0:max_done", "sm0:exp_done", "sm0:st_done",
                  "sm1:S_loaded", "sm1:max_done", "sm1:exp_done", "sm1:st_done"]}[which]
