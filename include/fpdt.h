@@ -160,7 +160,7 @@ int fpdt_selftest_perf(int what, int n, int iters, float* out, void* stream);
  * [0, n_rows) of q/k/v/dout against each other (the diagonal pair when causal = 1).
  *   which 0 (forward):  out0 = o bf16 [n_rows][n_q_heads][head_dim], out1 = log2-domain lse fp32 [n_q_heads][n_rows]
  *   which 1 (backward): lse2 / Dstat fp32 [n_q_heads][n_rows] (log2-domain lse, rowsum(dO o O)),
- *                       out0 = dq accumulator fp32 [n_rows][n_q_heads][head_dim] (zeroed by the caller; scaled
+ *                       out0 = dq accumulator fp32 [n_q_heads][n_rows][head_dim] (zeroed by the caller; scaled
  *                       dQ is added), out1 / out2 = dK / dV bf16 [n_rows][n_kv_heads][head_dim]
  * trace (nullable): device int64 [16][4096] receiving SM-clock timestamps of warp-role protocol events of
  * CTA (trace_cta, 0).  Returns FPDT_OK or a status. */

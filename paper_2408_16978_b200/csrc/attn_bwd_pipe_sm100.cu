@@ -41,7 +41,7 @@ using namespace ptx;
 constexpr int kThreads = 512;
 #ifndef FPDT_BWD_EXP
 #define FPDT_BWD_EXP 0  // timing experiments only (wrong results): 1 no dQ reduce, 2 no dQ staging/reduce,
-                       // 3 no stats loads, 4 = 2 + 3
+                       // 3 no stats loads, 4 = 2 + 3, 5 no wait for the previous dQ reduce's smem read
 #endif
 #ifndef FPDT_BWD_POLY_EVERY
 #define FPDT_BWD_POLY_EVERY 4  // one exponential pair in FPDT_BWD_POLY_EVERY goes to the FMA-pipe polynomial
@@ -452,14 +452,14 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       if (FPDT_BWD_EXP == 2 || FPDT_BWD_EXP == 4) continue;
       if constexpr (kRedDQ) {
         // vector reductions straight from registers into the fp32 dq accumulator (no shared-memory staging)
-        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (((int64_t)qt * 128 + r) * a.hq + h) * D);
+        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (int64_t)h * a.dq_head_stride + ((int64_t)qt * 128 + r) * D);
 #pragma unroll
         for (int c = 0; c < D; c += 4)
           atomicAdd(dst + c / 4, make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale, v[c + 3] * a.scale));
         continue;
       }
       // the previous bulk reduce must have finished reading the staging tile
-      if (t128 == 0) bulk_wait_read0();
+      if (FPDT_BWD_EXP != 5 && t128 == 0) bulk_wait_read0();
       named_bar(1, 128);
       // staging = D/32 column chunks [128 rows][32 fp32] (128B-swizzled) + a [128][16] chunk (64B-swizzled) when
       // D % 32 == 16: the 16-byte piece j of row r lives at piece j ^ (r & 7) (resp. j ^ ((r >> 1) & 3)), so the
@@ -482,8 +482,8 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       named_bar(1, 128);
       if (FPDT_BWD_EXP != 1 && t128 == 0) {
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_3d(&tm.dq32, sDQ + cc * 16384, cc * 32, h, qt * 128);
-        if (D % 32) tma_reduce_add_3d(&tm.dq16, sDQ + (D / 32) * 16384, (D / 32) * 32, h, qt * 128);
+        for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_3d(&tm.dq32, sDQ + cc * 16384, cc * 32, qt * 128, h);
+        if (D % 32) tma_reduce_add_3d(&tm.dq16, sDQ + (D / 32) * 16384, (D / 32) * 32, qt * 128, h);
         bulk_commit();
         TRACE(11, n);
       }
@@ -509,8 +509,10 @@ int launch_pipe(const BwdArgs& a, cudaStream_t s) {
   ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
   ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
   ok &= make_tile_tmap<D>(&tm.o, a.dout.base, a.dout.rows, a.dout.heads);
-  ok &= make_tmap_f32_rows_heads_dim(&tm.dq32, a.dq_acc, a.n_q_rows, a.hq, D, 32, 128, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_tmap_f32_rows_heads_dim(&tm.dq16, a.dq_acc, a.n_q_rows, a.hq, D, 16, 128, CU_TENSOR_MAP_SWIZZLE_64B);
+  ok &= make_tmap_f32_head_major(&tm.dq32, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 32, 128,
+                                 CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_tmap_f32_head_major(&tm.dq16, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 16, 128,
+                                 CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return -1;
   auto kern = red ? attn_bwd_pipe_kernel<D, true> : attn_bwd_pipe_kernel<D, false>;
   static bool attr_set[2] = {false, false};

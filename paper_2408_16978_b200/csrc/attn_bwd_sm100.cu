@@ -420,13 +420,13 @@ attn_bwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdA
         fence_async_shared();
         named_bar(1, 128);
         if (t128 == 0) {
-          tma_reduce_add_3d(&tm.dq, sDQ, 0, h, qt * 128);
+          tma_reduce_add_3d(&tm.dq, sDQ, 0, qt * 128, h);
           bulk_commit();
           TRACE(11, n);
         }
       } else {
         const int64_t qrow = (int64_t)qt * 128 + r;
-        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (qrow * a.hq + h) * D);
+        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (int64_t)h * a.dq_head_stride + qrow * D);
 #pragma unroll
         for (int hf = 0; hf < D; hf += 64) {
           float v[64];
@@ -462,7 +462,8 @@ int launch_bwd(const BwdArgs& a, cudaStream_t s) {
   ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
   ok &= make_tile_tmap<D>(&tm.o, a.dout.base, a.dout.rows, a.dout.heads);
   if constexpr (C::kTmaDQ)
-    ok &= make_tmap_f32_rows_heads_dim(&tm.dq, a.dq_acc, a.n_q_rows, a.hq, D, D, 128);
+    ok &= make_tmap_f32_head_major(&tm.dq, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, D, 128,
+                                   CU_TENSOR_MAP_SWIZZLE_NONE);
   if (!ok) return -1;
   static bool attr_set = false;
   if (!attr_set) {

@@ -226,7 +226,7 @@ bwd_dq_f32_kernel(BwdArgs a) {
       if (d < D) dq[e] = fmaf(dS, kr[d], dq[e]);
     }
   }
-  float* dst = a.dq_acc + (row * a.hq + h) * D;
+  float* dst = a.dq_acc + (int64_t)h * a.dq_head_stride + row * D;
 #pragma unroll
   for (int e = 0; e < E; ++e) {
     const int d = lane + 32 * e;

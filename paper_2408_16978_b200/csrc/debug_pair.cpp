@@ -52,6 +52,7 @@ extern "C" int fpdt_debug_pair(int which, int head_dim, int causal, const void* 
   a.Dstat = Dstat;
   a.stat_ld = n_rows;
   a.dq_acc = static_cast<float*>(out0);
+  a.dq_head_stride = n_rows * head_dim;
   a.kv_acc_init = 1;
   a.kv_final = 1;
   a.dk_out = out1;

@@ -209,7 +209,7 @@ Config make_config(int64_t s_local, int Hq, int Hkv, int d, int causal, int64_t 
 }
 
 // Host chunk store layout (offload=1): per chunk m, q_m [C][hq][d], kv_m [C][2hkv][d], dO_m [C][hq][d] (eb bytes),
-// dq_acc_m [C][hq][d] fp32.
+// dq_acc_m [hq][C][d] fp32 (head-major, the layout of the device dq accumulators).
 struct HostLayout {
   size_t q_bytes, kv_bytes, do_bytes, dq_bytes, total;
   size_t q(int64_t m) const { return (size_t)m * q_bytes; }
@@ -607,12 +607,15 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   uint8_t* brecv = p > 1 ? (uint8_t*)dev(ctx, B_BWD_RECV, (size_t)C * hcomb * d * eb) : nullptr;
 
   // B6: dq_j final (fp32, already scaled) -> the caller's rows (p == 1) or the head-side send buffer (p > 1)
-  auto emit_dq = [&](int64_t j, const float* dq_final) {
+  // dq_final: head-major fp32 rows of chunk j, heads head_stride elements apart
+  auto emit_dq = [&](int64_t j, const float* dq_final, int64_t head_stride) {
     if (p == 1)
-      FPDT_CHECK_LAUNCH(launch_convert_out(dq_final, C, hq, d, 1.f, (uint8_t*)dq + (size_t)j * C * c.Hq * d * eb,
-                                           c.dtype, (int64_t)c.Hq * d, 0, cs));
+      FPDT_CHECK_LAUNCH(launch_convert_out(dq_final, C, hq, d, head_stride, 1.f,
+                                           (uint8_t*)dq + (size_t)j * C * c.Hq * d * eb, c.dtype, (int64_t)c.Hq * d,
+                                           0, cs));
     else
-      FPDT_CHECK_LAUNCH(launch_convert_out(dq_final, C, hq, d, 1.f, bsend, c.dtype, (int64_t)hcomb * d, 0, cs));
+      FPDT_CHECK_LAUNCH(launch_convert_out(dq_final, C, hq, d, head_stride, 1.f, bsend, c.dtype, (int64_t)hcomb * d,
+                                           0, cs));
     ctx->stats.kernel_launches++;
   };
   // B7: after outer iteration j, dq_j, dk_j, dv_j (in bsend) go back to their owner ranks (p > 1)
@@ -679,14 +682,15 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       a.lse2 = lse_save + j * C;
       a.Dstat = Dh + j * C;
       a.stat_ld = c.S;
-      a.dq_acc = dq_dev + (size_t)j * C * hq * d;
+      a.dq_acc = dq_dev + (size_t)j * C * d;  // head-major [hq][S][d]
+      a.dq_head_stride = c.S * d;
       a.dk_acc = dk_acc;
       a.dv_acc = dv_acc;
       a.kv_acc_init = 1;
       a.kv_final = 1;
       set_kv_out(a, j);
       launch_bwd(ctx, c, a, cs);
-      emit_dq(j, dq_dev + (size_t)j * C * hq * d);
+      emit_dq(j, dq_dev + (size_t)j * C * d, c.S * d);
       send_back(j);
     }
   } else {
@@ -739,7 +743,8 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
         a.lse2 = lse_save + i * C;
         a.Dstat = Dh + i * C;
         a.stat_ld = c.S;
-        a.dq_acc = dqs[sl];
+        a.dq_acc = dqs[sl];  // head-major [hq][C][d]
+        a.dq_head_stride = C * d;
         a.dk_acc = dk_acc;
         a.dv_acc = dv_acc;
         a.kv_acc_init = (i == j);
@@ -748,7 +753,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
         launch_bwd(ctx, c, a, cs);
         if (i == j) {
           // B6: dq_j is final after its last contribution (inner iteration i == j)
-          emit_dq(j, dqs[sl]);
+          emit_dq(j, dqs[sl], C * d);
           rec(ctx->ev_q_free[sl], cs);
         } else {
           // B6: write the dq partial back to the host store

@@ -60,7 +60,8 @@ struct BwdArgs {
   const float* lse2 = nullptr;      // log2-domain lse of the query rows, lse2[h*stat_ld + (row - q_row0)]
   const float* Dstat = nullptr;     // D = rowsum(dO o O), same indexing
   int64_t stat_ld = 0;
-  float* dq_acc = nullptr;          // fp32 [n_q_rows][hq][D], atomically accumulated (scaled)
+  float* dq_acc = nullptr;          // fp32 head-major [hq][dq_head_stride/D][D], rows [0, n_q_rows) of each head
+  int64_t dq_head_stride = 0;       // elements between heads of dq_acc (>= n_q_rows * D); accumulated (scaled)
   // dK/dV: fp32 accumulators [n_kv_rows][hkv][D] (kv_acc_init: overwrite instead of add)
   float* dk_acc = nullptr;
   float* dv_acc = nullptr;
@@ -87,9 +88,9 @@ int launch_attn_bwd_f32(const BwdArgs& a, int head_dim, cudaStream_t s);
 int launch_bwd_preprocess_D(const void* o, const void* dout, int dtype, int64_t rows, int heads, int head_dim,
                             int64_t row_ld, const void* resid, int64_t resid_ld, float* D, int64_t ld,
                             cudaStream_t s);
-// fp32 [rows][heads][d] * scale -> bf16/fp32 dst[row*dst_ld + (dst_head0+h)*d + e]
-int launch_convert_out(const float* src, int64_t rows, int heads, int head_dim, float scale, void* dst, int dtype,
-                       int64_t dst_ld, int dst_head0, cudaStream_t s);
+// fp32 head-major src[h*src_head_stride + row*d + e] * scale -> bf16/fp32 dst[row*dst_ld + (dst_head0+h)*d + e]
+int launch_convert_out(const float* src, int64_t rows, int heads, int head_dim, int64_t src_head_stride, float scale,
+                       void* dst, int dtype, int64_t dst_ld, int dst_head0, cudaStream_t s);
 // pack rows [c][H][d] of a sequence-layout tensor into send[p][c][H/p][d] (elem_bytes 2 or 4)
 int launch_pack_seq2head(const void* src, int64_t c, int H, int head_dim, int p, int elem_bytes, void* dst,
                          int64_t dst_peer_stride_elems, int64_t dst_row_ld, int dst_head0, cudaStream_t s);

@@ -56,14 +56,16 @@ __global__ void preprocess_D_kernel(const T* __restrict__ o, const T* __restrict
 }
 
 template <typename T>
-__global__ void convert_out_kernel(const float* __restrict__ src, int64_t rows, int heads, int head_dim, float scale,
-                                   T* __restrict__ dst, int64_t dst_ld, int dst_head0) {
+__global__ void convert_out_kernel(const float* __restrict__ src, int64_t rows, int heads, int head_dim,
+                                   int64_t src_head_stride, float scale, T* __restrict__ dst, int64_t dst_ld,
+                                   int dst_head0) {
   const int64_t per_row = (int64_t)heads * head_dim / 4;
   const int64_t n = rows * per_row;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
     const int64_t t = idx / per_row;
-    const int64_t w = (idx - t * per_row) * 4;  // element offset within the row
-    const float4 v = *reinterpret_cast<const float4*>(src + t * heads * head_dim + w);
+    const int64_t w = (idx - t * per_row) * 4;  // element offset within the destination row
+    const int64_t h = w / head_dim, e = w - h * head_dim;
+    const float4 v = *reinterpret_cast<const float4*>(src + h * src_head_stride + t * head_dim + e);
     T* out = dst + t * dst_ld + (int64_t)dst_head0 * head_dim + w;
     if constexpr (sizeof(T) == 2) {
       __nv_bfloat162 a = __floats2bfloat162_rn(v.x * scale, v.y * scale);
@@ -127,15 +129,15 @@ int launch_bwd_preprocess_D(const void* o, const void* dout, int dtype, int64_t 
   return (int)cudaGetLastError();
 }
 
-int launch_convert_out(const float* src, int64_t rows, int heads, int head_dim, float scale, void* dst, int dtype,
-                       int64_t dst_ld, int dst_head0, cudaStream_t s) {
+int launch_convert_out(const float* src, int64_t rows, int heads, int head_dim, int64_t src_head_stride, float scale,
+                       void* dst, int dtype, int64_t dst_ld, int dst_head0, cudaStream_t s) {
   const int64_t n = rows * heads * head_dim / 4;
   if (dtype == 0)
-    convert_out_kernel<__nv_bfloat16><<<grid_for(n), kBlock, 0, s>>>(src, rows, heads, head_dim, scale,
-                                                                     (__nv_bfloat16*)dst, dst_ld, dst_head0);
+    convert_out_kernel<__nv_bfloat16><<<grid_for(n), kBlock, 0, s>>>(src, rows, heads, head_dim, src_head_stride,
+                                                                     scale, (__nv_bfloat16*)dst, dst_ld, dst_head0);
   else
-    convert_out_kernel<float><<<grid_for(n), kBlock, 0, s>>>(src, rows, heads, head_dim, scale, (float*)dst, dst_ld,
-                                                             dst_head0);
+    convert_out_kernel<float><<<grid_for(n), kBlock, 0, s>>>(src, rows, heads, head_dim, src_head_stride, scale,
+                                                             (float*)dst, dst_ld, dst_head0);
   return (int)cudaGetLastError();
 }
 

@@ -64,4 +64,21 @@ inline bool make_tmap_f32_rows_heads_dim(CUtensorMap* m, const void* base, uint6
   return r == CUDA_SUCCESS;
 }
 
+// Tensor map over a head-major fp32 tensor [heads][head_stride/head_dim rows][head_dim] (the dq accumulator):
+// coordinates (col, row, head); box = {box_cols, box_rows, 1}.
+inline bool make_tmap_f32_head_major(CUtensorMap* m, const void* base, uint64_t rows, uint32_t heads,
+                                     uint32_t head_dim, uint64_t head_stride, uint32_t box_cols, uint32_t box_rows,
+                                     CUtensorMapSwizzle swizzle) {
+  EncodeTiledFn fn = get_encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[3] = {head_dim, rows, heads};
+  cuuint64_t strides[2] = {(cuuint64_t)head_dim * 4, (cuuint64_t)head_stride * 4};
+  cuuint32_t box[3] = {box_cols, box_rows, 1};
+  cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = fn(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<void*>(base), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, swizzle, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
 }  // namespace fpdt
