@@ -39,6 +39,10 @@ namespace {
 using namespace ptx;
 
 constexpr int kThreads = 512;
+// setmaxnreg budget: the softmax warpgroups grow only by what WG2 / WG3 give back (pool = launch allocation)
+constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 128
+constexpr int kRegsSoftmax = 168, kRegsDQ = 104, kRegsCtl = 72;
+static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
 #ifndef FPDT_BWD_EXP
 #define FPDT_BWD_EXP 0  // timing experiments only (wrong results): 1 no dQ reduce, 2 no dQ staging/reduce,
                        // 3 no stats loads, 4 = 2 + 3, 5 no wait for the previous dQ reduce's smem read
@@ -177,7 +181,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
   const uint32_t tmem = *tmem_slot;
 
   if (warp >= 12) {
-    setmaxnreg_dec<72>();
+    setmaxnreg_dec<kRegsCtl>();
     if (warp == 12) {
       // ---------------------------------------------------------------- TMA producer
       if (elect_one() && n_iter > 0) {
@@ -277,7 +281,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       }
     }
   } else if (warp < 8) {
-    setmaxnreg_inc<168>();
+    setmaxnreg_inc<kRegsSoftmax>();
     // ------------------------------------------------------------------ softmax gradient (key rows)
     const int half = warp >> 2;  // query columns [64*half, 64*half+64)
     const int r = (warp & 3) * 32 + lane;
@@ -432,7 +436,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       }
     }
   } else {
-    setmaxnreg_dec<104>();
+    setmaxnreg_dec<kRegsDQ>();
     // ------------------------------------------------------------------ dQ read-out (query rows)
     const int r = (warp - 8) * 32 + lane;
     const int t128 = threadIdx.x - 256;

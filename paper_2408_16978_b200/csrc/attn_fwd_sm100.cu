@@ -5,15 +5,23 @@
 // merges it with the running partial result of earlier pairs by log-sum-exp (the "online attention
 // policy").  Causal masking on global token positions (key pos <= query pos; reading R3).
 //
-// CTA = 2 query tiles of 128 rows of ONE query head (sharing every K/V tile), 10 warps:
-//   warps 0-3  softmax + correction + epilogue of query tile 0 (thread = query row = TMEM lane)
-//   warps 4-7  same for query tile 1
-//   warp  8    TMA producer (Q once, then a K/V ring of kStages stages)
-//   warp  9    TMEM allocator + single-thread tcgen05.mma issuer
-// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,256+D) O1 [384,384+D); P_t (bf16) aliases S_t[0,64).
+// CTA = 2 query tiles of 128 rows of ONE query head (sharing every K/V tile), 12 warps (3 warpgroups):
+//   WG0 (0-3)   softmax + correction + epilogue of query tile 0 (thread = query row = TMEM lane)
+//   WG1 (4-7)   same for query tile 1
+//   WG2 (8)     TMA producer (Q once, then a K/V ring of kStages stages); (9) TMEM allocator +
+//               single-thread tcgen05.mma issuer; (10, 11) idle
+// (Measured alternative, not kept: two threads per row, 16 softmax warps — the exponential phase of a tile took
+// as long, the pipes being shared per SMSP, and the registers per thread dropped to 104.)
+// TMEM (512 columns): S0 [0,128) S1 [128,256) O0 [256,256+NO) O1 [384,384+NO); P_t (bf16) aliases S_t[0,64).
 // MMA order per key tile j:  PV0_j, S0_{j+1}, PV1_j, S1_{j+1} — tcgen05 MMAs of one thread execute in
 // issue order, so S_t{j+1} overwriting P_t_j after PV_t_j is safe, and the commit that signals S_t{j+1}
 // also guarantees PV_t_j has finished (so the softmax warps may rescale O_t in TMEM then).
+// Softmax (the bottleneck at d <= 80: per (row, key) the exponential costs more than the 4d MMA FLOPs):
+//   * row max with three-input FMNMX3, scale/subtract with packed FFMA2;
+//   * a quarter of the exponentials (every 4th pair) as a degree-3 polynomial on the FMA pipe, the rest on MUFU;
+//   * d = 80: the row sum of P comes from the tensor core — each V stage carries a 16-column atom of ones,
+//     so PV has N = 96 and O column 80 accumulates sum(P) with the same rescaling as O (and the same bf16 P
+//     the numerator uses); d = 64 / 128 sum with packed FADD2.
 // Lazy rescale: the running max used for exponentiation is only raised when a row max exceeds it by
 // more than 8 (log2 units), bounding P by 2^8 (exact result either way; rescale skipped otherwise).
 #include "attn_tile.cuh"
@@ -25,19 +33,26 @@ namespace {
 
 using namespace ptx;
 
-constexpr int kThreads = 320;
+constexpr int kThreads = 384;
+// setmaxnreg budget: the CTA's register pool is what the launch allocated (kLaunchRegs per thread); the two
+// softmax warpgroups may only grow by what WG2 gives back (an over-subscribed setmaxnreg.inc never returns)
+constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 168
+constexpr int kRegsSoftmax = 200, kRegsOther = 88;
+static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (kLaunchRegs - kRegsOther), "register pool");
 constexpr float kRescaleThreshold = 8.0f;
-#ifndef FPDT_FWD_POLY
-#define FPDT_FWD_POLY 0
+#ifndef FPDT_FWD_POLY_EVERY
+#define FPDT_FWD_POLY_EVERY 4  // one exponential pair in 4 on the FMA pipe (measured: 0, 1, 2, 3, 4 -> 800, 669, 811, 865, 873 TF)
 #endif
-constexpr bool kFwdPoly = FPDT_FWD_POLY != 0;  // FMA-pipe exp2 for every 4th element (issue-bound here: off)
 
 template <int D>
 struct FwdCfg {
   using T = Tile<D>;
+  static constexpr bool kSumMMA = (D == 80);     // row sums from a ones column of V (SW32 atoms only)
+  static constexpr int NO = kSumMMA ? D + 16 : D;  // PV N / O columns
   static constexpr int kStages = (D == 128) ? 2 : 3;
   static constexpr int kQBytes = 2 * T::kBytes;
-  static constexpr int kStageBytes = 2 * T::kBytes;  // K + V
+  static constexpr int kOnes = kSumMMA ? 128 * 16 * 2 : 0;      // the ones atom right after each V tile
+  static constexpr int kStageBytes = 2 * T::kBytes + kOnes;       // K + V (+ ones)
   static constexpr int kSmem = kQBytes + kStages * kStageBytes + 1024;
 };
 
@@ -55,45 +70,60 @@ __device__ __forceinline__ float lg2(float x) {
   asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
 }
-
-// 2^x on the FMA pipe (FA4-style MUFU offload): round-to-nearest split x = k + f, f in [-1/2, 1/2],
-// degree-3 minimax polynomial for 2^f (max rel. error 7.5e-5 << bf16's 2^-9), exponent added as an integer.
-// Valid for -127 <= x <= 127; callers use it only where x is finite.
-__device__ __forceinline__ float exp2_poly(float x) {
-  x = fmaxf(x, -127.f);
-  const float j = __fadd_rn(x, 12582912.f);  // 1.5 * 2^23: integer part lands in the low mantissa bits
-  const float f = __fsub_rn(x, __fsub_rn(j, 12582912.f));
-  float p = fmaf(f, 0.055169348f, 0.24260798f);
-  p = fmaf(p, f, 0.69326115f);
-  p = fmaf(p, f, 0.9999283f);
-  return __int_as_float(__float_as_int(p) + (__float_as_int(j) << 23));
+__device__ __forceinline__ void named_bar_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+__device__ __forceinline__ float max3(float a, float b, float c) {
+  float y;
+  asm("max.f32 %0, %1, %2, %3;" : "=f"(y) : "f"(a), "f"(b), "f"(c));
+  return y;
 }
 
-// exp2(x*sl2 - mb) for one 128-column row, packed to bf16 and stored to TMEM columns [tS, tS+64); returns the
-// row sum of the fp32 values.  kPoly: every 4th exponential on the FMA pipe.
-template <bool kPoly>
+// 2^x for a pair on the FMA pipe (FA4-style MUFU offload): x = j + f, j = rint(x), f in [-1/2, 1/2];
+// degree-3 minimax for 2^f (max rel. error 7.5e-5 << bf16's 2^-9); the exponent is added as an integer.
+// x is clamped to >= -127 (callers use it only where x is finite).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -127.f);
+  x.y = fmaxf(x.y, -127.f);
+  const float2 kRnd = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 j = __fadd2_rn(x, kRnd);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(kRnd, make_float2(-j.x, -j.y)));
+  float2 p = __ffma2_rn(f, make_float2(0.055169348f, 0.055169348f), make_float2(0.24260798f, 0.24260798f));
+  p = __ffma2_rn(p, f, make_float2(0.69326115f, 0.69326115f));
+  p = __ffma2_rn(p, f, make_float2(0.9999283f, 0.9999283f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
+
+// P = exp2(x*sl2 - mb) for the 128 columns of a row, packed to bf16 and stored to TMEM columns [tS, tS+64); returns
+// the sum of the fp32 values when kSum (else 0).  kPoly: every FPDT_FWD_POLY_EVERY-th pair on the FMA pipe.
+template <bool kPoly, bool kSum>
 __device__ __forceinline__ float exp_pack_store(const float* x, float sl2, float mb, uint32_t tS) {
-  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+  float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
+  const float2 s2 = make_float2(sl2, sl2), nm = make_float2(-mb, -mb);
 #pragma unroll
   for (int c = 0; c < 128; c += 32) {
     uint32_t pk[16];
 #pragma unroll
-    for (int i = 0; i < 32; i += 4) {
-      const float p0 = ex2(fmaf(x[c + i], sl2, -mb));
-      const float p1 = ex2(fmaf(x[c + i + 1], sl2, -mb));
-      const float p2 = ex2(fmaf(x[c + i + 2], sl2, -mb));
-      const float e3 = fmaf(x[c + i + 3], sl2, -mb);
-      const float p3 = kPoly ? exp2_poly(e3) : ex2(e3);
-      s0 += p0;
-      s1 += p1;
-      s2 += p2;
-      s3 += p3;
-      pk[i / 2] = pack_bf16x2(p0, p1);
-      pk[i / 2 + 1] = pack_bf16x2(p2, p3);
+    for (int i = 0; i < 32; i += 2) {
+      const float2 e = __ffma2_rn(make_float2(x[c + i], x[c + i + 1]), s2, nm);
+      float2 pr;
+      if (kPoly && FPDT_FWD_POLY_EVERY > 0 && (i / 2) % FPDT_FWD_POLY_EVERY == FPDT_FWD_POLY_EVERY - 1) {
+        pr = ex2_poly2(e);
+      } else {
+        pr = make_float2(ex2(e.x), ex2(e.y));
+      }
+      if (kSum) {
+        if ((i / 2) & 1)
+          acc1 = __fadd2_rn(acc1, pr);
+        else
+          acc0 = __fadd2_rn(acc0, pr);
+      }
+      pk[i / 2] = pack_bf16x2(pr.x, pr.y);
     }
     tmem_st16(tS + c / 2, pk);
   }
-  return (s0 + s1) + (s2 + s3);
+  return kSum ? (acc0.x + acc0.y) + (acc1.x + acc1.y) : 0.f;
 }
 
 template <int D>
@@ -128,6 +158,19 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
   } while (0)
 
   if (warp == 9) tmem_alloc<512>(smem_u32(&tmem_slot));
+  if constexpr (C::kSumMMA) {
+    // the ones atom after every V tile (constant; MN-major B columns D..D+15 of PV): all 16 columns = 1.0, so
+    // the swizzle does not matter and O column D accumulates sum(P)
+    if (warp >= 10) {
+      const int t = threadIdx.x - 320;
+      for (int s2 = 0; s2 < ST; ++s2) {
+        uint4* dst = reinterpret_cast<uint4*>(smem + C::kQBytes + s2 * C::kStageBytes + 2 * T::kBytes);
+        for (int i = t; i < C::kOnes / 16; i += 64)
+          dst[i] = make_uint4(0x3f803f80u, 0x3f803f80u, 0x3f803f80u, 0x3f803f80u);
+      }
+      fence_async_shared();
+    }
+  }
   if (warp == 8 && lane == 0) {
     mbar_init(smem_u32(&bar_q), 1);
     for (int s = 0; s < ST; ++s) {
@@ -147,7 +190,9 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
   tc_fence_after();
   const uint32_t tmem = tmem_slot;
 
-  if (warp == 8) {
+  if (warp >= 8) {
+   setmaxnreg_dec<kRegsOther>();
+   if (warp == 8) {
     // ------------------------------------------------------------------ TMA producer
     if (elect_one()) {
       tma_prefetch_desc(&tm.q);
@@ -171,11 +216,11 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         T::load(sv, &tm.v, smem_u32(&bar_v[s]), a.v.head0 + g, krow, pol_kv);
       }
     }
-  } else if (warp == 9) {
+   } else if (warp == 9) {
     // ------------------------------------------------------------------ MMA issuer
     if (elect_one()) {
       const uint32_t idS = idesc_bf16(128, 128, 0, 0);
-      const uint32_t idPV = idesc_bf16(128, D, 0, 1);
+      const uint32_t idPV = idesc_bf16(128, C::NO, 0, 1);
       const uint32_t tS[2] = {tmem, tmem + 128};
       const uint32_t tO[2] = {tmem + 256, tmem + 384};
       auto issue_S = [&](int t, int s) {
@@ -232,13 +277,16 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         }
       }
     }
+   }
   } else {
+    setmaxnreg_inc<kRegsSoftmax>();
     // ------------------------------------------------------------------ softmax / correction / epilogue
     const int t = warp >> 2;
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_off = ((warp & 3) * 32) << 16;
-    const uint32_t tS = tmem + t * 128 + lane_off;
-    const uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    uint32_t tS = tmem + t * 128 + lane_off;
+    uint32_t tO = tmem + 256 + t * 128 + lane_off;
+    asm volatile("" : "+r"(tS), "+r"(tO));
     const int64_t qpos = q_pos_first + t * 128 + r;
     const float sl2 = a.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
@@ -263,25 +311,26 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         for (int i = 0; i < 128; ++i)
           if (i > lim) x[i] = -INFINITY;
       }
+      // row max: 8 independent three-input max chains
       float m8[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) m8[k] = x[k];
 #pragma unroll
-      for (int i = 8; i < 128; i += 8) {
+      for (int i = 8; i < 128; i += 16) {
 #pragma unroll
-        for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], x[i + k]);
+        for (int k = 0; k < 8; ++k) m8[k] = max3(m8[k], x[i + k], x[i + 8 + k]);
       }
-      float mx = fmaxf(fmaxf(fmaxf(m8[0], m8[1]), fmaxf(m8[2], m8[3])), fmaxf(fmaxf(m8[4], m8[5]), fmaxf(m8[6], m8[7])));
+      float mx = max3(max3(m8[0], m8[1], m8[2]), max3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
       mx *= sl2;
       if ((warp & 3) == 0 && lane == 0) TRACE(9 + 4 * t, j);
       const bool need = mx > m_run + kRescaleThreshold;
       if (__any_sync(0xffffffffu, need)) {
         const float m_new = need ? mx : m_run;
         const float alpha = need ? ex2(m_run - m_new) : 1.f;
-        l_run *= alpha;
+        if constexpr (!C::kSumMMA) l_run *= alpha;
         if (j > 0) {
 #pragma unroll
-          for (int c = 0; c < D; c += 16) {
+          for (int c = 0; c < C::NO; c += 16) {
             uint32_t o[16];
             tmem_ld16(tO + c, o);
             tmem_wait_ld();
@@ -293,10 +342,12 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         m_run = m_new;
       }
       const float mb = (m_run == -INFINITY) ? 0.f : m_run;
-      // P = exp2(S*scale*log2e - m): a quarter of the exponentials on the FMA pipe (exp2_poly), the rest on
-      // MUFU, except on masked tiles (MUFU maps -inf to exactly 0)
-      const float sum = any_masked ? exp_pack_store<false>(x, sl2, mb, tS) : exp_pack_store<kFwdPoly>(x, sl2, mb, tS);
-      l_run += sum;
+      // P = exp2(S*scale*log2e - m): every FPDT_FWD_POLY_EVERY-th pair on the FMA pipe, the rest on MUFU, except on
+      // masked tiles (MUFU maps -inf to exactly 0)
+      constexpr bool kSumHere = !C::kSumMMA;
+      const float sum = any_masked ? exp_pack_store<false, kSumHere>(x, sl2, mb, tS)
+                                   : exp_pack_store<true, kSumHere>(x, sl2, mb, tS);
+      if constexpr (kSumHere) l_run += sum;
       if ((warp & 3) == 0 && lane == 0) TRACE(10 + 4 * t, j);
       tmem_wait_st();
       if ((warp & 3) == 0 && lane == 0) TRACE(11 + 4 * t, j);
@@ -307,10 +358,11 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
     // epilogue: normalise, merge with the running partial result, write
     mbar_wait(smem_u32(&bar_o[t]), 0);
     tc_fence_after();
-    float o[D];
+    float o[C::NO];
 #pragma unroll
-    for (int c = 0; c < D; c += 16) tmem_ld16(tO + c, reinterpret_cast<uint32_t(&)[16]>(o[c]));
+    for (int c = 0; c < C::NO; c += 16) tmem_ld16(tO + c, reinterpret_cast<uint32_t(&)[16]>(o[c]));
     tmem_wait_ld();
+    if constexpr (C::kSumMMA) l_run = o[D];
     const float inv_l = 1.f / l_run;
     float lse_b = m_run + lg2(l_run);
     const int64_t row = (int64_t)pair * 256 + t * 128 + r;  // row within the launch's query range
@@ -346,7 +398,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         w.w = pack_bf16x2(o[c + 6], o[c + 7]);
         *reinterpret_cast<uint4*>(out + c) = w;
         if (a.o_resid) {
-          // residual O - bf16(O), so the backward can form D from the fp32 output (R9)
+          // residual O - bf16(O), so the backward can form D from the fp32 output (R22)
           const __nv_bfloat162* wb2 = reinterpret_cast<const __nv_bfloat162*>(&w);
           uint4 rw;
           uint32_t* rp = reinterpret_cast<uint32_t*>(&rw);

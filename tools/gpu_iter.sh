@@ -6,5 +6,5 @@ timeout 300 python -m pytest tests/test_gpu_parity.py -x -q ${PYTEST_K:+-k "$PYT
 timeout 120 python tools/trace_pair.py bwd 65536 32 80 100 > gpurun_out/trace_bwd.log 2>&1; echo "trace rc=$?"; cat gpurun_out/trace_bwd.log
 timeout 120 env FPDT_BWD_KERNEL=v2 python tools/trace_pair.py bwd 65536 32 80 100 2>&1 | head -1
 timeout 120 python tools/trace_pair.py bwd 65536 32 64 100 2>&1 | head -1
-${RUN_BENCH:+timeout 600 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench.log}
+if [ -n "$RUN_BENCH" ]; then timeout 900 python bench.py --no-cpu-baseline > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench.log; fi
 timeout 120 env FPDT_BWD_DQ=red python tools/trace_pair.py bwd 65536 32 80 100 > gpurun_out/trace_bwd_red.log 2>&1; echo "red:"; grep -v "^it " gpurun_out/trace_bwd_red.log
