@@ -250,6 +250,8 @@ def run_ours(args):
     fwd_flops_launch = f_fwd / world / max(n_fwd // args.steps, 1)
     ach_bwd = bwd_flops_launch / (bwd_launch_ms / 1e3) / 1e12
     ach_fwd = fwd_flops_launch / (fwd_launch_ms / 1e3) / 1e12
+    # DRAM bytes of one backward pair launch from the committed ncu --set full capture (profiles/ncu_traffic.json:
+    # the full (i > j) chunk pair at this launch shape; the diagonal pairs move about half)
     traffic = None
     prof = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if os.path.exists(prof):
@@ -306,7 +308,7 @@ def run_ours(args):
                    "chunks": S // C, "s_local": s_local, "offload": offload, "causal": 1,
                    "parallelism": f"ulysses-sp{world}", "l2": "inputs 2.7 GB/tensor >> 126 MB L2, no flush",
                    "flops_per_step": f_fwd + f_bwd, "flop_convention": "14*d per causal pair per q-head"},
-        "roofline": {"bound": "tensor", "kernel": "attn_bwd_kernel (tcgen05 pair backward)",
+        "roofline": {"bound": "tensor", "kernel": "attn_bwd_pipe_kernel<80> (tcgen05 pair backward)",
                      "achieved": ach_bwd, "peak": sustained, "unit": "TFLOP/s", "frac": ach_bwd / sustained,
                      "traffic": traffic, "peak_source": peak_src + ", sustained bf16 (kernel timed inside a long step)",
                      "launch_ms": bwd_launch_ms, "launches_per_step": n_bwd // args.steps,
