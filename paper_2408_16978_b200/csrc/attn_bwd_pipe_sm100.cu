@@ -45,7 +45,8 @@ constexpr int kRegsSoftmax = 168, kRegsDQ = 104, kRegsCtl = 72;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
 #ifndef FPDT_BWD_EXP
 #define FPDT_BWD_EXP 0  // timing experiments only (wrong results): 1 no dQ reduce, 2 no dQ staging/reduce,
-                       // 3 no stats loads, 4 = 2 + 3, 5 no wait for the previous dQ reduce's smem read
+                       // 3 no stats loads, 4 = 2 + 3, 5 no wait for the previous dQ reduce's smem read,
+                       // 6 dQ reduce every other tile only, 7 only the 16-column dQ box
 #endif
 #ifndef FPDT_BWD_POLY_EVERY
 #define FPDT_BWD_POLY_EVERY 4  // one exponential pair in FPDT_BWD_POLY_EVERY goes to the FMA-pipe polynomial
@@ -484,9 +485,10 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       }
       fence_async_shared();
       named_bar(1, 128);
-      if (FPDT_BWD_EXP != 1 && t128 == 0) {
+      if (FPDT_BWD_EXP != 1 && !(FPDT_BWD_EXP == 6 && (n & 1)) && t128 == 0) {
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_3d(&tm.dq32, sDQ + cc * 16384, cc * 32, qt * 128, h);
+        for (int cc = 0; cc < D / 32; ++cc)
+          if (FPDT_BWD_EXP != 7) tma_reduce_add_3d(&tm.dq32, sDQ + cc * 16384, cc * 32, qt * 128, h);
         if (D % 32) tma_reduce_add_3d(&tm.dq16, sDQ + (D / 32) * 16384, (D / 32) * 32, qt * 128, h);
         bulk_commit();
         TRACE(11, n);
