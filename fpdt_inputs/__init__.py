@@ -57,14 +57,17 @@ def bf16_round(x: np.ndarray) -> np.ndarray:
     return ((u + bias) & np.uint32(0xFFFF0000)).view(np.float32)
 
 
-def base_values(seed: int, tensor: int, tokens: np.ndarray, n_heads: int, head_dim: int) -> np.ndarray:
+def base_values(seed: int, tensor: int, tokens: np.ndarray, n_heads: int, head_dim: int,
+                heads: np.ndarray | None = None) -> np.ndarray:
     """Raw Irwin-Hall values (fp32, before bf16 rounding) for rows `tokens` (global token ids).
 
-    Returns shape [len(tokens), n_heads, head_dim].
+    Returns shape [len(tokens), n_heads, head_dim], or [len(tokens), len(heads), head_dim] for a subset of the
+    n_heads heads (the values are those of the full tensor: the counter uses n_heads).
     """
     with np.errstate(over="ignore"):
         tok = np.asarray(tokens, dtype=np.uint64).reshape(-1, 1, 1)
-        hd = np.arange(n_heads, dtype=np.uint64).reshape(1, -1, 1)
+        hsel = np.arange(n_heads) if heads is None else np.asarray(heads)
+        hd = hsel.astype(np.uint64).reshape(1, -1, 1)
         dd = np.arange(head_dim, dtype=np.uint64).reshape(1, 1, -1)
         idx = (tok * np.uint64(n_heads) + hd) * np.uint64(head_dim) + dd
         a = _mix32(np.uint32((seed * 0x9E3779B9 + tensor * 0x85EBCA6B + 0x632BE5AB) & 0xFFFFFFFF))
@@ -87,10 +90,11 @@ def class_of(tokens: np.ndarray, seq_len: int) -> np.ndarray:
 
 
 def generate(name: str, dist: str, seed: int, tokens: np.ndarray, n_heads: int, head_dim: int,
-             seq_len: int) -> np.ndarray:
+             seq_len: int, heads: np.ndarray | None = None) -> np.ndarray:
     """Values (fp32 holding bf16-representable numbers) of tensor `name` for global `tokens`.
 
-    `seq_len` is the GLOBAL sequence length S (used by drift/class).  Shape [T, n_heads, head_dim].
+    `seq_len` is the GLOBAL sequence length S (used by drift/class).  Shape [T, n_heads, head_dim], or
+    [T, len(heads), head_dim] for a subset `heads` of the tensor's n_heads heads.
     """
     tensor = TENSOR_IDS[name]
     tokens = np.asarray(tokens, dtype=np.int64)
@@ -98,11 +102,11 @@ def generate(name: str, dist: str, seed: int, tokens: np.ndarray, n_heads: int, 
         raise ValueError(f"unknown distribution {dist!r}")
     if name == "k" and dist in ("same", "class"):
         cls = np.zeros_like(tokens) if dist == "same" else class_of(tokens, seq_len)
-        x = base_values(seed, tensor, cls, n_heads, head_dim)
+        x = base_values(seed, tensor, cls, n_heads, head_dim, heads)
         if dist == "class":
             x = np.where((cls == 3).reshape(-1, 1, 1), x * np.float32(4.0), x).astype(np.float32)
         return bf16_round(x)
-    x = base_values(seed, tensor, tokens, n_heads, head_dim)
+    x = base_values(seed, tensor, tokens, n_heads, head_dim, heads)
     if dist == "peaky" and name == "q":
         x = x * np.float32(4.0)
     elif dist == "drift":

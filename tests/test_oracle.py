@@ -312,3 +312,12 @@ def test_store_semantics():
     st.free("a")
     with pytest.raises(StoreError):
         st.free("a")
+
+
+def test_generator_head_subset_matches_full():
+    """The oracle regenerates single heads at full size: a head subset must equal those heads of the full tensor."""
+    toks = np.array([0, 5, 1023, 4096, 70000])
+    for dist in ("normal", "drift", "class"):
+        full = gen.generate("k", dist, 4, toks, 8, 16, 100000)
+        sub = gen.generate("k", dist, 4, toks, 8, 16, 100000, heads=[1, 6])
+        assert np.array_equal(full[:, [1, 6]], sub)
