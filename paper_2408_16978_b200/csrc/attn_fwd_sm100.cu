@@ -49,6 +49,10 @@ struct FwdCfg {
   using T = Tile<D>;
   static constexpr bool kSumMMA = (D == 80);     // row sums from a ones column of V (SW32 atoms only)
   static constexpr int NO = kSumMMA ? D + 16 : D;  // PV N / O columns
+  // separate P buffer (d <= 80): S0, S1, P, O0, O1 fit the 512 TMEM columns, so S_t(j+1) can be computed while the
+  // softmax of S_t(j) runs; d = 128 keeps P aliased onto S_t (S_t(j+1) then waits for PV_t(j))
+  static constexpr bool kSepP = 2 * 128 + 64 + 2 * NO <= 512;
+  static constexpr uint32_t tP = 256, tO0 = kSepP ? 320 : 256, tOstride = kSepP ? NO : 128;
   static constexpr int kStages = (D == 128) ? 2 : 3;
   static constexpr int kQBytes = 2 * T::kBytes;
   static constexpr int kOnes = kSumMMA ? 128 * 16 * 2 : 0;      // the ones atom right after each V tile
@@ -97,13 +101,15 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
 
 // P = exp2(x*sl2 - mb) for the 128 columns of a row, packed to bf16 and stored to TMEM columns [tS, tS+64); returns
 // the sum of the fp32 values when kSum (else 0).  kPoly: every FPDT_FWD_POLY_EVERY-th pair on the FMA pipe.
-template <bool kPoly, bool kSum>
-__device__ __forceinline__ float exp_pack_store(const float* x, float sl2, float mb, uint32_t tS) {
+template <bool kPoly, bool kSum, bool kStore = true>
+__device__ __forceinline__ float exp_pack_store(const float* x, float sl2, float mb, uint32_t tS,
+                                                uint32_t* pko = nullptr) {
   float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
   const float2 s2 = make_float2(sl2, sl2), nm = make_float2(-mb, -mb);
 #pragma unroll
   for (int c = 0; c < 128; c += 32) {
-    uint32_t pk[16];
+    uint32_t pkl[16];
+    uint32_t* pk = kStore ? pkl : pko + c / 2;
 #pragma unroll
     for (int i = 0; i < 32; i += 2) {
       const float2 e = __ffma2_rn(make_float2(x[c + i], x[c + i + 1]), s2, nm);
@@ -121,7 +127,7 @@ __device__ __forceinline__ float exp_pack_store(const float* x, float sl2, float
       }
       pk[i / 2] = pack_bf16x2(pr.x, pr.y);
     }
-    tmem_st16(tS + c / 2, pk);
+    if (kStore) tmem_st16(tS + c / 2, pk);
   }
   return kSum ? (acc0.x + acc0.y) + (acc1.x + acc1.y) : 0.f;
 }
@@ -134,7 +140,8 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
   constexpr int ST = C::kStages;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  __shared__ uint64_t bar_q, bar_k[ST], bar_v[ST], bar_kv_empty[ST], bar_s[2], bar_p[2], bar_o[2];
+  __shared__ uint64_t bar_q, bar_k[ST], bar_v[ST], bar_kv_empty[ST], bar_s[2], bar_p[2], bar_o[2], bar_sfree[2],
+      bar_pvdone[2];
   __shared__ uint32_t tmem_slot;
 
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -182,6 +189,8 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
       mbar_init(smem_u32(&bar_s[t]), 1);
       mbar_init(smem_u32(&bar_p[t]), 128);
       mbar_init(smem_u32(&bar_o[t]), 1);
+      mbar_init(smem_u32(&bar_sfree[t]), 128);
+      mbar_init(smem_u32(&bar_pvdone[t]), 1);
     }
     fence_mbar_init();
   }
@@ -222,7 +231,8 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
       const uint32_t idS = idesc_bf16(128, 128, 0, 0);
       const uint32_t idPV = idesc_bf16(128, C::NO, 0, 1);
       const uint32_t tS[2] = {tmem, tmem + 128};
-      const uint32_t tO[2] = {tmem + 256, tmem + 384};
+      const uint32_t tO[2] = {tmem + C::tO0, tmem + C::tO0 + C::tOstride};
+      const uint32_t tPa[2] = {C::kSepP ? tmem + C::tP : tS[0], C::kSepP ? tmem + C::tP : tS[1]};
       auto issue_S = [&](int t, int s) {
         const uint32_t sq = sQ + t * T::kBytes, sk = sKV + s * C::kStageBytes;
 #pragma unroll
@@ -233,10 +243,48 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         const uint32_t sv = sKV + s * C::kStageBytes + T::kBytes;
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk)
-          mma_ts(tO[t], tS[t] + kk * 8, T::desc_mn(sv, kk), idPV, (j > 0 || kk > 0) ? 1u : 0u);
+          mma_ts(tO[t], tPa[t] + kk * 8, T::desc_mn(sv, kk), idPV, (j > 0 || kk > 0) ? 1u : 0u);
       };
       mbar_wait(smem_u32(&bar_q), 0);
       tc_fence_after();
+      if constexpr (C::kSepP) {
+        // per key tile j: S_t(j+1) as soon as the softmax warps have read S_t(j) out of TMEM; PV_t(j) when P_t(j)
+        // is in the shared P buffer (the softmax warps of the other tile wait for PV_t(j) before overwriting it)
+        mbar_wait(smem_u32(&bar_k[0]), 0);
+        tc_fence_after();
+        issue_S(0, 0);
+        mma_commit(smem_u32(&bar_s[0]));
+        issue_S(1, 0);
+        mma_commit(smem_u32(&bar_s[1]));
+        for (int j = 0; j < n_tiles; ++j) {
+          const int s = j % ST, s2 = (j + 1) % ST;
+          const uint32_t ph = (j / ST) & 1;
+          const bool more = j + 1 < n_tiles;
+          if (more) {
+            mbar_wait(smem_u32(&bar_k[s2]), ((j + 1) / ST) & 1);
+            mbar_wait(smem_u32(&bar_sfree[0]), j & 1);
+            TRACE(6, j);
+            tc_fence_after();
+            issue_S(0, s2);
+            mma_commit(smem_u32(&bar_s[0]));
+            mbar_wait(smem_u32(&bar_sfree[1]), j & 1);
+            tc_fence_after();
+            issue_S(1, s2);
+            mma_commit(smem_u32(&bar_s[1]));
+          }
+          mbar_wait(smem_u32(&bar_v[s]), ph);
+#pragma unroll
+          for (int t = 0; t < 2; ++t) {
+            mbar_wait(smem_u32(&bar_p[t]), j & 1);
+            TRACE(4 + t, j);
+            tc_fence_after();
+            issue_PV(t, s, j);
+            mma_commit(smem_u32(&bar_pvdone[t]));
+            if (t == 1) mma_commit(smem_u32(&bar_kv_empty[s]));
+            if (!more) mma_commit(smem_u32(&bar_o[t]));
+          }
+        }
+      } else
       for (int j = 0; j < n_tiles; ++j) {
         const int s = j % ST;
         const uint32_t ph = (j / ST) & 1;
@@ -285,8 +333,9 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
     const int r = (warp & 3) * 32 + lane;
     const uint32_t lane_off = ((warp & 3) * 32) << 16;
     uint32_t tS = tmem + t * 128 + lane_off;
-    uint32_t tO = tmem + 256 + t * 128 + lane_off;
-    asm volatile("" : "+r"(tS), "+r"(tO));
+    uint32_t tO = tmem + C::tO0 + t * C::tOstride + lane_off;
+    uint32_t tPw = C::kSepP ? tmem + C::tP + lane_off : tS;
+    asm volatile("" : "+r"(tS), "+r"(tO), "+r"(tPw));
     const int64_t qpos = q_pos_first + t * 128 + r;
     const float sl2 = a.scale_log2;
     float m_run = -INFINITY, l_run = 0.f;
@@ -300,6 +349,10 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
       tmem_ld32(tS + 64, reinterpret_cast<uint32_t*>(x) + 64);
       tmem_ld32(tS + 96, reinterpret_cast<uint32_t*>(x) + 96);
       tmem_wait_ld();
+      if constexpr (C::kSepP) {
+        tc_fence_before();
+        mbar_arrive(smem_u32(&bar_sfree[t]));  // S_t(j) is in registers: the MMA warp may compute S_t(j+1)
+      }
       if ((warp & 3) == 0 && lane == 0) TRACE(8 + 4 * t, j);
       // causal mask: only on the tile(s) that straddle the diagonal (warp-uniform fast path otherwise)
       const int64_t lim64 = qpos - (a.kv_pos0 + (int64_t)j * 128);
@@ -329,6 +382,10 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         const float alpha = need ? ex2(m_run - m_new) : 1.f;
         if constexpr (!C::kSumMMA) l_run *= alpha;
         if (j > 0) {
+          if constexpr (C::kSepP) {
+            mbar_wait(smem_u32(&bar_pvdone[t]), (j - 1) & 1);  // PV_t(j-1) has accumulated into O_t
+            tc_fence_after();
+          }
 #pragma unroll
           for (int c = 0; c < C::NO; c += 16) {
             uint32_t o[16];
@@ -345,8 +402,21 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
       // P = exp2(S*scale*log2e - m): every FPDT_FWD_POLY_EVERY-th pair on the FMA pipe, the rest on MUFU, except on
       // masked tiles (MUFU maps -inf to exactly 0)
       constexpr bool kSumHere = !C::kSumMMA;
-      const float sum = any_masked ? exp_pack_store<false, kSumHere>(x, sl2, mb, tS)
-                                   : exp_pack_store<true, kSumHere>(x, sl2, mb, tS);
+      float sum;
+      if constexpr (C::kSepP) {
+        // P in registers first; then the shared P buffer: P_0(j) after PV_1(j-1) has read it, P_1(j) after PV_0(j)
+        uint32_t pk[64];
+        sum = any_masked ? exp_pack_store<false, kSumHere, false>(x, sl2, mb, 0, pk)
+                         : exp_pack_store<true, kSumHere, false>(x, sl2, mb, 0, pk);
+        if (t == 0 && j > 0) mbar_wait(smem_u32(&bar_pvdone[1]), (j - 1) & 1);
+        if (t == 1) mbar_wait(smem_u32(&bar_pvdone[0]), j & 1);
+        tc_fence_after();
+#pragma unroll
+        for (int c = 0; c < 64; c += 16) tmem_st16(tPw + c, pk + c);
+      } else {
+        sum = any_masked ? exp_pack_store<false, kSumHere>(x, sl2, mb, tPw)
+                         : exp_pack_store<true, kSumHere>(x, sl2, mb, tPw);
+      }
       if constexpr (kSumHere) l_run += sum;
       if ((warp & 3) == 0 && lane == 0) TRACE(10 + 4 * t, j);
       tmem_wait_st();

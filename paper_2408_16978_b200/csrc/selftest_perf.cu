@@ -1,6 +1,8 @@
 // Micro-benchmarks of the sm_100a units the attention kernels lean on (diagnostic, not on the hot path):
 // tcgen05.mma issue cost per instruction shape, MUFU ex2 throughput, TMEM load throughput.
 // Each runs one CTA per SM (148 CTAs) and reports the median SM-cycles per operation of CTA 0.
+#include <cuda_fp16.h>
+
 #include "attn_tile.cuh"
 #include "fpdt.h"
 
@@ -77,6 +79,52 @@ __global__ void __launch_bounds__(1024, 1) perf_kernel(int what, int n, int iter
     t1 = clock64();
 #pragma unroll
     for (int c = 0; c < 8; ++c) sink += x[c];
+  } else if (what == 5 || what == 6 || what == 7 || what == 8) {
+    // 5: MUFU ex2 throughput, 32 independent chains per thread; 6: MUFU ex2 latency, one chain;
+    // 7: FMA-pipe exp2 (packed f32x2 polynomial) throughput, 16 independent pairs; 8: ex2.approx.f16x2, 16 chains
+    float x[32];
+#pragma unroll
+    for (int c = 0; c < 32; ++c) x[c] = -0.001f * threadIdx.x - 0.01f * c;
+    t0 = clock64();
+    if (what == 5) {
+      for (int i = 0; i < iters; i += 32) {
+#pragma unroll
+        for (int c = 0; c < 32; ++c) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x[c]));
+      }
+    } else if (what == 6) {
+      for (int i = 0; i < iters; ++i) asm volatile("ex2.approx.ftz.f32 %0, %0;" : "+f"(x[0]));
+    } else if (what == 7) {
+      for (int i = 0; i < iters; i += 32) {
+#pragma unroll
+        for (int c = 0; c < 32; c += 2) {
+          float2 v = make_float2(fmaxf(x[c], -127.f), fmaxf(x[c + 1], -127.f));
+          const float2 kR = make_float2(12582912.f, 12582912.f);
+          const float2 j = __fadd2_rn(v, kR);
+          const float2 f = __fadd2_rn(v, __fadd2_rn(kR, make_float2(-j.x, -j.y)));
+          float2 p = __ffma2_rn(f, make_float2(0.055f, 0.055f), make_float2(0.2426f, 0.2426f));
+          p = __ffma2_rn(p, f, make_float2(0.6933f, 0.6933f));
+          p = __ffma2_rn(p, f, make_float2(0.99993f, 0.99993f));
+          x[c] = -__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23));
+          x[c + 1] = -__int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23));
+        }
+      }
+    } else {
+      uint32_t h[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        __half2 t = __floats2half2_rn(x[2 * c], x[2 * c + 1]);
+        h[c] = *reinterpret_cast<uint32_t*>(&t);
+      }
+      for (int i = 0; i < iters; i += 32) {
+#pragma unroll
+        for (int c = 0; c < 16; ++c) asm volatile("ex2.approx.f16x2 %0, %0;" : "+r"(h[c]));
+      }
+#pragma unroll
+      for (int c = 0; c < 16; ++c) x[c] = __uint_as_float(h[c]);
+    }
+    t1 = clock64();
+#pragma unroll
+    for (int c = 0; c < 32; ++c) sink += x[c];
   } else if (what == 3) {
     const uint32_t lane_off = ((warp & 3) * 32) << 16;
     uint32_t r[32];
@@ -105,7 +153,7 @@ __global__ void __launch_bounds__(1024, 1) perf_kernel(int what, int n, int iter
 extern "C" int fpdt_selftest_perf(int what, int n, int iters, float* out, void* stream) {
   const int smem = 65536 + 1024;
   cudaFuncSetAttribute(fpdt::perf_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  const int threads = ((what == 2 || what == 4) && n > 0) ? n : 128;  // n = threads per CTA for the ALU tests
+  const int threads = ((what == 2 || what >= 4) && n > 0) ? n : 128;  // n = threads per CTA for the ALU tests
   fpdt::perf_kernel<<<148, threads, smem, static_cast<cudaStream_t>(stream)>>>(what, n, iters, out);
   return (int)cudaGetLastError();
 }

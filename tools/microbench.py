@@ -27,3 +27,10 @@ for what, name in ((2, "MUFU ex2"), (4, "poly exp2")):
         print(f"{name} {thr} thr/SM, 8 chains/thread: {c:.2f} cyc/op/thread -> {thr / c:.1f} ops/clk/SM")
 run(3, 0, 64)
 print(f"tcgen05.ld x32 per warp (4 warps, 4 in flight): {run(3, 0, 4096):.2f} cyc/op")
+for what, name, per in ((5, "MUFU ex2 32 chains", 1), (7, "poly exp2 x2 16 pairs", 1), (8, "ex2.f16x2 16 chains", 2)):
+    for thr in (128, 256, 512, 1024):
+        run(what, thr, 64)
+        c = run(what, thr, 4096)
+        print(f"{name}: {thr} thr/SM: {c:.2f} cyc/elem/thread -> {per * thr / c:.1f} elem/clk/SM")
+run(6, 128, 64)
+print(f"MUFU ex2 latency (one dependent chain): {run(6, 128, 4096):.1f} cyc")
