@@ -46,7 +46,8 @@ static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs -
 #ifndef FPDT_BWD_EXP
 #define FPDT_BWD_EXP 0  // timing experiments only (wrong results): 1 no dQ reduce, 2 no dQ staging/reduce,
                        // 3 no stats loads, 4 = 2 + 3, 5 no wait for the previous dQ reduce's smem read,
-                       // 6 dQ reduce every other tile only, 7 only the 16-column dQ box
+                       // 6 dQ reduce every other tile only, 7 only the 16-column dQ box, 8 only even key tiles reduce,
+                       // 9 linear staging + one 1-D bulk reduce (correct, bank-conflicted), 10 trailing 16 columns by REDG
 #endif
 #ifndef FPDT_BWD_POLY_EVERY
 #define FPDT_BWD_POLY_EVERY 4  // one exponential pair in FPDT_BWD_POLY_EVERY goes to the FMA-pipe polynomial
@@ -73,6 +74,7 @@ struct PipeCfg {
 
 struct TmapSet {
   CUtensorMap q, k, v, o, dq32, dq16;  // dq32: 32-column fp32 boxes, 128B swizzle; dq16: 16 columns, 64B swizzle
+  CUtensorMap dq32h, dq16h;           // the same with 64-row boxes (cluster-pair mode: one half tile per CTA)
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -107,8 +109,16 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
                : "memory");
 }
+// 1-D bulk reduce-add of `bytes` contiguous fp32 from shared to global memory (bulk async-group completion)
+__device__ __forceinline__ void bulk_reduce_add_f32(void* gdst, uint32_t ssrc, uint32_t bytes) {
+  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
+                   reinterpret_cast<uint64_t>(gdst)),
+               "r"(ssrc), "r"(bytes)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ float4 lds4(const float* p) {
@@ -116,7 +126,7 @@ __device__ __forceinline__ float4 lds4(const float* p) {
   return *reinterpret_cast<const float4*>(p);
 }
 
-template <int D, bool kRedDQ>
+template <int D, bool kPair>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdArgs a) {
   using T = Tile<D>;
@@ -131,7 +141,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
   constexpr int B_KV = 0, B_QF = 1, B_QE = B_QF + QS, B_OF = B_QE + QS, B_OE = B_OF + OS, B_S = B_OE + OS,
                 B_SFREE = B_S + 1, B_DP = B_SFREE + 1, B_P = B_DP + 1, B_DS = B_P + 1,
                 B_DSFREE = B_DS + 1, B_DQF = B_DSFREE + 1, B_DQE = B_DQF + 1, B_KVDONE = B_DQE + 1,
-                B_NUM = B_KVDONE + 1;
+                B_FULL = B_KVDONE + 1, B_PFREE = B_FULL + 2, B_NUM = B_PFREE + 2;
   static_assert(B_NUM <= 30, "barrier area");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::oBars + 30 * 8);
 
@@ -174,10 +184,17 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
     mbar_init(bar(B_DQF), 1);
     mbar_init(bar(B_DQE), 128);
     mbar_init(bar(B_KVDONE), 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(bar(B_FULL + b), 1);
+      mbar_init(bar(B_PFREE + b), 1);
+    }
     fence_mbar_init();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync();  // the partner CTA's barriers are initialised before any remote arrive / st.async
+  else
+    __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -443,6 +460,26 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
     const int t128 = threadIdx.x - 256;
     uint32_t tdQ = tmem + C::tdQ + (((warp & 3) * 32) << 16);
     asm volatile("" : "+r"(tdQ));
+    // cluster pair: rank 0 holds the even key tile, rank 1 the next one; on the causal diagonal the even tile sees
+    // (qt_first_partner - qt_first) more query tiles, which it reduces alone (n < n_solo)
+    uint32_t crank = 0, peer_stg = 0, peer_full[2] = {0, 0}, peer_pfree[2] = {0, 0};
+    int n_solo = 0;
+    bool recv_rows = true;
+    if constexpr (kPair) {
+      crank = cluster_ctarank();
+      recv_rows = (r >> 6) == (int)crank;  // this thread's query row is in the half this CTA reduces
+      peer_stg = mapa(sDQ, crank ^ 1);
+      for (int b2 = 0; b2 < 2; ++b2) {
+        peer_full[b2] = mapa(bar(B_FULL + b2), crank ^ 1);
+        peer_pfree[b2] = mapa(bar(B_PFREE + b2), crank ^ 1);
+      }
+      if (crank == 0 && a.causal) {
+        const int64_t rel = kv_base + 128 - a.q_pos0;
+        int qf = rel > 0 ? (int)(rel / 128) : 0;
+        if (qf > n_qt_total) qf = n_qt_total;
+        n_solo = (qf - qt_first) * G;
+      }
+    }
     for (int n = 0; n < n_iter; ++n) {
       const int qt = qt_first + n / G, h = g * G + n % G;
       mbar_wait(bar(B_DQF), n & 1);
@@ -455,12 +492,69 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       tc_fence_before();
       mbar_arrive(bar(B_DQE));
       if (FPDT_BWD_EXP == 2 || FPDT_BWD_EXP == 4) continue;
-      if constexpr (kRedDQ) {
-        // vector reductions straight from registers into the fp32 dq accumulator (no shared-memory staging)
-        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (int64_t)h * a.dq_head_stride + ((int64_t)qt * 128 + r) * D);
+      if constexpr (kPair) {
+        // Cluster pair (two CTAs on neighbouring key tiles of one head, same query tiles): the per-SM write path to
+        // L2 is what limits the dQ reduce-add, so each CTA reduces only HALF of the query rows of a tile — rows
+        // [64 rank, 64 rank + 64): its own partial plus the partner's, which arrives over DSMEM (st.async) — and
+        // sends its other half to the partner.  Double-buffered 64-row staging (the same 40 KB as one full tile).
+        if (n < n_solo) {  // causal diagonal: a query tile the partner does not see; rare, vector atomics
+          float4* dst = reinterpret_cast<float4*>(a.dq_acc + (int64_t)h * a.dq_head_stride + ((int64_t)qt * 128 + r) * D);
 #pragma unroll
-        for (int c = 0; c < D; c += 4)
-          atomicAdd(dst + c / 4, make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale, v[c + 3] * a.scale));
+          for (int c = 0; c < D; c += 4)
+            atomicAdd(dst + c / 4, make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale,
+                                               v[c + 3] * a.scale));
+          continue;
+        }
+        const int k = n - n_solo, bsel = k & 1;
+        const uint32_t par = (k >> 1) & 1;
+        const int rr = r & 63;
+        auto half_off = [&](int c) -> uint32_t {  // 64-row staging: 32-column chunks 128B-swizzled, then 16 columns
+          const int j = (c & 31) >> 2;
+          if (c < (D / 32) * 32) return (c >> 5) * 8192 + rr * 128 + ((j ^ (rr & 7)) << 4);
+          return (D / 32) * 8192 + rr * 64 + ((j ^ ((rr >> 1) & 3)) << 4);
+        };
+        constexpr uint32_t HB = 64 * D * 4;
+        const float2 sc2 = make_float2(a.scale, a.scale);
+        if (!recv_rows) {
+          mbar_wait_cluster(bar(B_PFREE + bsel), par);  // the partner's buffer has been read by its last reduce
+#pragma unroll
+          for (int c = 0; c < D; c += 4) {
+            const float2 x0 = __fmul2_rn(make_float2(v[c], v[c + 1]), sc2);
+            const float2 x1 = __fmul2_rn(make_float2(v[c + 2], v[c + 3]), sc2);
+            uint32_t dst = peer_stg + bsel * HB;
+            asm volatile("" : "+r"(dst));  // address math per store: 20 hoisted addresses would spill
+            st_async_v4(dst + half_off(c), make_float4(x0.x, x0.y, x1.x, x1.y), peer_full[bsel]);
+          }
+          continue;
+        }
+        const bool tr0 = (r & 63) == 0;
+        if (tr0) bulk_wait_read1();  // buffer bsel's reduce (2 tiles ago) has been read; the last one may run on
+        named_bar(2, 64);
+        if (tr0) {
+          mbar_expect_tx(bar(B_FULL + bsel), HB);
+          mbar_arrive_remote(peer_pfree[bsel]);
+        }
+        mbar_wait_cluster(bar(B_FULL + bsel), par);
+        uint8_t* stg = smem + C::oDQ + bsel * HB;
+#pragma unroll
+        for (int c = 0; c < D; c += 4) {
+          float4* q4 = reinterpret_cast<float4*>(stg + half_off(c));
+          const float4 pv = *q4;
+          const float2 x0 = __ffma2_rn(make_float2(v[c], v[c + 1]), sc2, make_float2(pv.x, pv.y));
+          const float2 x1 = __ffma2_rn(make_float2(v[c + 2], v[c + 3]), sc2, make_float2(pv.z, pv.w));
+          *q4 = make_float4(x0.x, x0.y, x1.x, x1.y);
+        }
+        fence_async_shared();
+        named_bar(2, 64);
+        if (tr0) {
+          const uint32_t sb = sDQ + bsel * HB;
+          const int row0 = qt * 128 + 64 * (int)crank;
+#pragma unroll
+          for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_3d(&tm.dq32h, sb + cc * 8192, cc * 32, row0, h);
+          if (D % 32) tma_reduce_add_3d(&tm.dq16h, sb + (D / 32) * 8192, (D / 32) * 32, row0, h);
+          bulk_commit();
+          TRACE(11, n);
+        }
         continue;
       }
       // the previous bulk reduce must have finished reading the staging tile
@@ -471,13 +565,22 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       // 32 rows of a warp hit all 32 banks (an unswizzled 320-byte row pitch would be a 16-way bank conflict)
       const float2 sc = make_float2(a.scale, a.scale);
       uint8_t* stg = smem + C::oDQ;
+      constexpr int kRedCols = (FPDT_BWD_EXP == 10 && D % 32) ? 16 : 0;  // trailing columns reduced with REDG
+      if (kRedCols) {
+        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (int64_t)h * a.dq_head_stride + ((int64_t)qt * 128 + r) * D);
 #pragma unroll
-      for (int c = 0; c < D; c += 4) {
+        for (int c = D - kRedCols; c < D; c += 4)
+          atomicAdd(dst + c / 4, make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale, v[c + 3] * a.scale));
+      }
+#pragma unroll
+      for (int c = 0; c < D - kRedCols; c += 4) {
         const float2 x0 = __fmul2_rn(make_float2(v[c], v[c + 1]), sc);
         const float2 x1 = __fmul2_rn(make_float2(v[c + 2], v[c + 3]), sc);
         const int j = (c & 31) >> 2;
         uint32_t off;
-        if (c < (D / 32) * 32)
+        if (FPDT_BWD_EXP == 9)
+          off = (r * D + c) * 4;  // linear [128][D] (bank-conflicted; timing experiment for the 1-D bulk reduce)
+        else if (c < (D / 32) * 32)
           off = (c >> 5) * 16384 + r * 128 + ((j ^ (r & 7)) << 4);
         else
           off = (D / 32) * 16384 + r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
@@ -485,19 +588,26 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       }
       fence_async_shared();
       named_bar(1, 128);
-      if (FPDT_BWD_EXP != 1 && !(FPDT_BWD_EXP == 6 && (n & 1)) && t128 == 0) {
+      if (FPDT_BWD_EXP == 9 && t128 == 0) {
+        bulk_reduce_add_f32(a.dq_acc + (int64_t)h * a.dq_head_stride + (int64_t)qt * 128 * D, sDQ, 128 * D * 4);
+        bulk_commit();
+      } else if (FPDT_BWD_EXP != 1 && !(FPDT_BWD_EXP == 6 && (n & 1)) && !(FPDT_BWD_EXP == 8 && (kt & 1)) &&
+                 t128 == 0) {
 #pragma unroll
         for (int cc = 0; cc < D / 32; ++cc)
           if (FPDT_BWD_EXP != 7) tma_reduce_add_3d(&tm.dq32, sDQ + cc * 16384, cc * 32, qt * 128, h);
-        if (D % 32) tma_reduce_add_3d(&tm.dq16, sDQ + (D / 32) * 16384, (D / 32) * 32, qt * 128, h);
+        if (D % 32 && kRedCols == 0) tma_reduce_add_3d(&tm.dq16, sDQ + (D / 32) * 16384, (D / 32) * 32, qt * 128, h);
         bulk_commit();
         TRACE(11, n);
       }
     }
-    if (!kRedDQ && t128 == 0) bulk_wait0();
+    if (t128 == 0 || (kPair && (r & 63) == 0)) bulk_wait0();
   }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (kPair)
+    cluster_sync();  // no CTA leaves while its partner may still write into its shared memory
+  else
+    __syncthreads();
   if (warp == 13) tmem_dealloc<512>(tmem);
 #undef TRACE
 }
@@ -505,30 +615,45 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
 template <int D>
 int launch_pipe(const BwdArgs& a, cudaStream_t s) {
   using C = PipeCfg<D>;
-  // FPDT_BWD_DQ=red: dQ partials by vector atomics from registers; default: TMA bulk reduce-add from smem staging
-  static const bool red = [] {
-    const char* e = getenv("FPDT_BWD_DQ");
-    return e && strcmp(e, "red") == 0;
+  // FPDT_BWD_PAIR=1: cluster pairs split the dQ reduce-add (see kernel).  Off by default: measured 579 TFLOP/s vs 867
+  // (the two CTAs' dQ warps run in lockstep through the DSMEM exchange, and that chain is longer than the reduce)
+  static const bool pair = [] {
+    const char* e = getenv("FPDT_BWD_PAIR");
+    return e && strcmp(e, "1") == 0;
   }();
   TmapSet tm;
   bool ok = make_tile_tmap<D>(&tm.q, a.q.base, a.q.rows, a.q.heads);
   ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
   ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
   ok &= make_tile_tmap<D>(&tm.o, a.dout.base, a.dout.rows, a.dout.heads);
-  ok &= make_tmap_f32_head_major(&tm.dq32, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 32, 128,
-                                 CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_tmap_f32_head_major(&tm.dq16, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 16, 128,
-                                 CU_TENSOR_MAP_SWIZZLE_64B);
-  if (!ok) return -1;
-  auto kern = red ? attn_bwd_pipe_kernel<D, true> : attn_bwd_pipe_kernel<D, false>;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[red]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    attr_set[red] = true;
+  for (int rows = 128; rows >= 64; rows -= 64) {
+    ok &= make_tmap_f32_head_major(rows == 128 ? &tm.dq32 : &tm.dq32h, a.dq_acc, a.n_q_rows, a.hq, D,
+                                   a.dq_head_stride, 32, rows, CU_TENSOR_MAP_SWIZZLE_128B);
+    ok &= make_tmap_f32_head_major(rows == 128 ? &tm.dq16 : &tm.dq16h, a.dq_acc, a.n_q_rows, a.hq, D,
+                                   a.dq_head_stride, 16, rows, CU_TENSOR_MAP_SWIZZLE_64B);
   }
-  dim3 grid(a.n_kv_rows / 128, a.hq / a.G);
-  kern<<<grid, kThreads, C::kSmem, s>>>(tm, a);
-  return (int)cudaGetLastError();
+  if (!ok) return -1;
+  const int n_kv_tiles = a.n_kv_rows / 128;
+  const bool use_pair = pair && (n_kv_tiles % 2 == 0);
+  auto kern = use_pair ? attn_bwd_pipe_kernel<D, true> : attn_bwd_pipe_kernel<D, false>;
+  static bool attr_set[2] = {false, false};
+  if (!attr_set[use_pair]) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr_set[use_pair] = true;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(n_kv_tiles, a.hq / a.G);
+  cfg.blockDim = dim3(kThreads);
+  cfg.dynamicSmemBytes = C::kSmem;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = use_pair ? 2 : 1;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return (int)cudaLaunchKernelEx(&cfg, kern, tm, a);
 }
 
 }  // namespace
