@@ -11,3 +11,6 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn
   python bench.py --seq 131072 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_bwd_bench.log 2>&1; echo "ncu bwd rc=$?"
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:attn_fwd -s 1 -c 1 -o gpurun_out/prof_fwd_bench \
   python bench.py --seq 131072 --steps 1 --warmup 0 --no-e2e --no-cpu-baseline > gpurun_out/ncu_fwd_bench.log 2>&1; echo "ncu fwd rc=$?"
+timeout 120 python tools/trace_pair.py bwd 65536 32 128 100 2>&1 | head -1
+timeout 120 python tools/trace_pair.py fwd 65536 32 128 100 2>&1 | head -1
+timeout 900 python -m pytest tests -x -q -m gpu > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"; tail -2 gpurun_out/pytest_gpu.log
