@@ -94,3 +94,30 @@ def test_oracle_parity_multirank_fp32():
     got = run_group(x, 2, C, "fp32", 1)
     errs = {n: rel_err(got[n], ref[n]) for n in ("o", "lse", "dq", "dk", "dv")}
     assert all(e <= TOL["fp32"] for e in errs.values()), errs
+
+
+@pytest.mark.parametrize("p,Hq,Hkv", [
+    (4, 32, 8),    # Llama-3 8B ratio (BASELINE configs[2]: 32 q / 8 kv heads, d = 128) at p = 4
+    (8, 64, 8),    # 70B ratio (configs[4]: 64 q / 8 kv heads) at p = 8: one kv head per rank
+])
+def test_gqa_configs_sampled_rows(p, Hq, Hkv):
+    """BASELINE configs[2] / [4] head shapes and world sizes at a reduced sequence (S = 16K, chunk 4K): sampled rows
+    of O, lse, dQ against the oracle's single-row definition, and the dK/dV identities on every kv head."""
+    from oracle import sampled
+    S, d, C = 16384, 128, 4096
+    x = gen.make_inputs("drift", 11, S, Hq, Hkv, d)
+    got = run_group(x, p, C, "bf16", 1)
+    rows = np.array(sorted(set([0, 1, 255, 256, C - 1, C, S - 1, 2 * C + 77, 3 * C + 4000, 9999])))
+    G = Hq // Hkv
+    for h in (0, Hq - 1):
+        g = h // G
+        dq, o, lse = sampled.rows_dq(x["q"][rows, h], x["do"][rows, h], rows, x["k"][:, g].astype(np.float64),
+                                     x["v"][:, g].astype(np.float64), sampled.default_scale(d))
+        errs = {"o": rel_err(got["o"][rows, h], o), "lse": rel_err(got["lse"][rows, h], lse),
+                "dq": rel_err(got["dq"][rows, h], dq)}
+        assert all(e <= TOL["bf16"] for e in errs.values()), (h, errs)
+    dk_sum, dk_abs = got["dk"].sum(0), np.abs(got["dk"]).sum(0)
+    assert np.max(np.abs(dk_sum) / dk_abs) <= TOL["bf16"]
+    dv_sum, dv_abs = got["dv"].sum(0), np.abs(got["dv"]).sum(0)
+    do_sum = x["do"].reshape(S, Hkv, G, d).sum(axis=(0, 2))
+    assert np.max(np.abs(dv_sum - do_sum) / dv_abs) <= TOL["bf16"]
