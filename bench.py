@@ -356,6 +356,11 @@ def run_ours(args):
         "e2e": e2e,
         "gpu_launches": launches,
         "pcie_bytes_per_step": {"h2d": h2d_lib, "d2h": d2h_lib},
+        # offload / prefetch traffic of the library (per rank) against the host link: pinned copies measured on the
+        # box at 55.6 GB/s H2D, 57.3 GB/s D2H (profiles/r01_box_probe.md); the transfers overlap compute
+        "host_link": {"h2d_GBps": h2d_lib / (ms / 1e3) / 1e9, "d2h_GBps": d2h_lib / (ms / 1e3) / 1e9,
+                      "measured_peak_GBps": {"h2d": 55.6, "d2h": 57.3}},
+        "a2a_bytes_per_step": (st1["bytes_a2a"] - st0["bytes_a2a"]) // args.steps,
         "wall_s_timed": wall,
         "cpu_baseline": cpu,
     }
