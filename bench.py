@@ -35,8 +35,11 @@ WORKLOAD = dict(name="GPT-2.7B-shaped causal attention layer (BASELINE.json conf
                 d=80, C=65536, dtype="bf16")
 
 
-def flops_per_step(S, Hq, d):
+def flops_per_step(S, Hq, d, keep=None, C=None):
     pairs = S * (S + 1) / 2  # causal (query, key) pairs incl. the diagonal
+    if keep is not None:  # block-sparse (§5.6): only the kept chunk blocks are computed
+        u = keep.shape[0]
+        pairs = u * C * (C + 1) / 2 + float(np.tril(keep, -1).sum()) * C * C
     return 4 * d * Hq * pairs, 10 * d * Hq * pairs  # fwd (QK^T, PV), bwd (recompute QK^T, dP, dV, dK, dQ)
 
 
@@ -178,6 +181,10 @@ def run_ours(args):
     # NCCL id through torch.distributed (plumbing only)
     nid = distributed.broadcast_nccl_id(rank, world, fpdt.fpdt_get_unique_id)
     ctx = fpdt.FPDTContext(world, rank, nid, local)
+    keep = None
+    if args.sparsity > 0:
+        keep = gen.sparsity_plan(S // C, args.sparsity, seed=0)
+        ctx.set_sparsity(keep)
     genlib = _lib.load_generator()
     bf = torch.bfloat16
 
@@ -237,7 +244,7 @@ def run_ours(args):
     h2d_lib = (st1["bytes_h2d"] - st0["bytes_h2d"]) // args.steps
     d2h_lib = (st1["bytes_d2h"] - st0["bytes_d2h"]) // args.steps
 
-    f_fwd, f_bwd = flops_per_step(S, Hq, d)
+    f_fwd, f_bwd = flops_per_step(S, Hq, d, keep, C)
     tokens_per_s = S / (ms / 1e3)
     tflops_gpu = (f_fwd + f_bwd) / (world * ms / 1e3) / 1e12
     burst, sustained, hbm, peak_src = load_peaks()
@@ -344,7 +351,8 @@ def run_ours(args):
         "config": {"workload": W["name"], "S": S, "heads_q": Hq, "heads_kv": Hkv, "head_dim": d, "chunk": C,
                    "chunks": S // C, "s_local": s_local, "offload": offload, "causal": 1,
                    "parallelism": f"ulysses-sp{world}", "l2": "inputs 2.7 GB/tensor >> 126 MB L2, no flush",
-                   "flops_per_step": f_fwd + f_bwd, "flop_convention": "14*d per causal pair per q-head"},
+                   "flops_per_step": f_fwd + f_bwd, "flop_convention": "14*d per causal pair per q-head",
+                   "sparsity": args.sparsity},
         "roofline": {"bound": "tensor", "kernel": "attn_bwd_pipe_kernel<80> (tcgen05 pair backward)",
                      "achieved": ach_bwd, "peak": sustained, "unit": "TFLOP/s", "frac": ach_bwd / sustained,
                      "traffic": traffic, "peak_source": peak_src + ", sustained bf16 (kernel timed inside a long step)",
@@ -381,6 +389,8 @@ def main():
     ap.add_argument("--offload", type=int, default=1)
     ap.add_argument("--seq", type=int, default=0, help="override S (testing)")
     ap.add_argument("--chunk", type=int, default=0, help="override the chunk size (testing)")
+    ap.add_argument("--sparsity", type=float, default=0.0,
+                    help="block sparsity rho (PAPER.md §5.6 / Table sparsity): fraction of causal chunk blocks dropped")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -146,3 +146,19 @@ def make_inputs(dist: str, seed: int, seq_len: int, n_q_heads: int, n_kv_heads: 
         "v": generate("v", dist, seed, tokens, n_kv_heads, head_dim, seq_len),
         "do": generate("do", dist, seed, tokens, n_q_heads, head_dim, seq_len),
     }
+
+
+def sparsity_plan(n_chunks: int, rho: float, seed: int = 0) -> np.ndarray:
+    """Block-sparsity plan keep[m][i] (bool, [u,u]) over (query chunk m, key chunk i) — an INPUT of the method
+    (§5.6 "block sparse attention"): every causally valid block i <= m is kept
+    except floor(rho * u(u+1)/2) off-diagonal blocks chosen by a seeded permutation; diagonal blocks are never
+    dropped (capped at all off-diagonal blocks); blocks i > m are False (causally invisible)."""
+    u = int(n_chunks)
+    keep = np.tril(np.ones((u, u), dtype=bool))
+    off = [(m, i) for m in range(u) for i in range(m)]
+    n_drop = min(int(np.floor(rho * u * (u + 1) / 2)), len(off))
+    if n_drop:
+        rng = np.random.default_rng(np.uint64(seed) * np.uint64(0x9E3779B9) + np.uint64(u))
+        for idx in rng.permutation(len(off))[:n_drop]:
+            keep[off[idx]] = False
+    return keep

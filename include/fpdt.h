@@ -115,6 +115,17 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
                   int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
                   int dtype, int offload, float softmax_scale, void* stream);
 
+/* Block-sparse attention (§5.6, Table "MFU at different attention sparsity": "only part of the tokens in
+ * key and value will be fetched from the host memory, while the query will always be the entire sequence").
+ *   keep: host array [n_chunks][n_chunks], row m = query chunk, column i = key chunk (GLOBAL chunk indices, chunk
+ *   size = the calls' chunk_size); nonzero = the block is computed.  Entries i > m are ignored (causally invisible);
+ *   diagonal blocks must be kept.  Copied; n_chunks = 0 (keep NULL) restores dense attention.
+ * Applies to the following fpdt_attn_fwd calls (which check n_chunks == S / chunk_size: FPDT_ERR_ARG, a dropped
+ * diagonal: FPDT_ERR_ARG, offload == 0: FPDT_ERR_UNSUPPORTED); fpdt_attn_bwd uses the plan of its forward.
+ * Dropped blocks are neither fetched from host memory nor computed: key j is visible to query i iff j <= i and
+ * keep[i / C][j / C].  Collective: every rank passes the same plan. */
+int fpdt_set_sparsity(fpdt_ctx* ctx, const uint8_t* keep, int64_t n_chunks);
+
 /* Message of the last non-OK status returned on this thread ("" if none). */
 const char* fpdt_last_error(void);
 

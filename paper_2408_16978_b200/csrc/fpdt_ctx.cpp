@@ -140,6 +140,10 @@ struct fpdt_ctx {
   // saved state
   bool fwd_done = false;
   Config saved;
+  // block-sparsity plan (fpdt_set_sparsity): keep[m*u + i] over (query chunk m, key chunk i); empty = dense.
+  // The forward copies it into saved_plan; the backward of that forward uses the copy.
+  std::vector<uint8_t> plan, saved_plan;
+  int64_t plan_u = 0;
   const void *saved_q = nullptr, *saved_k = nullptr, *saved_v = nullptr;
   fpdt_stats stats{};
   // kernel timing
@@ -389,7 +393,13 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   }
   int fetch = 0;
   int64_t high = 0;
+  // block sparsity (§5.6): skipped key chunks are neither fetched nor computed
+  const std::vector<uint8_t>& plan = ctx->saved_plan;
+  auto keep = [&](int64_t m, int64_t i) { return plan.empty() || plan[(size_t)(m * u + i)] != 0; };
   for (int64_t m = 0; m < u; ++m) {
+    int64_t last_kept = -1;  // the last earlier key chunk chunk m attends
+    for (int64_t i = 0; i < m; ++i)
+      if (keep(m, i)) last_kept = i;
     // ---- views of the current chunk's q, k, v in the head layout
     HeadView qv, kv, vv;
     int64_t q_row0, kv_row0_cur;
@@ -474,11 +484,12 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       a.n_kv_rows = (int)C;
       a.kv_pos0 = m * C;
       a.has_prev = 0;
-      a.is_final = (m == 0);
+      a.is_final = (last_kept < 0);
       launch_fwd(ctx, c, a, cs);
       if (p > 1) rec(ctx->ev_recv_used_c[m & 1], cs);
       // F7/F8: earlier chunks fetched from the host store, double-buffered
       for (int64_t i = 0; i < m; ++i) {
+        if (!keep(m, i)) continue;
         const int sl = fetch & 1;
         wait(ctx->s_h2d, ctx->ev_slot_free[sl]);
         wait(ctx->s_h2d, ctx->ev_off[i]);
@@ -491,7 +502,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
         a.kv_row0 = 0;
         a.kv_pos0 = i * C;
         a.has_prev = 1;
-        a.is_final = (i == m - 1);
+        a.is_final = (i == last_kept);
         launch_fwd(ctx, c, a, cs);
         rec(ctx->ev_slot_free[sl], cs);
         ++fetch;
@@ -703,27 +714,34 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       rec(ctx->ev_q_free[b], cs);
     }
     int step = 0;
+    const std::vector<uint8_t>& plan = ctx->saved_plan;
+    auto keep = [&](int64_t i, int64_t j) { return i == j || plan.empty() || plan[(size_t)(i * u + j)] != 0; };
+    std::vector<char> dq_started((size_t)u, 0);  // chunk i's dq partial already holds contributions (host store)
     for (int64_t j = 0; j < u; ++j) {
       const int ks = (int)(j & 1);
+      int64_t last_i = j;  // the last query chunk that attends key chunk j
+      for (int64_t i = j; i < u; ++i)
+        if (keep(i, j)) last_i = i;
       // B3: fetch kv_j
       wait(ctx->s_h2d, ctx->ev_kv_free[ks]);
       h2d(ctx, kvs[ks], ctx->host + hl.kv(j, u), (size_t)C * row_kv2);
       rec(ctx->ev_kv_filled[ks], ctx->s_h2d);
       wait(cs, ctx->ev_kv_filled[ks]);
-      for (int64_t i = j; i < u; ++i, ++step) {
-        const int sl = step & 1;
-        // B4: fetch q_i, dO_i and (j > 0) the dq partial of chunk i
+      for (int64_t i = j; i < u; ++i) {
+        if (!keep(i, j)) continue;
+        const int sl = (step++) & 1;
+        // B4: fetch q_i, dO_i and (when it already holds contributions) the dq partial of chunk i
         wait(ctx->s_h2d, ctx->ev_q_free[sl]);
         wait(ctx->s_h2d, ctx->ev_doff[i]);
         h2d(ctx, qs[sl], ctx->host + hl.q(i), (size_t)C * row_q);
         h2d(ctx, dos[sl], ctx->host + hl.dO(i, u), (size_t)C * row_q);
-        if (j > 0) {
+        if (dq_started[i]) {
           wait(ctx->s_h2d, ctx->ev_dqoff[i]);
           h2d(ctx, dqs[sl], ctx->host + hl.dq(i, u), (size_t)C * hq * d * 4);
         }
         rec(ctx->ev_q_filled[sl], ctx->s_h2d);
         wait(cs, ctx->ev_q_filled[sl]);
-        if (j == 0) FPDT_CHECK_CUDA(cudaMemsetAsync(dqs[sl], 0, (size_t)C * hq * d * 4, cs));
+        if (!dq_started[i]) FPDT_CHECK_CUDA(cudaMemsetAsync(dqs[sl], 0, (size_t)C * hq * d * 4, cs));
         BwdArgs a;
         a.q = {qs[sl], C, hq, 0};
         a.dout = {dos[sl], C, hq, 0};
@@ -748,7 +766,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
         a.dk_acc = dk_acc;
         a.dv_acc = dv_acc;
         a.kv_acc_init = (i == j);
-        a.kv_final = (i == u - 1);
+        a.kv_final = (i == last_i);
         set_kv_out(a, j);
         launch_bwd(ctx, c, a, cs);
         if (i == j) {
@@ -761,6 +779,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
           wait(ctx->s_d2h, ctx->ev_dq_ready[sl]);
           d2h(ctx, ctx->host + hl.dq(i, u), dqs[sl], (size_t)C * hq * d * 4);
           rec(ctx->ev_dqoff[i], ctx->s_d2h);
+          dq_started[i] = 1;
           rec(ctx->ev_q_free[sl], ctx->s_d2h);
         }
       }
@@ -917,6 +936,13 @@ int fpdt_attn_fwd(fpdt_ctx* ctx, const void* q, const void* k, const void* v, vo
     Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
                            softmax_scale);
     FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
+    if (!ctx->plan.empty()) {
+      if (ctx->plan_u != c.u) fail(FPDT_ERR_ARG, "sparsity plan has " + std::to_string(ctx->plan_u) + " chunks, the call " + std::to_string(c.u));
+      if (!c.offload) fail(FPDT_ERR_UNSUPPORTED, "block sparsity needs offload = 1 (per chunk-pair schedule)");
+      for (int64_t m = 0; m < c.u; ++m)
+        if (!ctx->plan[(size_t)(m * c.u + m)]) fail(FPDT_ERR_ARG, "sparsity plan drops a diagonal block");
+    }
+    ctx->saved_plan = ctx->plan;
     ctx->fwd_done = false;
     forward(ctx, c, q, k, v, o, lse, static_cast<cudaStream_t>(stream));
     ctx->saved = c;
@@ -939,6 +965,17 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
     if (!(c == ctx->saved)) fail(FPDT_ERR_STATE, "backward arguments differ from the saved forward's");
     FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
     backward(ctx, c, o, dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fpdt_set_sparsity(fpdt_ctx* ctx, const uint8_t* keep, int64_t n_chunks) {
+  return run([&] {
+    if (!ctx || n_chunks < 0 || (n_chunks > 0 && !keep)) fail(FPDT_ERR_ARG, "bad sparsity plan arguments");
+    if (n_chunks == 0)
+      ctx->plan.clear();
+    else
+      ctx->plan.assign(keep, keep + (size_t)(n_chunks * n_chunks));
+    ctx->plan_u = n_chunks;
   });
 }
 

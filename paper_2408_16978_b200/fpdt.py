@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "FPDT_OK", 1: "FPDT_ERR_ARG", 2: "FPDT_ERR_DIVISIBILITY", 3: 
 EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_attn_fwd", "fpdt_attn_bwd",
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair", "fpdt_group_create",
-            "fpdt_group_destroy", "fpdt_ctx_create_local")
+            "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity")
 
 
 class FpdtError(RuntimeError):
@@ -64,6 +64,8 @@ def _declare(lib):
     lib.fpdt_last_error.restype = ctypes.c_char_p
     lib.fpdt_global_token.argtypes = [c_int64, c_int64, c_int, c_int]
     lib.fpdt_global_token.restype = c_int64
+    lib.fpdt_set_sparsity.argtypes = [P, P, c_int64]
+    lib.fpdt_set_sparsity.restype = c_int
     lib.fpdt_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
     lib.fpdt_get_stats.restype = c_int
     lib.fpdt_set_kernel_timing.argtypes = [P, c_int]
@@ -154,6 +156,17 @@ class FPDTContext:
         s = Stats()
         _check(lib().fpdt_get_stats(self.handle, ctypes.byref(s)))
         return s.as_dict()
+
+    def set_sparsity(self, keep=None):
+        """Block-sparsity plan keep [u, u] (numpy bool/uint8; None = dense) for the following forward calls."""
+        if keep is None:
+            _check(lib().fpdt_set_sparsity(self.handle, None, 0))
+            return
+        import numpy as np
+        k = np.ascontiguousarray(np.asarray(keep, dtype=np.uint8))
+        assert k.ndim == 2 and k.shape[0] == k.shape[1]
+        self._plan = k  # keep alive during the call (the library copies it)
+        _check(lib().fpdt_set_sparsity(self.handle, c_void_p(k.ctypes.data), k.shape[0]))
 
     def set_kernel_timing(self, enable: bool):
         _check(lib().fpdt_set_kernel_timing(self.handle, int(enable)))

@@ -16,7 +16,7 @@ from fpdt_testlib import TOL, oracle_full, rel_err
 pytestmark = pytest.mark.gpu
 
 
-def run_group(x: dict, p: int, C: int, dtype: str, offload: int) -> dict:
+def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None) -> dict:
     """Shard the global inputs x by the rank-ordinal contract, run fwd+bwd on p local ranks, unshard."""
     from paper_2408_16978_b200 import fpdt
     S, Hq, d = x["q"].shape
@@ -41,6 +41,8 @@ def run_group(x: dict, p: int, C: int, dtype: str, offload: int) -> dict:
                 dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
             stream.synchronize()
             ctx = fpdt.FPDTContext(p, r, group=group) if p > 1 else fpdt.FPDTContext()
+            if keep is not None:
+                ctx.set_sparsity(keep)
             fpdt.fpdt_attn_fwd(ctx, q, k, v, o, lse, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
             fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
             stream.synchronize()
@@ -121,3 +123,17 @@ def test_gqa_configs_sampled_rows(p, Hq, Hkv):
     dv_sum, dv_abs = got["dv"].sum(0), np.abs(got["dv"]).sum(0)
     do_sum = x["do"].reshape(S, Hkv, G, d).sum(axis=(0, 2))
     assert np.max(np.abs(dv_sum - do_sum) / dv_abs) <= TOL["bf16"]
+
+
+def test_block_sparse_multirank():
+    """Block-sparse plan (§5.6) over global chunk indices at p = 2: equals the block-masked oracle."""
+    from oracle import attention
+    S, Hq, Hkv, d, C = 2048, 4, 2, 80, 256
+    keep = gen.sparsity_plan(S // C, 0.4, seed=2)
+    x = gen.make_inputs("normal", 13, S, Hq, Hkv, d)
+    got = run_group(x, 2, C, "bf16", 1, keep=keep)
+    o, lse = attention.attention_forward(x["q"], x["k"], x["v"], keep=keep, chunk=C)
+    dq, dk, dv = attention.attention_backward(x["q"], x["k"], x["v"], o, lse, x["do"], keep=keep, chunk=C)
+    ref = {"o": o, "lse": lse, "dq": dq, "dk": dk, "dv": dv}
+    errs = {n: rel_err(got[n], ref[n]) for n in ref}
+    assert all(e <= TOL["bf16"] for e in errs.values()), errs

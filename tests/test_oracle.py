@@ -321,3 +321,48 @@ def test_generator_head_subset_matches_full():
         full = gen.generate("k", dist, 4, toks, 8, 16, 100000)
         sub = gen.generate("k", dist, 4, toks, 8, 16, 100000, heads=[1, 6])
         assert np.array_equal(full[:, [1, 6]], sub)
+
+
+def test_sparsity_plan_properties():
+    for u, rho in ((8, 0.0), (8, 0.25), (8, 0.5), (4, 0.9)):
+        keep = gen.sparsity_plan(u, rho, seed=3)
+        assert keep.shape == (u, u) and keep.dtype == bool
+        assert np.all(np.diag(keep)) and not np.any(np.triu(keep, 1))
+        n_valid = u * (u + 1) // 2
+        assert n_valid - keep.sum() == min(int(np.floor(rho * n_valid)), u * (u - 1) // 2)
+        assert np.array_equal(keep, gen.sparsity_plan(u, rho, seed=3))
+
+
+def test_block_sparse_definition_pins():
+    """Block-sparse oracle pins (§5.6): all-kept == dense; diagonal-only == independent per-chunk causal
+    attention; a random plan == torch SDPA (fp64) with the explicit boolean block mask; and the backward of that
+    plan == autograd through the same SDPA."""
+    S, Hq, Hkv, d, C = 96, 4, 2, 16, 24
+    u = S // C
+    x = gen.make_inputs("normal", 5, S, Hq, Hkv, d)
+    dense = attention.attention_forward(x["q"], x["k"], x["v"])
+    allk = attention.attention_forward(x["q"], x["k"], x["v"], keep=np.tril(np.ones((u, u), bool)), chunk=C)
+    np.testing.assert_allclose(allk[0], dense[0], rtol=0, atol=1e-13)
+    diag = attention.attention_forward(x["q"], x["k"], x["v"], keep=np.eye(u, dtype=bool), chunk=C)
+    for m in range(u):
+        sl = slice(m * C, (m + 1) * C)
+        o_m, lse_m = attention.attention_forward(x["q"][sl], x["k"][sl], x["v"][sl])
+        np.testing.assert_allclose(diag[0][sl], o_m, rtol=0, atol=1e-13)
+        np.testing.assert_allclose(diag[1][sl], lse_m, rtol=0, atol=1e-13)
+    keep = gen.sparsity_plan(u, 0.4, seed=1)
+    o, lse = attention.attention_forward(x["q"], x["k"], x["v"], keep=keep, chunk=C)
+    do = x["do"]
+    dq, dk, dv = attention.attention_backward(x["q"], x["k"], x["v"], o, lse, do, keep=keep, chunk=C)
+    t = {n: torch.tensor(x[n], dtype=torch.float64, requires_grad=(n != "do")) for n in ("q", "k", "v", "do")}
+    G = Hq // Hkv
+    visible = (torch.arange(S)[None, :] <= torch.arange(S)[:, None]) & torch.tensor(
+        keep[np.arange(S)[:, None] // C, np.arange(S)[None, :] // C])
+    qh = t["q"].permute(1, 0, 2)
+    kh = t["k"].repeat_interleave(G, dim=1).permute(1, 0, 2)
+    vh = t["v"].repeat_interleave(G, dim=1).permute(1, 0, 2)
+    ref = torch.nn.functional.scaled_dot_product_attention(qh, kh, vh, attn_mask=visible).permute(1, 0, 2)
+    np.testing.assert_allclose(o, ref.detach().numpy(), rtol=0, atol=1e-12)
+    (ref * t["do"]).sum().backward()
+    np.testing.assert_allclose(dq, t["q"].grad.numpy(), rtol=0, atol=1e-11)
+    np.testing.assert_allclose(dk, t["k"].grad.numpy(), rtol=0, atol=1e-11)
+    np.testing.assert_allclose(dv, t["v"].grad.numpy(), rtol=0, atol=1e-11)
