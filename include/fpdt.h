@@ -167,6 +167,11 @@ int fpdt_selftest_umma(int variant, int head_dim, const void* a, const void* b, 
  * Returns 0 or a CUDA error code. */
 int fpdt_selftest_perf(int what, int n, int iters, float* out, void* stream);
 
+/* Diagnostic micro-benchmark of the forward softmax's exponential stage in registers (148 CTAs of `threads`):
+ * what 0 = 128 columns per thread, 1 = 64; one pair in `every` as the FMA-pipe polynomial (0 = all MUFU).
+ * Writes SM cycles per row per thread (CTA 0) to out[0] (device fp32).  Returns 0 or a CUDA error code. */
+int fpdt_selftest_softmax(int what, int threads, int every, int iters, float* out, void* stream);
+
 /* Diagnostic: launch ONE bf16 chunk-pair kernel directly (no scheduler) on caller device buffers, rows
  * [0, n_rows) of q/k/v/dout against each other (the diagonal pair when causal = 1).
  *   which 0 (forward):  out0 = o bf16 [n_rows][n_q_heads][head_dim], out1 = log2-domain lse fp32 [n_q_heads][n_rows]

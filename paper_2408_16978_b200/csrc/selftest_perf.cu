@@ -147,8 +147,67 @@ __global__ void __launch_bounds__(1024, 1) perf_kernel(int what, int n, int iter
   if (warp == 0) tmem_dealloc<512>(tmem);
 }
 
+// The forward softmax's exponential stage on one row of kElems columns per thread, registers only: FFMA2 scale,
+// MUFU ex2 or (every `every`-th pair, 0 = none) the FMA-pipe polynomial, bf16 packing.  Cycles per row of CTA 0.
+template <int kElems, int every>
+__global__ void __launch_bounds__(kElems == 128 ? 256 : 512, 1) softmax_bench_kernel(int iters, float* out) {
+  float x[kElems];
+#pragma unroll
+  for (int c = 0; c < kElems; ++c) x[c] = -0.03f * c - 0.001f * threadIdx.x;
+  uint32_t acc0 = 0, acc1 = 0;
+  const float2 s2 = make_float2(0.161f, 0.161f);
+  const long long t0 = clock64();
+  for (int it = 0; it < iters; ++it) {
+    const float mb = -1.5f - 1e-7f * it;  // per-iteration (as the running max): nothing is loop-invariant
+    const float2 nm = make_float2(mb, mb);
+#pragma unroll
+    for (int i = 0; i < kElems; i += 2) {
+      const float2 e = __ffma2_rn(make_float2(x[i], x[i + 1]), s2, nm);
+      float2 pr;
+      if (every && (i / 2) % every == every - 1) {
+        float2 v = make_float2(fmaxf(e.x, -127.f), fmaxf(e.y, -127.f));
+        const float2 kR = make_float2(12582912.f, 12582912.f);
+        const float2 j = __fadd2_rn(v, kR);
+        const float2 f = __fadd2_rn(v, __fadd2_rn(kR, make_float2(-j.x, -j.y)));
+        float2 p = __ffma2_rn(f, make_float2(0.055f, 0.055f), make_float2(0.2426f, 0.2426f));
+        p = __ffma2_rn(p, f, make_float2(0.6933f, 0.6933f));
+        p = __ffma2_rn(p, f, make_float2(0.99993f, 0.99993f));
+        pr = make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                         __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+      } else {
+        float a0, a1;
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(a0) : "f"(e.x));
+        asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(a1) : "f"(e.y));
+        pr = make_float2(a0, a1);
+      }
+      if ((i / 2) & 1)
+        acc1 ^= pack_bf16x2(pr.x, pr.y);
+      else
+        acc0 ^= pack_bf16x2(pr.x, pr.y);
+    }
+    x[0] += 1e-7f;
+  }
+  const long long t1 = clock64();
+  if (threadIdx.x == 0 && blockIdx.x == 0) out[0] = (float)(t1 - t0) / iters;
+  if ((acc0 ^ acc1) == 12345u) out[1] = x[1];
+}
+
 }  // namespace
 }  // namespace fpdt
+
+// Diagnostic: fwd-softmax exponential stage throughput (what = 0: 128 columns per thread, 1: 64), `threads` per
+// CTA, one pair in `every` on the FMA-pipe polynomial (0 = all MUFU).  out[0] = SM cycles per row per thread.
+extern "C" int fpdt_selftest_softmax(int what, int threads, int every, int iters, float* out, void* stream) {
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+#define FPDT_SMB(E, V) fpdt::softmax_bench_kernel<E, V><<<148, threads, 0, s>>>(iters, out)
+  if (what == 0) {
+    if (every == 0) FPDT_SMB(128, 0); else if (every == 2) FPDT_SMB(128, 2); else if (every == 4) FPDT_SMB(128, 4); else FPDT_SMB(128, 8);
+  } else {
+    if (every == 0) FPDT_SMB(64, 0); else if (every == 2) FPDT_SMB(64, 2); else if (every == 4) FPDT_SMB(64, 4); else FPDT_SMB(64, 8);
+  }
+#undef FPDT_SMB
+  return (int)cudaGetLastError();
+}
 
 extern "C" int fpdt_selftest_perf(int what, int n, int iters, float* out, void* stream) {
   const int smem = 65536 + 1024;

@@ -22,7 +22,8 @@ STATUS_NAMES = {0: "FPDT_OK", 1: "FPDT_ERR_ARG", 2: "FPDT_ERR_DIVISIBILITY", 3: 
 EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_attn_fwd", "fpdt_attn_bwd",
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair", "fpdt_group_create",
-            "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity")
+            "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity",
+            "fpdt_selftest_softmax")
 
 
 class FpdtError(RuntimeError):
@@ -75,6 +76,8 @@ def _declare(lib):
     lib.fpdt_kernel_time.restype = c_int
     lib.fpdt_selftest_umma.argtypes = [c_int, c_int, P, P, c_int, c_int, P, P]
     lib.fpdt_selftest_umma.restype = c_int
+    lib.fpdt_selftest_softmax.argtypes = [c_int, c_int, c_int, c_int, P, P]
+    lib.fpdt_selftest_softmax.restype = c_int
     lib.fpdt_selftest_perf.argtypes = [c_int, c_int, c_int, P, P]
     lib.fpdt_selftest_perf.restype = c_int
     lib.fpdt_debug_pair.argtypes = [c_int, c_int, c_int, P, P, P, P, P, P, P, P, P, c_int64, c_int, c_int, P, c_int, P]
