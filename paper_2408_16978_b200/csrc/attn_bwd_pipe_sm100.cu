@@ -46,8 +46,7 @@ static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs -
 #ifndef FPDT_BWD_EXP
 #define FPDT_BWD_EXP 0  // timing experiments only (wrong results): 1 no dQ reduce, 2 no dQ staging/reduce,
                        // 3 no stats loads, 4 = 2 + 3, 5 no wait for the previous dQ reduce's smem read,
-                       // 6 dQ reduce every other tile only, 7 only the 16-column dQ box, 8 only even key tiles reduce,
-                       // 9 linear staging + one 1-D bulk reduce (correct, bank-conflicted), 10 trailing 16 columns by REDG
+                       // 6 dQ reduce every other tile only, 8 only even key tiles reduce
 #endif
 #ifndef FPDT_BWD_POLY_EVERY
 #define FPDT_BWD_POLY_EVERY 4  // one exponential pair in FPDT_BWD_POLY_EVERY goes to the FMA-pipe polynomial
@@ -107,13 +106,6 @@ __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* m, uint32_t
 __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_t bytes, uint32_t bar) {
   asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
                "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
-               : "memory");
-}
-// 1-D bulk reduce-add of `bytes` contiguous fp32 from shared to global memory (bulk async-group completion)
-__device__ __forceinline__ void bulk_reduce_add_f32(void* gdst, uint32_t ssrc, uint32_t bytes) {
-  asm volatile("cp.reduce.async.bulk.global.shared::cta.bulk_group.add.f32 [%0], [%1], %2;" ::"l"(
-                   reinterpret_cast<uint64_t>(gdst)),
-               "r"(ssrc), "r"(bytes)
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
@@ -457,7 +449,6 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
     setmaxnreg_dec<kRegsDQ>();
     // ------------------------------------------------------------------ dQ read-out (query rows)
     const int r = (warp - 8) * 32 + lane;
-    const int t128 = threadIdx.x - 256;
     uint32_t tdQ = tmem + C::tdQ + (((warp & 3) * 32) << 16);
     asm volatile("" : "+r"(tdQ));
     // cluster pair: rank 0 holds the even key tile, rank 1 the next one; on the causal diagonal the even tile sees
@@ -557,51 +548,40 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
         }
         continue;
       }
-      // the previous bulk reduce must have finished reading the staging tile
-      if (FPDT_BWD_EXP != 5 && t128 == 0) bulk_wait_read0();
-      named_bar(1, 128);
-      // staging = D/32 column chunks [128 rows][32 fp32] (128B-swizzled) + a [128][16] chunk (64B-swizzled) when
-      // D % 32 == 16: the 16-byte piece j of row r lives at piece j ^ (r & 7) (resp. j ^ ((r >> 1) & 3)), so the
-      // 32 rows of a warp hit all 32 banks (an unswizzled 320-byte row pitch would be a 16-way bank conflict)
+      // Two independent 64-row halves (warps 8-9: query rows 0-63, warps 10-11: rows 64-127), each with its own half
+      // of the staging, named barrier and issuing thread: while one half waits for its previous reduce-add to finish
+      // reading its staging, the TMA engine works on the other half's.  Staging per half: D/32 column chunks
+      // [64 rows][32 fp32] (128B-swizzled) + a [64][16] chunk (64B-swizzled) when D % 32 == 16 — the 16-byte piece j
+      // of row rr lives at piece j ^ (rr & 7) (resp. j ^ ((rr >> 1) & 3)), so the 32 rows of a warp hit all 32 banks.
+      const int hrow = r >> 6, rr = r & 63;
+      const bool hlead = rr == 0;
+      constexpr uint32_t HB = 64 * D * 4;
+      if (FPDT_BWD_EXP != 5 && hlead) bulk_wait_read0();
+      named_bar(2 + hrow, 64);
       const float2 sc = make_float2(a.scale, a.scale);
-      uint8_t* stg = smem + C::oDQ;
-      constexpr int kRedCols = (FPDT_BWD_EXP == 10 && D % 32) ? 16 : 0;  // trailing columns reduced with REDG
-      if (kRedCols) {
-        float4* dst = reinterpret_cast<float4*>(a.dq_acc + (int64_t)h * a.dq_head_stride + ((int64_t)qt * 128 + r) * D);
+      uint8_t* stg = smem + C::oDQ + hrow * HB;
 #pragma unroll
-        for (int c = D - kRedCols; c < D; c += 4)
-          atomicAdd(dst + c / 4, make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale, v[c + 3] * a.scale));
-      }
-#pragma unroll
-      for (int c = 0; c < D - kRedCols; c += 4) {
+      for (int c = 0; c < D; c += 4) {
         const float2 x0 = __fmul2_rn(make_float2(v[c], v[c + 1]), sc);
         const float2 x1 = __fmul2_rn(make_float2(v[c + 2], v[c + 3]), sc);
         const int j = (c & 31) >> 2;
-        uint32_t off;
-        if (FPDT_BWD_EXP == 9)
-          off = (r * D + c) * 4;  // linear [128][D] (bank-conflicted; timing experiment for the 1-D bulk reduce)
-        else if (c < (D / 32) * 32)
-          off = (c >> 5) * 16384 + r * 128 + ((j ^ (r & 7)) << 4);
-        else
-          off = (D / 32) * 16384 + r * 64 + ((j ^ ((r >> 1) & 3)) << 4);
+        const uint32_t off = c < (D / 32) * 32 ? (c >> 5) * 8192 + rr * 128 + ((j ^ (rr & 7)) << 4)
+                                               : (D / 32) * 8192 + rr * 64 + ((j ^ ((rr >> 1) & 3)) << 4);
         *reinterpret_cast<float4*>(stg + off) = make_float4(x0.x, x0.y, x1.x, x1.y);
       }
       fence_async_shared();
-      named_bar(1, 128);
-      if (FPDT_BWD_EXP == 9 && t128 == 0) {
-        bulk_reduce_add_f32(a.dq_acc + (int64_t)h * a.dq_head_stride + (int64_t)qt * 128 * D, sDQ, 128 * D * 4);
-        bulk_commit();
-      } else if (FPDT_BWD_EXP != 1 && !(FPDT_BWD_EXP == 6 && (n & 1)) && !(FPDT_BWD_EXP == 8 && (kt & 1)) &&
-                 t128 == 0) {
+      named_bar(2 + hrow, 64);
+      if (FPDT_BWD_EXP != 1 && !(FPDT_BWD_EXP == 6 && (n & 1)) && !(FPDT_BWD_EXP == 8 && (kt & 1)) && hlead) {
+        const uint32_t sb = sDQ + hrow * HB;
+        const int row0 = qt * 128 + 64 * hrow;
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc)
-          if (FPDT_BWD_EXP != 7) tma_reduce_add_3d(&tm.dq32, sDQ + cc * 16384, cc * 32, qt * 128, h);
-        if (D % 32 && kRedCols == 0) tma_reduce_add_3d(&tm.dq16, sDQ + (D / 32) * 16384, (D / 32) * 32, qt * 128, h);
+        for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_3d(&tm.dq32h, sb + cc * 8192, cc * 32, row0, h);
+        if (D % 32) tma_reduce_add_3d(&tm.dq16h, sb + (D / 32) * 8192, (D / 32) * 32, row0, h);
         bulk_commit();
-        TRACE(11, n);
+        if (hrow == 0) TRACE(11, n);
       }
     }
-    if (t128 == 0 || (kPair && (r & 63) == 0)) bulk_wait0();
+    if ((r & 63) == 0) bulk_wait0();
   }
   tc_fence_before();
   if constexpr (kPair)

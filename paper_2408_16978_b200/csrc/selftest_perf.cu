@@ -164,7 +164,7 @@ __global__ void __launch_bounds__(kElems == 128 ? 256 : 512, 1) softmax_bench_ke
     for (int i = 0; i < kElems; i += 2) {
       const float2 e = __ffma2_rn(make_float2(x[i], x[i + 1]), s2, nm);
       float2 pr;
-      if (every && (i / 2) % every == every - 1) {
+      if (every && (i / 2) % (every ? every : 1) == every - 1) {
         float2 v = make_float2(fmaxf(e.x, -127.f), fmaxf(e.y, -127.f));
         const float2 kR = make_float2(12582912.f, 12582912.f);
         const float2 j = __fadd2_rn(v, kR);
