@@ -172,6 +172,13 @@ int fpdt_selftest_perf(int what, int n, int iters, float* out, void* stream);
  * Writes SM cycles per row per thread (CTA 0) to out[0] (device fp32).  Returns 0 or a CUDA error code. */
 int fpdt_selftest_softmax(int what, int threads, int every, int iters, float* out, void* stream);
 
+/* Diagnostic micro-benchmark of the dQ reduce-add path: 148 CTAs each reduce a 40 KB fp32 staging tile into global
+ * memory `iters` times (mode 0: three swizzled tensor boxes as in the backward kernel, 1: one 1-D bulk reduce,
+ * 2: ten 4 KB bulk reduces, 3: one unswizzled [128 x 80] box, 4: plain bulk store), `inflight` groups in flight
+ * (1 or 2), into one region per CTA or (shared_target) the same region.  gbuf: device fp32, >= 148*10240 floats.
+ * out[0] = SM cycles per tile (device fp32).  Returns 0 or an error code. */
+int fpdt_selftest_reduce(int mode, int iters, int inflight, int shared_target, float* gbuf, float* out, void* stream);
+
 /* Diagnostic: launch ONE bf16 chunk-pair kernel directly (no scheduler) on caller device buffers, rows
  * [0, n_rows) of q/k/v/dout against each other (the diagonal pair when causal = 1).
  *   which 0 (forward):  out0 = o bf16 [n_rows][n_q_heads][head_dim], out1 = log2-domain lse fp32 [n_q_heads][n_rows]

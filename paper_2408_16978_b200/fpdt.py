@@ -23,7 +23,7 @@ EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_a
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair", "fpdt_group_create",
             "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity",
-            "fpdt_selftest_softmax")
+            "fpdt_selftest_softmax", "fpdt_selftest_reduce")
 
 
 class FpdtError(RuntimeError):
@@ -76,6 +76,8 @@ def _declare(lib):
     lib.fpdt_kernel_time.restype = c_int
     lib.fpdt_selftest_umma.argtypes = [c_int, c_int, P, P, c_int, c_int, P, P]
     lib.fpdt_selftest_umma.restype = c_int
+    lib.fpdt_selftest_reduce.argtypes = [c_int, c_int, c_int, c_int, P, P, P]
+    lib.fpdt_selftest_reduce.restype = c_int
     lib.fpdt_selftest_softmax.argtypes = [c_int, c_int, c_int, c_int, P, P]
     lib.fpdt_selftest_softmax.restype = c_int
     lib.fpdt_selftest_perf.argtypes = [c_int, c_int, c_int, P, P]
