@@ -175,7 +175,8 @@ int fpdt_selftest_softmax(int what, int threads, int every, int iters, float* ou
 /* Diagnostic micro-benchmark of the dQ reduce-add path: 148 CTAs each reduce a 40 KB fp32 staging tile into global
  * memory `iters` times (mode 0: three swizzled tensor boxes as in the backward kernel, 1: one 1-D bulk reduce,
  * 2: ten 4 KB bulk reduces, 3: one unswizzled [128 x 80] box, 4: plain bulk store), `inflight` groups in flight
- * (1 or 2), into one region per CTA or (shared_target) the same region.  gbuf: device fp32, >= 148*10240 floats.
+ * (1 or 2), into one region per CTA or (shared_target) the same region; 5: mode 0 plus a 40 KB bulk load per tile,
+ * 6: the load alone.  gbuf: device fp32, >= 2*148*10240 floats.
  * out[0] = SM cycles per tile (device fp32).  Returns 0 or an error code. */
 int fpdt_selftest_reduce(int mode, int iters, int inflight, int shared_target, float* gbuf, float* out, void* stream);
 

@@ -7,10 +7,11 @@ import torch
 from paper_2408_16978_b200 import _lib
 
 lib = _lib.load()
-g = torch.zeros(148 * 10240 + 1024, device="cuda")
+g = torch.zeros(2 * 148 * 10240 + 1024, device="cuda")
 out = torch.zeros(4, device="cuda")
-names = {0: "3 swizzled boxes", 1: "1-D bulk 40KB", 2: "10 x 4KB bulk", 3: "1 box [128x80]", 4: "bulk STORE 40KB"}
-for mode in (0, 1, 2, 3, 4):
+names = {0: "3 swizzled boxes", 1: "1-D bulk 40KB", 2: "10 x 4KB bulk", 3: "1 box [128x80]", 4: "bulk STORE 40KB",
+         5: "boxes + 40KB load", 6: "40KB load only"}
+for mode in (0, 5, 6, 1, 4):
     for inflight in (1, 2):
         for shared in (0, 1):
             for iters in (8, 128):
