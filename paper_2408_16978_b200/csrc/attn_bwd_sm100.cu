@@ -484,7 +484,10 @@ int launch_attn_bwd_bf16(const BwdArgs& a, int head_dim, cudaStream_t s) {
     const char* e = getenv("FPDT_BWD_KERNEL");
     return e && strcmp(e, "v2") == 0;
   }();
-  if (head_dim != 128 && !use_v2) return launch_attn_bwd_pipe_bf16(a, head_dim, s);
+  if (!use_v2) {
+    if (head_dim == 128) return launch_attn_bwd_q64_bf16(a, head_dim, s);
+    return launch_attn_bwd_pipe_bf16(a, head_dim, s);
+  }
   switch (head_dim) {
     case 64: return launch_bwd<64>(a, s);
     case 80: return launch_bwd<80>(a, s);

@@ -78,6 +78,7 @@ struct BwdArgs {
 int launch_attn_fwd_bf16(const FwdArgs& a, int head_dim, cudaStream_t s);
 int launch_attn_bwd_bf16(const BwdArgs& a, int head_dim, cudaStream_t s);
 int launch_attn_bwd_pipe_bf16(const BwdArgs& a, int head_dim, cudaStream_t s);
+int launch_attn_bwd_q64_bf16(const BwdArgs& a, int head_dim, cudaStream_t s);  // head_dim 128
 int launch_attn_fwd_f32(const FwdArgs& a, int head_dim, cudaStream_t s);
 int launch_attn_bwd_f32(const BwdArgs& a, int head_dim, cudaStream_t s);
 
