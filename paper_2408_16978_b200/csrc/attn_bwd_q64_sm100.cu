@@ -1,4 +1,4 @@
-// Backward chunk-pair attention for sm_100a, head_dim 128: 64-row query tiles and a transposed dQ product.
+// Backward chunk-pair attention for sm_100a: 64-row query tiles and a transposed dQ product (head_dim 64/80/128).
 //
 // Same operation as attn_bwd_pipe_sm100.cu: one (key/value chunk j, query chunk i) step of FPDT's nested backward
 // loop (fig:bw_db). The CTA is KV-stationary: one 128-row key/value tile of one KV head, walking the
@@ -8,18 +8,17 @@
 //   dV  += P^T dO            dK  += dS^T Q
 //   dQ^T = K^T dS^T          (the partial dQ of the tile, TMA bulk reduce-added into the fp32 dq accumulator)
 //
-// Why a separate kernel for d = 128. With 128-row query tiles, Sᵀ, dPᵀ, dK and dV fill all 512 TMEM columns, and
-// K, V, the Q/dO stages and dS fill shared memory. There is then no room to stage the 64 KB dQ partial for a TMA
-// reduce-add, so attn_bwd_sm100.cu reduces it with vector atomics (≈ 630 TFLOP/s).
-// With 64-row query tiles:
-//   * every product keeps M = 128; dQ is computed transposed (M = head_dim = 128, N = 64 query rows) with
+// Why 64-row query tiles. With 128-row tiles at d = 128, Sᵀ, dPᵀ, dK and dV fill all 512 TMEM columns, and K, V,
+// the Q/dO stages and dS fill shared memory. There is no room to stage the 64 KB dQ partial for a TMA reduce-add,
+// so attn_bwd_sm100.cu reduces it with vector atomics (≈ 630 TFLOP/s). With 64-row query tiles:
+//   * every product keeps M = 128. dQ is computed transposed (M = 128 over head_dim, N = 64 query rows), with
 //     A = Kᵀ read MN-major from the resident K tile and B = dS read MN-major from the tile the softmax warps
-//     write;
-//   * TMEM: Sᵀ 64 | dPᵀ 64 | dQᵀ 2 × 64 (double-buffered) | dK 128 | dV 128 = 512 columns;
-//   * shared memory: K, V 64 KB | 3 Q + 2 dO stages 80 KB | dS 16 KB | dQ staging 2 × 32 KB | stats (226 KB).
-// The dQ read-out thread owns one head_dim column (a TMEM lane) and 64 query rows. It stages [64 rows][64 cols]
-// fp32 halves without swizzle (a warp writes 128 contiguous bytes per row), and each half leaves as one TMA
-// reduce-add box.
+//     write. For d < 128 the M = 128 read runs past the K tile into V; those rows of dQᵀ are never read out;
+//   * TMEM: Sᵀ 64 | dPᵀ 64 | Pᵀ, dSᵀ (bf16) 64 | dQᵀ 64 | dK d | dV d (512 columns at d = 128);
+//   * shared memory (d = 128): K, V 64 KB | 3 Q + 2 dO stages 80 KB | dS 16 KB | dQ staging 2 × 32 KB | stats.
+// The dQ read-out thread owns one head_dim column (a TMEM lane) and 64 query rows. It stages column groups of
+// [64 rows][64 cols] fp32 (and a 16-column group at d = 80) without swizzle: a warp writes 128 contiguous bytes
+// per row. Each group leaves as one TMA reduce-add box.
 // Warp roles and the issue order are those of attn_bwd_pipe_sm100.cu.
 #include "attn_tile.cuh"
 #include "kernels.h"
@@ -39,46 +38,61 @@ static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs -
 #define FPDT_BWD_POLY_EVERY 4
 #endif
 
-constexpr int D = 128, BQ = 64;
+constexpr int BQ = 64;
 
-// [R rows x 128 cols] bf16 operand tile: two 128B-swizzled atoms of [R rows x 64 cols] (TMA box = one atom)
-template <int R>
-struct T128 {
-  static constexpr int kAtom = R * 128;
-  static constexpr int kBytes = 2 * kAtom;
-  // K-major (rows = M or N, contraction over the 128 columns), step kk = 16 columns
+// [R rows x D cols] bf16 operand tile in the attn_tile.cuh format: D = 64, 128 -> 128B-swizzled atoms of
+// [R rows x 64 cols]; D = 80 -> 32B-swizzled atoms of [R rows x 16 cols] (TMA box = one atom)
+template <int D, int R>
+struct TileR {
+  static constexpr bool kNarrow = (D == 80);
+  static constexpr int kAC = kNarrow ? 16 : 64;    // columns per atom
+  static constexpr int kAtom = R * kAC * 2;        // bytes per atom
+  static constexpr int kBytes = R * D * 2;
+  static constexpr uint32_t kSBO = 8 * kAC * 2;    // 8-row group stride
+  static constexpr uint32_t kSw = kNarrow ? ptx::kSw32 : ptx::kSw128;
+  // K-major (rows = M or N, contraction over the D columns), step kk = 16 columns
   static __device__ __forceinline__ uint64_t kmajor(uint32_t t, int kk) {
-    return smem_desc(t + (kk >> 2) * kAtom + (kk & 3) * 32, 16, 1024, kSw128);
+    const int col = kk * 16;
+    return smem_desc(t + (col / kAC) * kAtom + (col % kAC) * 2, 16, kSBO, kSw);
   }
-  // MN-major (contraction over the R rows, M or N = the 128 columns in two atoms kAtom apart), step kk = 16 rows
-  static __device__ __forceinline__ uint64_t mn(uint32_t t, int kk) { return smem_desc(t + kk * 2048, kAtom, 1024, kSw128); }
+  // MN-major (contraction over the R rows; M or N runs along the columns, atoms kAtom apart), step kk = 16 rows
+  static __device__ __forceinline__ uint64_t mn(uint32_t t, int kk) {
+    return smem_desc(t + kk * 16 * kAC * 2, kAtom, kSBO, kSw);
+  }
   static __device__ __forceinline__ void load(uint32_t t, const CUtensorMap* m, uint32_t bar, int head, int row0,
                                               uint64_t pol) {
-    tma_load_3d(t, m, bar, 0, head, row0, pol);
-    tma_load_3d(t + kAtom, m, bar, 64, head, row0, pol);
+#pragma unroll
+    for (int a = 0; a < D / kAC; ++a) tma_load_3d(t + a * kAtom, m, bar, a * kAC, head, row0, pol);
   }
 };
-using TK = T128<128>;
-using TQ = T128<BQ>;
 
+template <int D>
 struct Cfg {
+  using TK = TileR<D, 128>;
+  using TQ = TileR<D, BQ>;
   static constexpr int QS = 3, OS = 2;
-  static constexpr int kDS = 128 * BQ * 2;    // dS, [128 keys][64 queries] bf16, MN-major (queries contiguous)
-  static constexpr int kDQH = BQ * 64 * 4;    // one staging half: [64 query rows][64 cols] fp32
-  static constexpr int kStats = 2 * BQ * 4;   // lse2[64] + D[64]
+  static constexpr int kDQW = (D + 31) / 32;       // dQ read-out warps (thread = one head_dim column)
+  static constexpr int kDS = 128 * BQ * 2;         // dS, [128 keys][64 queries] bf16, MN-major (queries contiguous)
+  static constexpr int kDQB = BQ * D * 4;          // one dQ staging buffer: column groups [64 rows][<=64 cols] fp32
+  static constexpr int kStats = 2 * BQ * 4;        // lse2[64] + D[64]
   static constexpr int oK = 0, oV = TK::kBytes, oQ = 2 * TK::kBytes, oO = oQ + QS * TQ::kBytes;
   static constexpr int oDS = oO + OS * TQ::kBytes;
   static constexpr int oDQ = oDS + kDS;
-  static constexpr int oStats = oDQ + 4 * kDQH;
+  static constexpr int oStats = oDQ + 2 * kDQB;
   static constexpr int oBars = oStats + QS * kStats;
   static constexpr int kSmem = oBars + 256;
   static_assert(oDS % 1024 == 0, "swizzle atoms are 1 KB aligned");
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
-  static constexpr uint32_t tS = 0, tdP = 64, tdQ = 128, tdK = 256, tdV = 384;
+  // dQ^T = K^T dS^T runs with M = 128 over the K tile read MN-major: for D < 128 its rows >= D read the bytes that
+  // follow the K tile in shared memory (V) and are never read out
+  static_assert(oK + 128 * 128 * 2 <= oDS, "M = 128 read of K^T stays inside the K/V/Q area");
+  // P^T / dS^T (bf16) get their own columns so that dP^T_{n+1} can be issued as soon as dP^T_n is in registers
+  static constexpr uint32_t tS = 0, tdP = 64, tPS = 128, tdQ = 192, tdK = 256, tdV = 256 + D;
+  static_assert(256 + 2 * D <= 512, "TMEM budget");
 };
 
 struct TmapSet {
-  CUtensorMap q, k, v, o, dq;
+  CUtensorMap q, k, v, o, dq64, dq16;  // dq boxes: [64 rows][64 cols] and [64 rows][16 cols] fp32, no swizzle
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -119,9 +133,12 @@ __device__ __forceinline__ void sts32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 
+template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdArgs a) {
-  using C = Cfg;
+  using C = Cfg<D>;
+  using TK = typename C::TK;
+  using TQ = typename C::TQ;
   constexpr int QS = C::QS, OS = C::OS;
   extern __shared__ __align__(1024) uint8_t smem[];
   const uint32_t base = smem_u32(smem);
@@ -129,8 +146,9 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem + C::oBars);
   auto bar = [&](int i) { return smem_u32(&bars[i]); };
   constexpr int B_KV = 0, B_QF = 1, B_QE = B_QF + QS, B_OF = B_QE + QS, B_OE = B_OF + OS, B_S = B_OE + OS,
-                B_SFREE = B_S + 1, B_DP = B_SFREE + 1, B_P = B_DP + 1, B_DS = B_P + 1, B_DSFREE = B_DS + 1,
-                B_DQF = B_DSFREE + 1, B_DQE = B_DQF + 2, B_KVDONE = B_DQE + 2, B_NUM = B_KVDONE + 1;
+                B_SFREE = B_S + 1, B_DP = B_SFREE + 1, B_DPFREE = B_DP + 1, B_P = B_DPFREE + 1,
+                B_PFREE = B_P + 1, B_DS = B_PFREE + 1, B_DSFREE = B_DS + 1, B_DQF = B_DSFREE + 1,
+                B_DQE = B_DQF + 1, B_KVDONE = B_DQE + 1, B_NUM = B_KVDONE + 1;
   static_assert(B_NUM <= 30, "barrier area");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::oBars + 30 * 8);
 
@@ -147,6 +165,11 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
     if (qt_first > n_qt_total) qt_first = n_qt_total;
   }
   const int n_iter = (n_qt_total - qt_first) * G;
+  const bool tracing = a.trace != nullptr && blockIdx.x == a.trace_cta && blockIdx.y == 0;
+#define TRACE(ev, n)                                                        \
+  do {                                                                      \
+    if (tracing && (n) < 4096) a.trace[(ev) * 4096 + (n)] = clock64();      \
+  } while (0)
 
   if (warp == 13) tmem_alloc<512>(smem_u32(tmem_slot));
   if (warp == 12 && lane == 0) {
@@ -162,13 +185,13 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
     mbar_init(bar(B_S), 1);
     mbar_init(bar(B_SFREE), 256);
     mbar_init(bar(B_DP), 1);
+    mbar_init(bar(B_DPFREE), 256);
     mbar_init(bar(B_P), 256);
+    mbar_init(bar(B_PFREE), 1);
     mbar_init(bar(B_DS), 256);
     mbar_init(bar(B_DSFREE), 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(bar(B_DQF + b), 1);
-      mbar_init(bar(B_DQE + b), 128);
-    }
+    mbar_init(bar(B_DQF), 1);
+    mbar_init(bar(B_DQE), 32 * C::kDQW);
     mbar_init(bar(B_KVDONE), 1);
     fence_mbar_init();
   }
@@ -192,6 +215,7 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
           const int qt = qt_first + n / G, h = g * G + n % G;
           const int qrow = (int)(a.q_row0 + (int64_t)qt * BQ);
           if (n >= QS) mbar_wait(bar(B_QE + qs), ((n / QS) - 1) & 1);
+          TRACE(12, n);
           const uint32_t fq = bar(B_QF + qs);
           const uint32_t stats = base + C::oStats + qs * C::kStats;
           mbar_expect_tx(fq, TQ::kBytes + C::kStats);
@@ -229,37 +253,46 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
         mbar_wait(bar(B_KV), 0);
         issue_S(0);
         issue_dP(0);
-        // per query tile n: S^T_{n+1} after SFREE(n); dV_n after P(n); dK_n after DS(n); dP^T_{n+1} (overwrites
-        // P^T_n / dS^T_n, after dV_n and dK_n in issue order); dQ^T_n into buffer n&1 once dQ^T_{n-2} is read out
+        // per query tile n: S^T_{n+1} after SFREE(n); dV_n after P(n); dP^T_{n+1} after DPFREE(n) (dP^T_n read out);
+        // dK_n and dQ^T_n after DS(n), dQ^T_n once dQ^T_{n-1} has been read out.  PFREE / DSFREE tell the softmax warps
+        // that P^T_n / dS^T_n (TMEM) and dS_n (smem) have been consumed.
+        const uint32_t tPS = tmem + C::tPS, tdQ = tmem + C::tdQ;
         for (int n = 0; n < n_iter; ++n) {
           const bool more = n + 1 < n_iter;
           if (more) {
             mbar_wait(bar(B_SFREE), n & 1);
+            TRACE(6, n);
             issue_S(n + 1);
           }
           mbar_wait(bar(B_P), n & 1);
+          TRACE(4, n);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)
-            mma_ts(tdV, tdP + 32 * (kk >> 1) + (kk & 1) * 8, TQ::mn(sO(n), kk), idG, (n > 0 || kk > 0));
+            mma_ts(tdV, tPS + 8 * kk, TQ::mn(sO(n), kk), idG, (n > 0 || kk > 0));
           mma_commit(bar(B_OE + n % OS));
+          mma_commit(bar(B_PFREE));
+          if (more) {
+            mbar_wait(bar(B_DPFREE), n & 1);
+            TRACE(8, n);
+            issue_dP(n + 1);
+          }
           mbar_wait(bar(B_DS), n & 1);
+          TRACE(5, n);
           tc_fence_after();
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)
-            mma_ts(tdK, tdP + 32 * (kk >> 1) + 16 + (kk & 1) * 8, TQ::mn(sQ(n), kk), idG, (n > 0 || kk > 0));
+            mma_ts(tdK, tPS + 32 + 8 * kk, TQ::mn(sQ(n), kk), idG, (n > 0 || kk > 0));
           mma_commit(bar(B_QE + n % QS));
-          if (more) issue_dP(n + 1);
-          const int buf = n & 1;
-          if (n >= 2) {
-            mbar_wait(bar(B_DQE + buf), ((n >> 1) - 1) & 1);
+          if (n > 0) {
+            mbar_wait(bar(B_DQE), (n - 1) & 1);
             tc_fence_after();
           }
+          TRACE(7, n);
 #pragma unroll
           for (int kk = 0; kk < 128 / 16; ++kk)
-            mma_ss(tmem + C::tdQ + 64 * buf, TK::mn(sK, kk), smem_desc(sDS + kk * 2048, 8192, 1024, kSw128), idQ,
-                   kk > 0);
-          mma_commit(bar(B_DQF + buf));
+            mma_ss(tdQ, TK::mn(sK, kk), smem_desc(sDS + kk * 2048, 8192, 1024, kSw128), idQ, kk > 0);
+          mma_commit(bar(B_DQF));
           mma_commit(bar(B_DSFREE));
         }
         mma_commit(bar(B_KVDONE));
@@ -272,7 +305,8 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
     const int r = (warp & 3) * 32 + lane;
     uint32_t tS = tmem + C::tS + (((warp & 3) * 32) << 16) + 32 * half;
     uint32_t tdP = tS + (C::tdP - C::tS);
-    asm volatile("" : "+r"(tS), "+r"(tdP));
+    uint32_t tPw = tmem + C::tPS + (((warp & 3) * 32) << 16) + 16 * half;  // P^T at tPw, dS^T at tPw + 32
+    asm volatile("" : "+r"(tS), "+r"(tdP), "+r"(tPw));
     // key row r of the dS tile: 128 bytes (64 queries) in a 1 KB 8-row group; 16-byte chunk c at chunk c ^ (r & 7)
     const uint32_t sDSr = sDS + (uint32_t)(r >> 3) * 1024 + (uint32_t)(r & 7) * 128;
     const uint32_t xr = (uint32_t)(r & 7);
@@ -282,12 +316,14 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
       const int qt = qt_first + n / G;
       const float* st = reinterpret_cast<const float*>(smem + C::oStats + (n % QS) * C::kStats) + 32 * half;
       mbar_wait(bar(B_S), n & 1);
+      if (warp == 0 && lane == 0) TRACE(0, n);
       tc_fence_after();
       float p[32];
       tmem_ld32(tS, reinterpret_cast<uint32_t*>(p));
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(bar(B_SFREE));
+      if (warp == 0 && lane == 0) TRACE(13, n);
       // query column (within this half) < lim is masked: its query position is before the key position
       const int64_t lim64 = (a.causal ? (kpos - (a.q_pos0 + (int64_t)qt * BQ)) : -1) - 32 * half;
       const int lim = (int)(lim64 < 0 ? 0 : (lim64 > 32 ? 32 : lim64));
@@ -322,21 +358,31 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
           }
         }
       }
-      // dP^T_n -> registers; this half's 32 dP^T columns then receive P^T_n [0,16) and dS^T_n [16,32) (bf16)
+      // dP^T_n -> registers (then dP^T_{n+1} may be issued); P^T_n and dS^T_n (bf16) go to their own columns
+      if (warp == 0 && lane == 0) TRACE(14, n);
       mbar_wait(bar(B_DP), n & 1);
+      if (warp == 0 && lane == 0) TRACE(2, n);
       tc_fence_after();
       float dp[32];
       tmem_ld32(tdP, reinterpret_cast<uint32_t*>(dp));
       tmem_wait_ld();
+      if (warp == 0 && lane == 0) TRACE(15, n);
+      tc_fence_before();
+      mbar_arrive(bar(B_DPFREE));
       {
         uint32_t pk[16];
 #pragma unroll
         for (int i = 0; i < 32; i += 2) pk[i / 2] = pack_bf16x2(p[i], p[i + 1]);
-        tmem_st16(tdP, pk);
+        if (n > 0) {
+          mbar_wait(bar(B_PFREE), (n - 1) & 1);  // dV_{n-1} has read P^T_{n-1}
+          tc_fence_after();
+        }
+        tmem_st16(tPw, pk);
       }
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(bar(B_P));
+      if (warp == 0 && lane == 0) TRACE(1, n);
       uint32_t pk[16];
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
@@ -348,8 +394,12 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
         pk[i / 2] = pack_bf16x2(a0.x, a0.y);
         pk[i / 2 + 1] = pack_bf16x2(a1.x, a1.y);
       }
-      tmem_st16(tdP + 16, pk);
-      if (n > 0) mbar_wait(bar(B_DSFREE), (n - 1) & 1);
+      if (n > 0) {
+        mbar_wait(bar(B_DSFREE), (n - 1) & 1);  // dK_{n-1} and dQ^T_{n-1} have read dS^T_{n-1} / dS_{n-1}
+        tc_fence_after();
+      }
+      if (warp == 0 && lane == 0) TRACE(10, n);
+      tmem_st16(tPw + 32, pk);
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
         const uint32_t w[4] = {pk[m * 4], pk[m * 4 + 1], pk[m * 4 + 2], pk[m * 4 + 3]};
@@ -359,6 +409,7 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
       fence_async_shared();
       tc_fence_before();
       mbar_arrive(bar(B_DS));
+      if (warp == 0 && lane == 0) TRACE(3, n);
     }
     // ---- final dK (half 0) / dV (half 1), thread = key row
     const int64_t row = (int64_t)kt * 128 + r;
@@ -408,61 +459,87 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
   } else {
     setmaxnreg_dec<kRegsDQ>();
     // ------------------------------------------------------------------ dQ read-out: thread = one head_dim column
+    // Column group cg = columns [64 cg, 64 cg + 64) (D = 80: the second group is 16 wide) has its own staging, named
+    // barrier and issuing thread, so one group stages while the TMA engine reads the other's.
     const int e = (warp & 3) * 32 + lane;  // TMEM lane of dQ^T = head_dim index
-    const int chalf = e >> 6, el = e & 63;  // staging half (columns [64*chalf, +64)) and column within it
-    const bool lead = el == 0;
-    uint32_t tdQ = tmem + C::tdQ + (((warp & 3) * 32) << 16);
-    asm volatile("" : "+r"(tdQ));
-    const float sc = a.scale;
-    for (int n = 0; n < n_iter; ++n) {
-      const int qt = qt_first + n / G, h = g * G + n % G;
-      const int buf = n & 1;
-      mbar_wait(bar(B_DQF + buf), (n >> 1) & 1);
-      tc_fence_after();
-      float v[BQ];
-      tmem_ld32(tdQ + 64 * buf, reinterpret_cast<uint32_t*>(v));
-      tmem_ld32(tdQ + 64 * buf + 32, reinterpret_cast<uint32_t*>(v) + 32);
-      tmem_wait_ld();
-      tc_fence_before();
-      mbar_arrive(bar(B_DQE + buf));
-      if (lead) bulk_wait_read1();  // the reduce-add of tile n-2 (same staging buffer) has read its source
-      named_bar(2 + chalf, 64);
-      const uint32_t stg = sDQ + (uint32_t)(buf * 2 + chalf) * C::kDQH + (uint32_t)el * 4;
+    if ((int)(warp & 3) < C::kDQW) {
+      const int cg = e >> 6, el = e & 63;
+      const int gw = (D - 64 * cg) < 64 ? (D - 64 * cg) : 64;  // width of this column group
+      const int gthreads = cg == 0 ? 64 : 32 * (C::kDQW - 2);
+      const bool lead = el == 0, valid = e < D;
+      uint32_t tdQ = tmem + C::tdQ + (((warp & 3) * 32) << 16);
+      asm volatile("" : "+r"(tdQ));
+      const float sc = a.scale;
+      for (int n = 0; n < n_iter; ++n) {
+        const int qt = qt_first + n / G, h = g * G + n % G;
+        const int buf = n & 1;
+        mbar_wait(bar(B_DQF), n & 1);
+        if (e == 0) TRACE(9, n);
+        tc_fence_after();
+        float v[BQ];
+        tmem_ld32(tdQ, reinterpret_cast<uint32_t*>(v));
+        tmem_ld32(tdQ + 32, reinterpret_cast<uint32_t*>(v) + 32);
+        tmem_wait_ld();
+        tc_fence_before();
+        mbar_arrive(bar(B_DQE));
+        if (lead) bulk_wait_read1();  // the reduce-add of tile n-2 (same staging buffer) has read its source
+        named_bar(2 + cg, gthreads);
+        const uint32_t gbase = sDQ + (uint32_t)buf * C::kDQB + (uint32_t)(cg * 64 * BQ * 4);
+        if (valid) {
+          const uint32_t stg = gbase + (uint32_t)el * 4;
 #pragma unroll
-      for (int q = 0; q < BQ; ++q) sts32(stg + q * 256, v[q] * sc);
-      fence_async_shared();
-      named_bar(2 + chalf, 64);
-      if (lead) {
-        tma_reduce_add_3d(&tm.dq, sDQ + (uint32_t)(buf * 2 + chalf) * C::kDQH, 64 * chalf, qt * BQ, h);
-        bulk_commit();
+          for (int q = 0; q < BQ; ++q) sts32(stg + q * gw * 4, v[q] * sc);
+        }
+        fence_async_shared();
+        named_bar(2 + cg, gthreads);
+        if (lead) {
+          tma_reduce_add_3d(gw == 64 ? &tm.dq64 : &tm.dq16, gbase, 64 * cg, qt * BQ, h);
+          bulk_commit();
+          if (e == 0) TRACE(11, n);
+        }
       }
+      if (lead) bulk_wait0();
     }
-    if (lead) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
   if (warp == 13) tmem_dealloc<512>(tmem);
+#undef TRACE
+}
+
+template <int D>
+int launch_q64(const BwdArgs& a, cudaStream_t s) {
+  using C = Cfg<D>;
+  TmapSet tm;
+  const CUtensorMapSwizzle sw = D == 80 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+  const uint32_t ac = C::TQ::kAC;
+  bool ok = make_tmap_rows_heads_dim(&tm.q, a.q.base, a.q.rows, a.q.heads, D, ac, BQ, sw);
+  ok &= make_tmap_rows_heads_dim(&tm.o, a.dout.base, a.dout.rows, a.dout.heads, D, ac, BQ, sw);
+  ok &= make_tmap_rows_heads_dim(&tm.k, a.k.base, a.k.rows, a.k.heads, D, ac, 128, sw);
+  ok &= make_tmap_rows_heads_dim(&tm.v, a.v.base, a.v.rows, a.v.heads, D, ac, 128, sw);
+  ok &= make_tmap_f32_head_major(&tm.dq64, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 64, BQ,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE);
+  ok &= make_tmap_f32_head_major(&tm.dq16, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 16, BQ,
+                                 CU_TENSOR_MAP_SWIZZLE_NONE);
+  if (!ok) return -1;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaFuncSetAttribute(attn_bwd_q64_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
+    attr_set = true;
+  }
+  attn_bwd_q64_kernel<D><<<dim3(a.n_kv_rows / 128, a.hq / a.G), kThreads, C::kSmem, s>>>(tm, a);
+  return (int)cudaGetLastError();
 }
 
 }  // namespace
 
 int launch_attn_bwd_q64_bf16(const BwdArgs& a, int head_dim, cudaStream_t s) {
-  if (head_dim != D) return -2;
-  TmapSet tm;
-  bool ok = make_tmap_rows_heads_dim(&tm.q, a.q.base, a.q.rows, a.q.heads, D, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_tmap_rows_heads_dim(&tm.o, a.dout.base, a.dout.rows, a.dout.heads, D, 64, BQ, CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
-  ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
-  ok &= make_tmap_f32_head_major(&tm.dq, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 64, BQ,
-                                 CU_TENSOR_MAP_SWIZZLE_NONE);
-  if (!ok) return -1;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(attn_bwd_q64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, Cfg::kSmem);
-    attr_set = true;
+  switch (head_dim) {
+    case 64: return launch_q64<64>(a, s);
+    case 80: return launch_q64<80>(a, s);
+    case 128: return launch_q64<128>(a, s);
   }
-  attn_bwd_q64_kernel<<<dim3(a.n_kv_rows / 128, a.hq / a.G), kThreads, Cfg::kSmem, s>>>(tm, a);
-  return (int)cudaGetLastError();
+  return -2;
 }
 
 }  // namespace fpdt

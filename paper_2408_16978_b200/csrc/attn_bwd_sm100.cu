@@ -480,14 +480,17 @@ int launch_bwd(const BwdArgs& a, cudaStream_t s) {
 // head_dim 64 / 80 run the software-pipelined kernel (attn_bwd_pipe_sm100.cu) unless FPDT_BWD_KERNEL=v2 selects
 // this one (A/B measurements); head_dim 128 always runs this one.
 int launch_attn_bwd_bf16(const BwdArgs& a, int head_dim, cudaStream_t s) {
-  static const bool use_v2 = [] {
+  // FPDT_BWD_KERNEL: unset = attn_bwd_q64 for d = 128 and attn_bwd_pipe for 64/80; "q64" / "pipe" / "v2" (this
+  // file's kernel) force one kernel for every head_dim it supports
+  static const int which = [] {
     const char* e = getenv("FPDT_BWD_KERNEL");
-    return e && strcmp(e, "v2") == 0;
+    if (e && strcmp(e, "v2") == 0) return 2;
+    if (e && strcmp(e, "q64") == 0) return 1;
+    if (e && strcmp(e, "pipe") == 0) return 3;
+    return 0;
   }();
-  if (!use_v2) {
-    if (head_dim == 128) return launch_attn_bwd_q64_bf16(a, head_dim, s);
-    return launch_attn_bwd_pipe_bf16(a, head_dim, s);
-  }
+  if (which == 1 || (which == 0 && head_dim == 128)) return launch_attn_bwd_q64_bf16(a, head_dim, s);
+  if (which == 0 || which == 3) return launch_attn_bwd_pipe_bf16(a, head_dim, s);
   switch (head_dim) {
     case 64: return launch_bwd<64>(a, s);
     case 80: return launch_bwd<80>(a, s);

@@ -98,6 +98,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--only", nargs="+", default=None)
     ap.add_argument("--steps", type=int, default=1)
+    ap.add_argument("--chunks", type=int, nargs="+", default=None, help="restrict the chunk sizes (in K tokens)")
     args = ap.parse_args()
     torch.cuda.set_device(0)
     genlib = _lib.load_generator()
@@ -105,6 +106,8 @@ def main():
         if args.only and name not in args.only:
             continue
         for C in chunks:
+            if args.chunks and C // K not in args.chunks:
+                continue
             try:
                 rec = run_one(name, text, S, Hq, Hkv, d, p, C, args.steps, genlib)
             except Exception as e:  # report and continue with the next workload
