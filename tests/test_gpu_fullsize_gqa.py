@@ -1,0 +1,94 @@
+"""Parity of the per-rank work of BASELINE.json configs[4] and configs[2] at their FULL sequence length.
+
+After the sequence-to-head all-to-all, a rank of a p-GPU run computes attention over the whole sequence for Hq/p
+query heads and Hkv/p kv heads; that is a p = 1 call with those head counts (tools/rank_workloads.py), here on the
+d = 128 backward kernel (attn_bwd_q64) with host offload:
+  c5: 70B layer at p = 8 -> S = 1,048,576, 8 q heads / 1 kv head (G = 8), d = 128, chunk 65,536 (u = 16)
+  c3: 8B layer at p = 4  -> S = 2,097,152, 8 q heads / 2 kv heads (G = 4), d = 128, chunk 65,536 (u = 32)
+Checks: sampled rows of O, lse, dQ (first/last row of every chunk plus seeded random rows)
+against oracle/sampled.rows_dq, and the exact identities sum_j dK_j = 0, sum_j dV_j = sum over the group of sum_i
+dO_i on every kv head.  Bar: 1e-2 (north_star, bf16)."""
+import ctypes
+
+import numpy as np
+import pytest
+import torch
+
+import fpdt_inputs as gen
+from fpdt_testlib import TOL, rel_err
+from oracle import sampled
+
+pytestmark = pytest.mark.gpu
+
+K64 = 65536
+CASES = {
+    "c5": dict(S=1 << 20, hq=8, hkv=1, heads=(0, 7), n_random=32),
+    "c3": dict(S=2 << 20, hq=8, hkv=2, heads=(7,), n_random=16),
+}
+D = 128
+
+
+def _run(S, hq, hkv, rows):
+    from paper_2408_16978_b200 import _lib, fpdt
+    torch.cuda.set_device(0)
+    genlib = _lib.load_generator()
+
+    def gen_tensor(name, h):
+        t = torch.empty(S, h, D, dtype=torch.bfloat16, device="cuda")
+        rc = genlib.fpdt_gen_fill(ctypes.c_void_p(t.data_ptr()), 0, gen.TENSOR_IDS[name], gen.DIST_IDS["normal"],
+                                  0, S, h, D, S, 0, 1, K64, ctypes.c_void_p(0))
+        assert rc == 0
+        return t
+
+    q, k, v, do = gen_tensor("q", hq), gen_tensor("k", hkv), gen_tensor("v", hkv), gen_tensor("do", hq)
+    o = torch.empty_like(q)
+    lse = torch.empty(S, hq, dtype=torch.float32, device="cuda")
+    dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+    ctx = fpdt.FPDTContext()
+    fpdt.fpdt_attn_fwd(ctx, q, k, v, o, lse, S, hq, hkv, D, 1, K64, 1, fpdt.FPDT_BF16, 1)
+    fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, S, hq, hkv, D, 1, K64, 1, fpdt.FPDT_BF16, 1)
+    torch.cuda.synchronize()
+    ctx.close()
+    ridx = torch.tensor(rows, device="cuda")
+    G = hq // hkv
+    out = {
+        "o": o.index_select(0, ridx).float().cpu().numpy(),
+        "lse": lse.index_select(0, ridx).cpu().numpy(),
+        "dq": dq.index_select(0, ridx).float().cpu().numpy(),
+        "dk_sum": dk.float().sum(0).cpu().numpy(), "dk_abs": dk.float().abs().sum(0).cpu().numpy(),
+        "dv_sum": dv.float().sum(0).cpu().numpy(), "dv_abs": dv.float().abs().sum(0).cpu().numpy(),
+        "do_group_sum": do.float().sum(0).reshape(hkv, G, D).sum(1).cpu().numpy(),
+    }
+    del q, k, v, do, o, lse, dq, dk, dv
+    torch.cuda.empty_cache()
+    return out
+
+
+@pytest.mark.parametrize("cfg", ["c5", "c3"])
+def test_fullsize_per_rank_gqa(cfg):
+    c = CASES[cfg]
+    S, hq, hkv = c["S"], c["hq"], c["hkv"]
+    rng = np.random.default_rng(1)
+    rows = sorted(set([0, S - 1] + [m * K64 for m in range(S // K64)] + [m * K64 + K64 - 1 for m in range(S // K64)]
+                      + rng.integers(0, S, c["n_random"]).tolist()))
+    got = _run(S, hq, hkv, rows)
+    # identities on every kv head, over all S rows
+    assert np.max(np.abs(got["dk_sum"]) / got["dk_abs"]) <= TOL["bf16"]
+    assert np.max(np.abs(got["dv_sum"] - got["do_group_sum"]) / got["dv_abs"]) <= TOL["bf16"]
+    # sampled rows against the plain definition (numpy twin of the generator)
+    G = hq // hkv
+    rows_a = np.array(rows)
+    toks = np.arange(S)
+    kv_cache = {}
+    for h in c["heads"]:
+        g = h // G
+        if g not in kv_cache:
+            kv_cache = {g: (gen.generate("k", "normal", 0, toks, hkv, D, S, heads=[g])[:, 0].astype(np.float64),
+                            gen.generate("v", "normal", 0, toks, hkv, D, S, heads=[g])[:, 0].astype(np.float64))}
+        kg, vg = kv_cache[g]
+        qr = gen.generate("q", "normal", 0, rows_a, hq, D, S, heads=[h])[:, 0]
+        dor = gen.generate("do", "normal", 0, rows_a, hq, D, S, heads=[h])[:, 0]
+        dq, o, lse = sampled.rows_dq(qr, dor, rows_a, kg, vg, sampled.default_scale(D))
+        errs = {"o": rel_err(got["o"][:, h], o), "lse": rel_err(got["lse"][:, h], lse),
+                "dq": rel_err(got["dq"][:, h], dq)}
+        assert all(e <= TOL["bf16"] for e in errs.values()), (cfg, h, errs)
