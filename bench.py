@@ -181,6 +181,8 @@ def run_ours(args):
     # NCCL id through torch.distributed (plumbing only)
     nid = distributed.broadcast_nccl_id(rank, world, fpdt.fpdt_get_unique_id)
     ctx = fpdt.FPDTContext(world, rank, nid, local)
+    if args.residency:
+        ctx.set_residency(*args.residency)
     keep = None
     if args.sparsity > 0:
         keep = gen.sparsity_plan(S // C, args.sparsity, seed=0)
@@ -352,7 +354,7 @@ def run_ours(args):
                    "chunks": S // C, "s_local": s_local, "offload": offload, "causal": 1,
                    "parallelism": f"ulysses-sp{world}", "l2": "inputs 2.7 GB/tensor >> 126 MB L2, no flush",
                    "flops_per_step": f_fwd + f_bwd, "flop_convention": "14*d per causal pair per q-head",
-                   "sparsity": args.sparsity},
+                   "sparsity": args.sparsity, "residency": args.residency or [0, 0]},
         "roofline": {"bound": "tensor", "kernel": "attn_bwd_pipe_kernel<80> (tcgen05 pair backward)",
                      "achieved": ach_bwd, "peak": sustained, "unit": "TFLOP/s", "frac": ach_bwd / sustained,
                      "traffic": traffic, "peak_source": peak_src + ", sustained bf16 (kernel timed inside a long step)",
@@ -369,6 +371,7 @@ def run_ours(args):
         "host_link": {"h2d_GBps": h2d_lib / (ms / 1e3) / 1e9, "d2h_GBps": d2h_lib / (ms / 1e3) / 1e9,
                       "measured_peak_GBps": {"h2d": 55.6, "d2h": 57.3}},
         "a2a_bytes_per_step": (st1["bytes_a2a"] - st0["bytes_a2a"]) // args.steps,
+        "device_bytes_library": st1["device_bytes"],
         "wall_s_timed": wall,
         "cpu_baseline": cpu,
     }
@@ -391,6 +394,9 @@ def main():
     ap.add_argument("--chunk", type=int, default=0, help="override the chunk size (testing)")
     ap.add_argument("--sparsity", type=float, default=0.0,
                     help="block sparsity rho (PAPER.md §5.6 / Table sparsity): fraction of causal chunk blocks dropped")
+    ap.add_argument("--residency", type=int, nargs=2, default=None, metavar=("KV_CHUNKS", "Q_CHUNKS"),
+                    help="HBM residency budget (fpdt_set_residency): first KV chunks / last query-side chunks kept on "
+                         "the device")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

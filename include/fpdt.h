@@ -126,6 +126,20 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
  * keep[i / C][j / C].  Collective: every rank passes the same plan. */
 int fpdt_set_sparsity(fpdt_ctx* ctx, const uint8_t* keep, int64_t n_chunks);
 
+/* HBM residency budget (the paper offloads every chunk).  With
+ * offload = 1, keep some chunks in device memory instead of the pinned host store:
+ *   kv_chunks: key/value chunks i < kv_chunks (global chunk index) are never offloaded nor fetched.  The forward
+ *     fetches chunk i once for every later query chunk, so the first chunks save the most host-to-device bytes.
+ *   q_chunks: query-side chunks i >= u - q_chunks (u = S / chunk_size) keep q_i, dO_i and their fp32 dq partial on
+ *     the device.  The backward fetches chunk i for every key chunk j <= i, so the last chunks save the most.
+ * Values larger than u mean u.  0, 0 (the default) is the paper's schedule.  Applies to the following
+ * fpdt_attn_fwd calls; fpdt_attn_bwd uses the setting of its forward.  Results equal the offloaded schedule's up to
+ * the order of the dq reduce-adds.  Device memory: world_size 1 reads the caller's q, k, v rows of resident chunks
+ * in place (they must stay valid and unmodified until fpdt_attn_bwd) plus C * hq * head_dim * 4 bytes per
+ * query-side chunk; world_size > 1 keeps each resident head-layout chunk, C * (hq + 2 hkv) * head_dim * elem
+ * bytes, plus C * 2 hq * head_dim * elem bytes per query-side chunk.  Errors: FPDT_ERR_ARG for negative counts. */
+int fpdt_set_residency(fpdt_ctx* ctx, int64_t kv_chunks, int64_t q_chunks);
+
 /* Message of the last non-OK status returned on this thread ("" if none). */
 const char* fpdt_last_error(void);
 

@@ -94,7 +94,7 @@ struct DevBuf {
 enum BufId {
   B_OACC, B_LSEACC, B_LSESAVE, B_OHAT, B_KVSLOT0, B_KVSLOT1, B_A2A_SEND0, B_A2A_SEND1, B_A2A_RECV0, B_A2A_RECV1,
   B_STORE, B_D, B_DQDEV, B_QSLOT0, B_QSLOT1, B_DOSLOT0, B_DOSLOT1, B_DQSLOT0, B_DQSLOT1, B_DKACC, B_DVACC,
-  B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_NUM
+  B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_RESSTORE, B_DORES, B_DQRES, B_NUM
 };
 
 }  // namespace
@@ -145,6 +145,9 @@ struct fpdt_ctx {
   std::vector<uint8_t> plan, saved_plan;
   int64_t plan_u = 0;
   const void *saved_q = nullptr, *saved_k = nullptr, *saved_v = nullptr;
+  // HBM residency budget (fpdt_set_residency): key/value chunks i < res_kv and query-side chunks i >= u - res_q stay
+  // on the device (offload = 1 only); the forward copies the setting, its backward uses the copy
+  int64_t res_kv = 0, res_q = 0, saved_res_kv = 0, saved_res_q = 0;
   fpdt_stats stats{};
   // kernel timing
   bool timing = false;
@@ -174,6 +177,31 @@ void* dev(fpdt_ctx* ctx, int id, size_t bytes) {
     ctx->stats.device_bytes += (int64_t)bytes;
   }
   return b.ptr;
+}
+
+// Which chunks stay on the device under the residency budget.  Key/value chunk i is resident
+// when i < rkv: the forward fetches chunk i for every later query chunk, so the first chunks save the most fetches.
+// Query-side chunk i (q_i, dO_i and its dq partial) is resident when i >= u - rq: the backward fetches chunk i for
+// every key chunk j <= i, so the last chunks save the most.  slot[m]: index of chunk m in the resident device store
+// (p > 1: the whole head-layout chunk after the all-to-all), qslot[m]: index among the query-side resident chunks.
+struct Residency {
+  int64_t u = 0, rkv = 0, rq = 0, n = 0, nq = 0;
+  std::vector<int64_t> slot, qslot;
+  bool kv(int64_t i) const { return i < rkv; }
+  bool q(int64_t i) const { return i >= u - rq; }
+};
+Residency make_residency(int64_t u, int64_t rkv, int64_t rq) {
+  Residency r;
+  r.u = u;
+  r.rkv = std::min(rkv, u);
+  r.rq = std::min(rq, u);
+  r.slot.assign((size_t)u, -1);
+  r.qslot.assign((size_t)u, -1);
+  for (int64_t m = 0; m < u; ++m) {
+    if (r.kv(m) || r.q(m)) r.slot[(size_t)m] = r.n++;
+    if (r.q(m)) r.qslot[(size_t)m] = r.nq++;
+  }
+  return r;
 }
 
 void ensure_events(std::vector<cudaEvent_t>& v, size_t n) {
@@ -371,6 +399,9 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       if (c.offload) a2a_recv[b] = (uint8_t*)dev(ctx, B_A2A_RECV0 + b, (size_t)C * hcomb * d * eb);
     }
   }
+  const Residency R = make_residency(u, c.offload ? ctx->saved_res_kv : 0, c.offload ? ctx->saved_res_q : 0);
+  uint8_t* resstore = (p > 1 && R.n > 0) ? (uint8_t*)dev(ctx, B_RESSTORE, (size_t)R.n * C * hcomb * d * eb) : nullptr;
+  auto res_chunk = [&](int64_t m) { return resstore + (size_t)R.slot[(size_t)m] * C * hcomb * d * eb; };
   uint8_t* kv_slot[2] = {nullptr, nullptr};
   if (c.offload) {
     kv_slot[0] = (uint8_t*)dev(ctx, B_KVSLOT0, (size_t)C * row_kv2);
@@ -384,10 +415,12 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   // p == 1 with offload: the head-layout chunk IS the caller's rows; offload all chunks up front
   if (p == 1 && c.offload) {
     for (int64_t m = 0; m < u; ++m) {
-      d2h(ctx, ctx->host + hl.q(m), (const uint8_t*)q + (size_t)m * C * row_q, (size_t)C * row_q);
-      const size_t wkv = (size_t)hkv * d * eb;
-      d2h_2d(ctx, ctx->host + hl.kv(m, u), row_kv2, (const uint8_t*)k + (size_t)m * C * wkv, wkv, wkv, C);
-      d2h_2d(ctx, ctx->host + hl.kv(m, u) + wkv, row_kv2, (const uint8_t*)v + (size_t)m * C * wkv, wkv, wkv, C);
+      if (!R.q(m)) d2h(ctx, ctx->host + hl.q(m), (const uint8_t*)q + (size_t)m * C * row_q, (size_t)C * row_q);
+      if (!R.kv(m)) {
+        const size_t wkv = (size_t)hkv * d * eb;
+        d2h_2d(ctx, ctx->host + hl.kv(m, u), row_kv2, (const uint8_t*)k + (size_t)m * C * wkv, wkv, wkv, C);
+        d2h_2d(ctx, ctx->host + hl.kv(m, u) + wkv, row_kv2, (const uint8_t*)v + (size_t)m * C * wkv, wkv, wkv, C);
+      }
       rec(ctx->ev_off[m], ctx->s_d2h);
     }
   }
@@ -412,7 +445,8 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     } else {
       // F3/F4: pack q,k,v rows of slot m and all-to-all (seq -> head)
       const int b = (int)(m & 1);
-      uint8_t* recv = c.offload ? a2a_recv[b] : store + (size_t)m * C * hcomb * d * eb;
+      uint8_t* recv = !c.offload ? store + (size_t)m * C * hcomb * d * eb : R.slot[(size_t)m] >= 0 ? res_chunk(m)
+                                                                                               : a2a_recv[b];
       wait(ctx->s_comm, ctx->ev_recv_used_c[b]);
       wait(ctx->s_comm, ctx->ev_recv_used_d[b]);
       const size_t per_peer = (size_t)c.c * hcomb * d;
@@ -429,8 +463,8 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
         // F5: offload q_m, kv_m from the receive buffer
         wait(ctx->s_d2h, ctx->ev_a2a[m]);
         const size_t pitch = (size_t)hcomb * d * eb;
-        d2h_2d(ctx, ctx->host + hl.q(m), row_q, recv, pitch, row_q, C);
-        d2h_2d(ctx, ctx->host + hl.kv(m, u), row_kv2, recv + row_q, pitch, row_kv2, C);
+        if (!R.q(m)) d2h_2d(ctx, ctx->host + hl.q(m), row_q, recv, pitch, row_q, C);
+        if (!R.kv(m)) d2h_2d(ctx, ctx->host + hl.kv(m, u), row_kv2, recv + row_q, pitch, row_kv2, C);
         rec(ctx->ev_off[m], ctx->s_d2h);
         rec(ctx->ev_recv_used_d[b], ctx->s_d2h);
       }
@@ -490,6 +524,22 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       // F7/F8: earlier chunks fetched from the host store, double-buffered
       for (int64_t i = 0; i < m; ++i) {
         if (!keep(m, i)) continue;
+        a.kv_pos0 = i * C;
+        a.has_prev = 1;
+        a.is_final = (i == last_kept);
+        if (R.kv(i)) {  // resident key/value chunk: no fetch
+          if (p == 1) {
+            a.k = {k, c.S, hkv, 0};
+            a.v = {v, c.S, hkv, 0};
+            a.kv_row0 = i * C;
+          } else {
+            a.k = {res_chunk(i), C, hcomb, hq};
+            a.v = {res_chunk(i), C, hcomb, hq + hkv};
+            a.kv_row0 = 0;
+          }
+          launch_fwd(ctx, c, a, cs);
+          continue;
+        }
         const int sl = fetch & 1;
         wait(ctx->s_h2d, ctx->ev_slot_free[sl]);
         wait(ctx->s_h2d, ctx->ev_off[i]);
@@ -560,6 +610,11 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   for (cudaStream_t s : {ctx->s_comm, ctx->s_h2d, ctx->s_d2h}) wait(s, ctx->ev_enter);
   HostLayout hl{};
   if (c.offload) hl = host_layout(c);
+  const Residency R = make_residency(u, c.offload ? ctx->saved_res_kv : 0, c.offload ? ctx->saved_res_q : 0);
+  uint8_t* resstore = (uint8_t*)ctx->bufs[B_RESSTORE].ptr;  // p > 1: the forward's resident head-layout chunks
+  auto res_chunk = [&](int64_t m) { return resstore + (size_t)R.slot[(size_t)m] * C * hcomb * d * eb; };
+  uint8_t* dores = (p > 1 && R.nq > 0) ? (uint8_t*)dev(ctx, B_DORES, (size_t)R.nq * C * 2 * hq * d * eb) : nullptr;
+  float* dqres = R.nq > 0 ? (float*)dev(ctx, B_DQRES, (size_t)R.nq * C * hq * d * 4) : nullptr;
   // ---- B1/B2: D and the head-layout dO
   const void* do_h = dout;            // head-layout dO view base (p == 1: the caller's dO)
   int64_t do_rows = c.S;
@@ -573,7 +628,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       rec(ctx->ev_tmp, cs);
       wait(ctx->s_d2h, ctx->ev_tmp);
       for (int64_t m = 0; m < u; ++m) {
-        d2h(ctx, ctx->host + hl.dO(m, u), (const uint8_t*)dout + (size_t)m * C * row_q, (size_t)C * row_q);
+        if (!R.q(m)) d2h(ctx, ctx->host + hl.dO(m, u), (const uint8_t*)dout + (size_t)m * C * row_q, (size_t)C * row_q);
         rec(ctx->ev_doff[m], ctx->s_d2h);
       }
     }
@@ -583,9 +638,11 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
     uint8_t* send = (uint8_t*)dev(ctx, B_A2A_SEND0, (size_t)C * 2 * hq * d * eb);
     gathered = (uint8_t*)dev(ctx, B_DOSTORE, (size_t)(c.offload ? 2 * C : c.S) * 2 * hq * d * eb);
     for (int64_t m = 0; m < u; ++m) {
-      uint8_t* recv = c.offload ? gathered + (size_t)(m & 1) * C * 2 * hq * d * eb
-                                : gathered + (size_t)m * C * 2 * hq * d * eb;
-      if (c.offload && m >= 2) wait(ctx->s_comm, ctx->ev_doff[m - 2]);
+      // query-side resident chunks (a suffix of m) keep their (O, dO) chunk; the others share a double buffer
+      uint8_t* recv = !c.offload ? gathered + (size_t)m * C * 2 * hq * d * eb
+                      : R.q(m)   ? dores + (size_t)R.qslot[(size_t)m] * C * 2 * hq * d * eb
+                                 : gathered + (size_t)(m & 1) * C * 2 * hq * d * eb;
+      if (c.offload && !R.q(m) && m >= 2) wait(ctx->s_comm, ctx->ev_doff[m - 2]);
       FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)o + (size_t)m * c.c * c.Hq * d * eb, c.c, c.Hq, d, p, eb,
                                              send, per_peer, (int64_t)2 * hq * d, 0, ctx->s_comm));
       FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)dout + (size_t)m * c.c * c.Hq * d * eb, c.c, c.Hq, d, p,
@@ -598,7 +655,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
                                                 (int64_t)hq * d, Dh + m * C, c.S, ctx->s_comm));
       ctx->stats.kernel_launches++;
       rec(ctx->ev_a2a[m], ctx->s_comm);
-      if (c.offload) {
+      if (c.offload && !R.q(m)) {
         wait(ctx->s_d2h, ctx->ev_a2a[m]);
         d2h_2d(ctx, ctx->host + hl.dO(m, u), row_q, recv + row_q, (size_t)2 * hq * d * eb, row_q, C);
         rec(ctx->ev_doff[m], ctx->s_d2h);
@@ -722,33 +779,69 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       int64_t last_i = j;  // the last query chunk that attends key chunk j
       for (int64_t i = j; i < u; ++i)
         if (keep(i, j)) last_i = i;
-      // B3: fetch kv_j
-      wait(ctx->s_h2d, ctx->ev_kv_free[ks]);
-      h2d(ctx, kvs[ks], ctx->host + hl.kv(j, u), (size_t)C * row_kv2);
-      rec(ctx->ev_kv_filled[ks], ctx->s_h2d);
-      wait(cs, ctx->ev_kv_filled[ks]);
+      // B3: fetch kv_j (resident key/value chunks are read in place)
+      HeadView kj, vj;
+      int64_t kv_row0 = 0;
+      if (R.kv(j)) {
+        if (p == 1) {
+          kj = {ctx->saved_k, c.S, hkv, 0};
+          vj = {ctx->saved_v, c.S, hkv, 0};
+          kv_row0 = j * C;
+        } else {
+          kj = {res_chunk(j), C, hcomb, hq};
+          vj = {res_chunk(j), C, hcomb, hq + hkv};
+        }
+      } else {
+        wait(ctx->s_h2d, ctx->ev_kv_free[ks]);
+        h2d(ctx, kvs[ks], ctx->host + hl.kv(j, u), (size_t)C * row_kv2);
+        rec(ctx->ev_kv_filled[ks], ctx->s_h2d);
+        wait(cs, ctx->ev_kv_filled[ks]);
+        kj = {kvs[ks], C, 2 * hkv, 0};
+        vj = {kvs[ks], C, 2 * hkv, hkv};
+      }
       for (int64_t i = j; i < u; ++i) {
         if (!keep(i, j)) continue;
-        const int sl = (step++) & 1;
-        // B4: fetch q_i, dO_i and (when it already holds contributions) the dq partial of chunk i
-        wait(ctx->s_h2d, ctx->ev_q_free[sl]);
-        wait(ctx->s_h2d, ctx->ev_doff[i]);
-        h2d(ctx, qs[sl], ctx->host + hl.q(i), (size_t)C * row_q);
-        h2d(ctx, dos[sl], ctx->host + hl.dO(i, u), (size_t)C * row_q);
-        if (dq_started[i]) {
-          wait(ctx->s_h2d, ctx->ev_dqoff[i]);
-          h2d(ctx, dqs[sl], ctx->host + hl.dq(i, u), (size_t)C * hq * d * 4);
+        const bool qres = R.q(i);
+        const int sl = qres ? 0 : (step++) & 1;
+        HeadView qi, doi;
+        int64_t q_row0 = 0;
+        float* dqi = nullptr;
+        if (qres) {
+          // query-side resident chunk: q_i, dO_i in place, its dq partial accumulates in device memory
+          if (p == 1) {
+            qi = {ctx->saved_q, c.S, hq, 0};
+            doi = {do_h, do_rows, do_heads, do_head0};
+            q_row0 = i * C;
+          } else {
+            qi = {res_chunk(i), C, hcomb, 0};
+            doi = {dores + (size_t)R.qslot[(size_t)i] * C * 2 * hq * d * eb, C, 2 * hq, hq};
+          }
+          dqi = dqres + (size_t)R.qslot[(size_t)i] * C * hq * d;
+          if (!dq_started[i]) FPDT_CHECK_CUDA(cudaMemsetAsync(dqi, 0, (size_t)C * hq * d * 4, cs));
+        } else {
+          // B4: fetch q_i, dO_i and (when it already holds contributions) the dq partial of chunk i
+          wait(ctx->s_h2d, ctx->ev_q_free[sl]);
+          wait(ctx->s_h2d, ctx->ev_doff[i]);
+          h2d(ctx, qs[sl], ctx->host + hl.q(i), (size_t)C * row_q);
+          h2d(ctx, dos[sl], ctx->host + hl.dO(i, u), (size_t)C * row_q);
+          if (dq_started[i]) {
+            wait(ctx->s_h2d, ctx->ev_dqoff[i]);
+            h2d(ctx, dqs[sl], ctx->host + hl.dq(i, u), (size_t)C * hq * d * 4);
+          }
+          rec(ctx->ev_q_filled[sl], ctx->s_h2d);
+          wait(cs, ctx->ev_q_filled[sl]);
+          if (!dq_started[i]) FPDT_CHECK_CUDA(cudaMemsetAsync(dqs[sl], 0, (size_t)C * hq * d * 4, cs));
+          qi = {qs[sl], C, hq, 0};
+          doi = {dos[sl], C, hq, 0};
+          dqi = dqs[sl];
         }
-        rec(ctx->ev_q_filled[sl], ctx->s_h2d);
-        wait(cs, ctx->ev_q_filled[sl]);
-        if (!dq_started[i]) FPDT_CHECK_CUDA(cudaMemsetAsync(dqs[sl], 0, (size_t)C * hq * d * 4, cs));
         BwdArgs a;
-        a.q = {qs[sl], C, hq, 0};
-        a.dout = {dos[sl], C, hq, 0};
-        a.k = {kvs[ks], C, 2 * hkv, 0};
-        a.v = {kvs[ks], C, 2 * hkv, hkv};
-        a.q_row0 = 0;
-        a.kv_row0 = 0;
+        a.q = qi;
+        a.dout = doi;
+        a.k = kj;
+        a.v = vj;
+        a.q_row0 = q_row0;
+        a.kv_row0 = kv_row0;
         a.n_q_rows = (int)C;
         a.n_kv_rows = (int)C;
         a.q_pos0 = i * C;
@@ -761,7 +854,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
         a.lse2 = lse_save + i * C;
         a.Dstat = Dh + i * C;
         a.stat_ld = c.S;
-        a.dq_acc = dqs[sl];  // head-major [hq][C][d]
+        a.dq_acc = dqi;  // head-major [hq][C][d]
         a.dq_head_stride = C * d;
         a.dk_acc = dk_acc;
         a.dv_acc = dv_acc;
@@ -769,7 +862,10 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
         a.kv_final = (i == last_i);
         set_kv_out(a, j);
         launch_bwd(ctx, c, a, cs);
-        if (i == j) {
+        if (qres) {
+          dq_started[i] = 1;
+          if (i == j) emit_dq(j, dqi, C * d);  // B6: final
+        } else if (i == j) {
           // B6: dq_j is final after its last contribution (inner iteration i == j)
           emit_dq(j, dqs[sl], C * d);
           rec(ctx->ev_q_free[sl], cs);
@@ -943,6 +1039,8 @@ int fpdt_attn_fwd(fpdt_ctx* ctx, const void* q, const void* k, const void* v, vo
         if (!ctx->plan[(size_t)(m * c.u + m)]) fail(FPDT_ERR_ARG, "sparsity plan drops a diagonal block");
     }
     ctx->saved_plan = ctx->plan;
+    ctx->saved_res_kv = ctx->res_kv;
+    ctx->saved_res_q = ctx->res_q;
     ctx->fwd_done = false;
     forward(ctx, c, q, k, v, o, lse, static_cast<cudaStream_t>(stream));
     ctx->saved = c;
@@ -976,6 +1074,14 @@ int fpdt_set_sparsity(fpdt_ctx* ctx, const uint8_t* keep, int64_t n_chunks) {
     else
       ctx->plan.assign(keep, keep + (size_t)(n_chunks * n_chunks));
     ctx->plan_u = n_chunks;
+  });
+}
+
+int fpdt_set_residency(fpdt_ctx* ctx, int64_t kv_chunks, int64_t q_chunks) {
+  return run([&] {
+    if (!ctx || kv_chunks < 0 || q_chunks < 0) fail(FPDT_ERR_ARG, "bad residency arguments");
+    ctx->res_kv = kv_chunks;
+    ctx->res_q = q_chunks;
   });
 }
 

@@ -22,7 +22,7 @@ STATUS_NAMES = {0: "FPDT_OK", 1: "FPDT_ERR_ARG", 2: "FPDT_ERR_DIVISIBILITY", 3: 
 EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_attn_fwd", "fpdt_attn_bwd",
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair", "fpdt_group_create",
-            "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity",
+            "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity", "fpdt_set_residency",
             "fpdt_selftest_softmax", "fpdt_selftest_reduce")
 
 
@@ -67,6 +67,8 @@ def _declare(lib):
     lib.fpdt_global_token.restype = c_int64
     lib.fpdt_set_sparsity.argtypes = [P, P, c_int64]
     lib.fpdt_set_sparsity.restype = c_int
+    lib.fpdt_set_residency.argtypes = [P, c_int64, c_int64]
+    lib.fpdt_set_residency.restype = c_int
     lib.fpdt_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
     lib.fpdt_get_stats.restype = c_int
     lib.fpdt_set_kernel_timing.argtypes = [P, c_int]
@@ -172,6 +174,11 @@ class FPDTContext:
         assert k.ndim == 2 and k.shape[0] == k.shape[1]
         self._plan = k  # keep alive during the call (the library copies it)
         _check(lib().fpdt_set_sparsity(self.handle, c_void_p(k.ctypes.data), k.shape[0]))
+
+    def set_residency(self, kv_chunks: int = 0, q_chunks: int = 0):
+        """HBM residency budget for the following forward calls (offload = 1): key/value chunks i < kv_chunks and
+        query-side chunks i >= u - q_chunks stay in device memory (include/fpdt.h)."""
+        _check(lib().fpdt_set_residency(self.handle, int(kv_chunks), int(q_chunks)))
 
     def set_kernel_timing(self, enable: bool):
         _check(lib().fpdt_set_kernel_timing(self.handle, int(enable)))

@@ -16,7 +16,7 @@ from fpdt_testlib import TOL, oracle_full, rel_err
 pytestmark = pytest.mark.gpu
 
 
-def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None) -> dict:
+def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None, residency=None) -> dict:
     """Shard the global inputs x by the rank-ordinal contract, run fwd+bwd on p local ranks, unshard."""
     from paper_2408_16978_b200 import fpdt
     S, Hq, d = x["q"].shape
@@ -43,6 +43,8 @@ def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None) -> d
             ctx = fpdt.FPDTContext(p, r, group=group) if p > 1 else fpdt.FPDTContext()
             if keep is not None:
                 ctx.set_sparsity(keep)
+            if residency is not None:
+                ctx.set_residency(*residency)
             fpdt.fpdt_attn_fwd(ctx, q, k, v, o, lse, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
             fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
             stream.synchronize()
@@ -136,4 +138,21 @@ def test_block_sparse_multirank():
     dq, dk, dv = attention.attention_backward(x["q"], x["k"], x["v"], o, lse, x["do"], keep=keep, chunk=C)
     ref = {"o": o, "lse": lse, "dq": dq, "dk": dk, "dv": dv}
     errs = {n: rel_err(got[n], ref[n]) for n in ref}
+    assert all(e <= TOL["bf16"] for e in errs.values()), errs
+
+
+@pytest.mark.parametrize("residency", [(1, 1), (2, 3), (4, 4)])
+def test_residency_multirank(residency):
+    """HBM residency budget (include/fpdt.h fpdt_set_residency) at p = 2: resident head-layout chunks and (O, dO)
+    chunks stay on the device; O, lse, dK, dV bitwise equal to the fully offloaded run, dQ within its reduce order,
+    and the oracle."""
+    S, Hq, Hkv, d, C = 2048, 4, 2, 80, 512   # u = 4
+    x = gen.make_inputs("normal", 14, S, Hq, Hkv, d)
+    base = run_group(x, 2, C, "bf16", 1)
+    got = run_group(x, 2, C, "bf16", 1, residency=residency)
+    for n in ("o", "lse", "dk", "dv"):
+        assert np.array_equal(got[n], base[n]), (n, residency)
+    assert rel_err(got["dq"], base["dq"]) < 1e-3
+    ref = oracle_full(x)
+    errs = {n: rel_err(got[n], ref[n]) for n in ("o", "lse", "dq", "dk", "dv")}
     assert all(e <= TOL["bf16"] for e in errs.values()), errs
