@@ -183,6 +183,7 @@ def run_ours(args):
     ctx = fpdt.FPDTContext(world, rank, nid, local)
     if args.residency:
         ctx.set_residency(*args.residency)
+    ctx.set_bwd_order({"kv": fpdt.FPDT_BWD_KV_OUTER, "q": fpdt.FPDT_BWD_Q_OUTER, "auto": fpdt.FPDT_BWD_AUTO}[args.bwd_order])
     keep = None
     if args.sparsity > 0:
         keep = gen.sparsity_plan(S // C, args.sparsity, seed=0)
@@ -354,7 +355,8 @@ def run_ours(args):
                    "chunks": S // C, "s_local": s_local, "offload": offload, "causal": 1,
                    "parallelism": f"ulysses-sp{world}", "l2": "inputs 2.7 GB/tensor >> 126 MB L2, no flush",
                    "flops_per_step": f_fwd + f_bwd, "flop_convention": "14*d per causal pair per q-head",
-                   "sparsity": args.sparsity, "residency": args.residency or [0, 0]},
+                   "sparsity": args.sparsity, "residency": args.residency or [0, 0],
+                   "bwd_order": ["kv_outer", "q_outer"][st1["bwd_order"]]},
         "roofline": {"bound": "tensor", "kernel": "attn_bwd_pipe_kernel<80> (tcgen05 pair backward)",
                      "achieved": ach_bwd, "peak": sustained, "unit": "TFLOP/s", "frac": ach_bwd / sustained,
                      "traffic": traffic, "peak_source": peak_src + ", sustained bf16 (kernel timed inside a long step)",
@@ -397,6 +399,8 @@ def main():
     ap.add_argument("--residency", type=int, nargs=2, default=None, metavar=("KV_CHUNKS", "Q_CHUNKS"),
                     help="HBM residency budget (fpdt_set_residency): first KV chunks / last query-side chunks kept on "
                          "the device")
+    ap.add_argument("--bwd-order", default="kv", choices=["kv", "q", "auto"],
+                    help="backward loop order (fpdt_set_bwd_order): kv = the paper's (KV outer), q = GQA-aware Q outer")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -140,6 +140,24 @@ int fpdt_set_sparsity(fpdt_ctx* ctx, const uint8_t* keep, int64_t n_chunks);
  * bytes, plus C * 2 hq * head_dim * elem bytes per query-side chunk.  Errors: FPDT_ERR_ARG for negative counts. */
 int fpdt_set_residency(fpdt_ctx* ctx, int64_t kv_chunks, int64_t q_chunks);
 
+/* Backward loop order (offload = 1 only, offload = 0 always runs the paper's order).
+ *   FPDT_BWD_KV_OUTER (default): the paper's order (fig:bw_db): outer loop over key/value chunks j, inner
+ *     loop over query chunks i >= j; the fp32 dq partial of every query chunk round-trips the host store
+ *     (C * hq * head_dim * 4 bytes each way per pair).
+ *   FPDT_BWD_Q_OUTER (GQA-aware): outer loop over query chunks i, inner loop over key/value chunks j <= i.  q_i, dO_i
+ *     are fetched once per outer iteration and dq_i stays on the device until it is final; the fp32 dK_j/dV_j
+ *     partials round-trip the host store instead (C * 2 hkv * head_dim * 4 bytes each way per pair).  With GQA
+ *     (2 hkv < hq) that moves fewer host bytes; dK_j, dV_j are final only after the last query chunk that attends
+ *     key chunk j (the chunk-wise dK/dV hand-off of P:L365 is lost for the dense mask).  Its extra pinned store
+ *     (u * C * 2 hkv * head_dim * 4 bytes) is allocated by the first Q-outer backward.
+ *   FPDT_BWD_AUTO: per backward call, the order whose schedule moves fewer host bytes (given the sparsity plan and
+ *     residency budget of the forward); ties take KV_OUTER.
+ * Both orders compute the same sums; results agree up to the order of the fp32 additions.  Applies to the following
+ * fpdt_attn_bwd calls; fpdt_get_stats reports the order the last backward ran.  Errors: FPDT_ERR_ARG for an
+ * unknown order. */
+enum { FPDT_BWD_KV_OUTER = 0, FPDT_BWD_Q_OUTER = 1, FPDT_BWD_AUTO = 2 };
+int fpdt_set_bwd_order(fpdt_ctx* ctx, int order);
+
 /* Message of the last non-OK status returned on this thread ("" if none). */
 const char* fpdt_last_error(void);
 
@@ -156,6 +174,8 @@ typedef struct fpdt_stats {
   int64_t fetch_slots_highwater; /* max fetched key/value chunk sets resident at once (<= 2) */
   int64_t host_arena_bytes;   /* pinned host store reserved */
   int64_t device_bytes;       /* library-owned device working set */
+  int64_t bwd_order;          /* loop order of the last fpdt_attn_bwd (FPDT_BWD_KV_OUTER / FPDT_BWD_Q_OUTER) */
+  int64_t host_dkv_bytes;     /* pinned store of the Q-outer backward's dK/dV partials (0 until first used) */
 } fpdt_stats;
 int fpdt_get_stats(const fpdt_ctx* ctx, fpdt_stats* out);
 

@@ -19,6 +19,7 @@
 #include <cmath>
 #include <condition_variable>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <mutex>
@@ -94,7 +95,8 @@ struct DevBuf {
 enum BufId {
   B_OACC, B_LSEACC, B_LSESAVE, B_OHAT, B_KVSLOT0, B_KVSLOT1, B_A2A_SEND0, B_A2A_SEND1, B_A2A_RECV0, B_A2A_RECV1,
   B_STORE, B_D, B_DQDEV, B_QSLOT0, B_QSLOT1, B_DOSLOT0, B_DOSLOT1, B_DQSLOT0, B_DQSLOT1, B_DKACC, B_DVACC,
-  B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_RESSTORE, B_DORES, B_DQRES, B_NUM
+  B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_RESSTORE, B_DORES, B_DQRES, B_DKVSLOT0,
+  B_DKVSLOT1, B_DKVRES, B_KVSLOT2, B_KVSLOT3, B_DKVSLOT2, B_DKVSLOT3, B_QOSEND, B_QORECV, B_NUM
 };
 
 }  // namespace
@@ -128,11 +130,18 @@ struct fpdt_ctx {
   ncclComm_t comm = nullptr;
   fpdt_group* group = nullptr;  // non-null: in-process group instead of NCCL
   cudaStream_t s_comm = nullptr, s_h2d = nullptr, s_d2h = nullptr;
+  // Q-outer backward: second compute stream (pairs of one query chunk run two at a time) and its slot events
+  cudaStream_t s_comp2 = nullptr;
+  int qo_streams = 2;  // FPDT_BWD_QO_STREAMS (1 or 2)
+  cudaEvent_t ev_qo_free[4] = {}, ev_qo_filled[4] = {}, ev_qo_done[4] = {}, ev_qo_send[3] = {}, ev_fork = nullptr,
+              ev_join = nullptr;
   uint8_t* host = nullptr;
   size_t host_bytes = 0;
+  uint8_t* host_dkv = nullptr;  // Q-outer backward: fp32 dK/dV partials [u][2][C][hkv][d] (fpdt_set_bwd_order)
+  size_t host_dkv_bytes = 0;
   DevBuf bufs[B_NUM];
   // per-chunk events
-  std::vector<cudaEvent_t> ev_off, ev_doff, ev_dqoff, ev_a2a;
+  std::vector<cudaEvent_t> ev_off, ev_doff, ev_dqoff, ev_dkvoff, ev_a2a;
   cudaEvent_t ev_enter = nullptr, ev_slot_free[2] = {}, ev_slot_filled[2] = {}, ev_q_free[2] = {}, ev_q_filled[2] = {},
               ev_dq_ready[2] = {}, ev_kv_free[2] = {}, ev_kv_filled[2] = {}, ev_recv_used_c[2] = {},
               ev_recv_used_d[2] = {}, ev_o_ready = nullptr, ev_comm_done = nullptr, ev_d2h_done = nullptr,
@@ -148,6 +157,7 @@ struct fpdt_ctx {
   // HBM residency budget (fpdt_set_residency): key/value chunks i < res_kv and query-side chunks i >= u - res_q stay
   // on the device (offload = 1 only); the forward copies the setting, its backward uses the copy
   int64_t res_kv = 0, res_q = 0, saved_res_kv = 0, saved_res_q = 0;
+  int bwd_order = FPDT_BWD_KV_OUTER;  // fpdt_set_bwd_order
   fpdt_stats stats{};
   // kernel timing
   bool timing = false;
@@ -257,6 +267,48 @@ HostLayout host_layout(const Config& c) {
   h.dq_bytes = (size_t)c.C * c.hq * c.d * 4;
   h.total = (size_t)c.u * (h.q_bytes + h.kv_bytes + h.do_bytes + h.dq_bytes);
   return h;
+}
+
+// Host-link bytes (H2D + D2H) of the offloaded backward's chunk loop in either order (fpdt_set_bwd_order), for
+// FPDT_BWD_AUTO.  keep(i, j): block (query chunk i, key chunk j) is computed; kres / qres: residency.
+//   KV-outer: per j kv_j; per kept (i, j): q_i, dO_i, and the dq partial of i in (unless first) and out
+//     (unless i == j, where dq_i is final).
+//   Q-outer: per i q_i, dO_i; per kept (i, j): kv_j, and the dK/dV partial of j in (unless first) and out (unless
+//     i is the last query chunk attending j).
+template <class Keep>
+int64_t bwd_host_bytes(int order, const Config& c, int64_t rkv, int64_t rq, const Keep& keep) {
+  const int64_t u = c.u;
+  const int64_t kv = c.C * 2 * c.hkv * c.d * c.eb, qc = c.C * c.hq * c.d * c.eb;
+  const int64_t dqc = c.C * c.hq * c.d * 4, dkvc = c.C * 2 * c.hkv * c.d * 4;
+  auto kres = [&](int64_t i) { return i < rkv; };
+  auto qres = [&](int64_t i) { return i >= u - rq; };
+  int64_t b = 0;
+  if (order == FPDT_BWD_KV_OUTER) {
+    std::vector<char> started((size_t)u, 0);
+    for (int64_t j = 0; j < u; ++j) {
+      if (!kres(j)) b += kv;
+      for (int64_t i = j; i < u; ++i) {
+        if (!keep(i, j)) continue;
+        if (!qres(i)) b += 2 * qc + (started[(size_t)i] ? dqc : 0) + (i != j ? dqc : 0);
+        started[(size_t)i] = 1;
+      }
+    }
+  } else {
+    std::vector<int64_t> last((size_t)u, 0);
+    for (int64_t j = 0; j < u; ++j)
+      for (int64_t i = j; i < u; ++i)
+        if (keep(i, j)) last[(size_t)j] = i;
+    std::vector<char> started((size_t)u, 0);
+    for (int64_t i = 0; i < u; ++i) {
+      if (!qres(i)) b += 2 * qc;
+      for (int64_t j = 0; j <= i; ++j) {
+        if (!keep(i, j)) continue;
+        if (!kres(j)) b += kv + (started[(size_t)j] ? dkvc : 0) + (i != last[(size_t)j] ? dkvc : 0);
+        started[(size_t)j] = 1;
+      }
+    }
+  }
+  return b;
 }
 
 void ensure_host(fpdt_ctx* ctx, size_t bytes) {
@@ -593,6 +645,247 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
 }
 
 // ------------------------------------------------------------------------------------------ backward
+// Q-outer chunk loop of the offloaded backward (fpdt_set_bwd_order FPDT_BWD_Q_OUTER).  The pair
+// kernels and their arguments are the paper order's; only the loop nesting and what round-trips the host
+// differ: for query chunk i (outer) fetch q_i, dO_i once and keep the fp32 dq_i accumulator on the device; for each
+// key chunk j <= i (inner) fetch kv_j and the fp32 dK_j/dV_j partial (unless it is j's first pair), run pair (i, j),
+// and write the partial back (unless i is the last query chunk attending j, where the kernel writes the final dK_j,
+// dV_j).  After the inner loop dq_i is final.  p > 1: dq_i and (dk_j, dv_j) return to their owner ranks by separate
+// all-to-alls, each as soon as it is final.
+template <class Keep>
+void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const Keep& keep, const void* do_h,
+                      int64_t do_rows, int do_heads, int do_head0, uint8_t* dores, void* dq, void* dk, void* dv,
+                      cudaStream_t cs) {
+  const int64_t C = c.C, u = c.u;
+  const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
+  const int hcomb = hq + 2 * hkv;
+  const size_t row_q = (size_t)hq * d * eb, row_kv2 = (size_t)2 * hkv * d * eb;
+  const size_t dkv_elems = (size_t)C * 2 * hkv * d, dkv_bytes = dkv_elems * 4;
+  const float sl2 = c.scale * 1.4426950408889634f;
+  float* lse_save = (float*)ctx->bufs[B_LSESAVE].ptr;
+  float* Dh = (float*)ctx->bufs[B_D].ptr;
+  const HostLayout hl = host_layout(c);
+  uint8_t* resstore = (uint8_t*)ctx->bufs[B_RESSTORE].ptr;
+  auto res_chunk = [&](int64_t m) { return resstore + (size_t)R.slot[(size_t)m] * C * hcomb * d * eb; };
+
+  std::vector<int64_t> last_i((size_t)u, 0);  // the last query chunk attending key chunk j
+  for (int64_t j = 0; j < u; ++j)
+    for (int64_t i = j; i < u; ++i)
+      if (keep(i, j)) last_i[(size_t)j] = i;
+  // pinned store of the dK/dV partials (grow-only, separate from the forward's store so the latter stays valid)
+  if (R.rkv < u && u > 1) {
+    const size_t need = (size_t)u * dkv_bytes;
+    if (ctx->host_dkv_bytes < need) {
+      if (ctx->host_dkv) {
+        FPDT_CHECK_CUDA(cudaDeviceSynchronize());
+        cudaFreeHost(ctx->host_dkv);
+        ctx->host_dkv = nullptr;
+        ctx->host_dkv_bytes = 0;
+      }
+      void* hp = nullptr;
+      cudaError_t e = cudaHostAlloc(&hp, need, cudaHostAllocDefault);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(FPDT_ERR_HOST_OOM, "pinned dK/dV partial store of " + std::to_string(need) + " bytes: " + cudaGetErrorString(e));
+      }
+      ctx->host_dkv = static_cast<uint8_t*>(hp);
+      ctx->host_dkv_bytes = need;
+      ctx->stats.host_dkv_bytes = (int64_t)need;
+    }
+  }
+  ensure_events(ctx->ev_dkvoff, u);
+  // The pairs (i, j) of one query chunk i share only dq_i, which the kernels reduce-add (order-free), so they run
+  // two at a time on two compute streams: the second kernel's CTAs fill the SMs the first one's last wave leaves
+  // idle (a full pair is 512 CTAs, 3.5 waves, when one kv head per rank is left: configs[4] at p = 8).
+  // Key/value slots: two per stream (fetch of the next pair while the current one computes).
+  const int ns = ctx->qo_streams, nslots = 2 * ns;
+  cudaStream_t streams[2] = {cs, ctx->s_comp2};
+  static const int kv_ids[4] = {B_KVSLOT0, B_KVSLOT1, B_KVSLOT2, B_KVSLOT3};
+  static const int dkv_ids[4] = {B_DKVSLOT0, B_DKVSLOT1, B_DKVSLOT2, B_DKVSLOT3};
+  uint8_t* kvs[4] = {};
+  float* dkvs[4] = {};
+  for (int b = 0; b < nslots; ++b) {
+    kvs[b] = (uint8_t*)dev(ctx, kv_ids[b], (size_t)C * row_kv2);
+    dkvs[b] = (float*)dev(ctx, dkv_ids[b], dkv_bytes);
+  }
+  float* dkvres = R.rkv > 0 ? (float*)dev(ctx, B_DKVRES, (size_t)R.rkv * dkv_bytes) : nullptr;
+  uint8_t* qs[2] = {(uint8_t*)dev(ctx, B_QSLOT0, (size_t)C * row_q), (uint8_t*)dev(ctx, B_QSLOT1, (size_t)C * row_q)};
+  uint8_t* dos[2] = {(uint8_t*)dev(ctx, B_DOSLOT0, (size_t)C * row_q), (uint8_t*)dev(ctx, B_DOSLOT1, (size_t)C * row_q)};
+  float* dqs[2] = {(float*)dev(ctx, B_DQSLOT0, (size_t)C * hq * d * 4), (float*)dev(ctx, B_DQSLOT1, (size_t)C * hq * d * 4)};
+  // p > 1 send / receive buffers: [C][hq][d] for dq, then two [C][2hkv][d] parts for (dk, dv), alternating between
+  // final key chunks (ev_qo_send[0] = dq part free, [1 + r] = part r free)
+  uint8_t *qsend = nullptr, *qrecv = nullptr;
+  const size_t kvpart = (size_t)C * row_kv2;
+  if (p > 1) {
+    qsend = (uint8_t*)dev(ctx, B_QOSEND, (size_t)C * row_q + 2 * kvpart);
+    qrecv = (uint8_t*)dev(ctx, B_QORECV, (size_t)C * row_q + 2 * kvpart);
+    for (int b = 0; b < 3; ++b) rec(ctx->ev_qo_send[b], cs);
+  }
+  for (int b = 0; b < nslots; ++b) rec(ctx->ev_qo_free[b], cs);
+  for (int b = 0; b < 2; ++b) rec(ctx->ev_q_free[b], cs);
+  // B7 (p > 1): a final part goes back to the sequence layout of its owner ranks, after the kernel on `st`
+  auto send_back = [&](cudaStream_t st, int part, int64_t chunk) {
+    const bool is_dq = part == 0;
+    const size_t off = is_dq ? 0 : (size_t)C * row_q + (size_t)(part - 1) * kvpart;
+    const int heads = is_dq ? hq : 2 * hkv;
+    rec(ctx->ev_o_ready, st);
+    wait(ctx->s_comm, ctx->ev_o_ready);
+    const int64_t pst = (int64_t)c.c * heads * d, rld = (int64_t)heads * d;
+    alltoall(ctx, qsend + off, qrecv + off, (size_t)pst, c.dtype);
+    if (is_dq) {
+      FPDT_CHECK_LAUNCH(launch_unpack_head2seq(qrecv + off, pst, rld, 0, c.c, c.Hq, d, p, eb,
+                                               (uint8_t*)dq + (size_t)chunk * c.c * c.Hq * d * eb, ctx->s_comm));
+      ctx->stats.kernel_launches += 1;
+    } else {
+      FPDT_CHECK_LAUNCH(launch_unpack_head2seq(qrecv + off, pst, rld, 0, c.c, c.Hkv, d, p, eb,
+                                               (uint8_t*)dk + (size_t)chunk * c.c * c.Hkv * d * eb, ctx->s_comm));
+      FPDT_CHECK_LAUNCH(launch_unpack_head2seq(qrecv + off, pst, rld, hkv, c.c, c.Hkv, d, p, eb,
+                                               (uint8_t*)dv + (size_t)chunk * c.c * c.Hkv * d * eb, ctx->s_comm));
+      ctx->stats.kernel_launches += 2;
+    }
+    rec(ctx->ev_qo_send[part], ctx->s_comm);  // the part's send / receive buffers are free again
+  };
+  std::vector<char> dkv_started((size_t)u, 0);
+  int kstep = 0, nfinal = 0;
+  for (int64_t i = 0; i < u; ++i) {
+    const int qsl = (int)(i & 1);
+    HeadView qi, doi;
+    int64_t q_row0 = 0;
+    if (R.q(i)) {
+      if (p == 1) {
+        qi = {ctx->saved_q, c.S, hq, 0};
+        doi = {do_h, do_rows, do_heads, do_head0};
+        q_row0 = i * C;
+      } else {
+        qi = {res_chunk(i), C, hcomb, 0};
+        doi = {dores + (size_t)R.qslot[(size_t)i] * C * 2 * hq * d * eb, C, 2 * hq, hq};
+      }
+    } else {
+      // B4 (once per outer iteration): fetch q_i, dO_i
+      wait(ctx->s_h2d, ctx->ev_q_free[qsl]);
+      wait(ctx->s_h2d, ctx->ev_doff[i]);
+      h2d(ctx, qs[qsl], ctx->host + hl.q(i), (size_t)C * row_q);
+      h2d(ctx, dos[qsl], ctx->host + hl.dO(i, u), (size_t)C * row_q);
+      rec(ctx->ev_q_filled[qsl], ctx->s_h2d);
+      wait(cs, ctx->ev_q_filled[qsl]);
+      qi = {qs[qsl], C, hq, 0};
+      doi = {dos[qsl], C, hq, 0};
+    }
+    float* dqi = dqs[qsl];
+    FPDT_CHECK_CUDA(cudaMemsetAsync(dqi, 0, (size_t)C * hq * d * 4, cs));
+    if (ns > 1) {  // the second stream starts after everything enqueued on the caller's stream so far
+      rec(ctx->ev_fork, cs);
+      wait(ctx->s_comp2, ctx->ev_fork);
+    }
+    int n = 0;  // pair index within this query chunk
+    for (int64_t j = 0; j <= i; ++j) {
+      if (!keep(i, j)) continue;
+      cudaStream_t st = streams[(n++) % ns];
+      const bool first = !dkv_started[(size_t)j], fin = (i == last_i[(size_t)j]);
+      HeadView kj, vj;
+      int64_t kv_row0 = 0;
+      float* acc = nullptr;
+      int sl = -1;
+      if (R.kv(j)) {
+        if (p == 1) {
+          kj = {ctx->saved_k, c.S, hkv, 0};
+          vj = {ctx->saved_v, c.S, hkv, 0};
+          kv_row0 = j * C;
+        } else {
+          kj = {res_chunk(j), C, hcomb, hq};
+          vj = {res_chunk(j), C, hcomb, hq + hkv};
+        }
+        acc = dkvres + (size_t)j * dkv_elems;
+      } else {
+        // B3 per pair: kv_j and (after its first pair) the dK_j/dV_j partial
+        sl = (kstep++) % nslots;
+        wait(ctx->s_h2d, ctx->ev_qo_free[sl]);
+        wait(ctx->s_h2d, ctx->ev_off[j]);
+        h2d(ctx, kvs[sl], ctx->host + hl.kv(j, u), (size_t)C * row_kv2);
+        if (!first) {
+          wait(ctx->s_h2d, ctx->ev_dkvoff[j]);
+          h2d(ctx, dkvs[sl], ctx->host_dkv + (size_t)j * dkv_bytes, dkv_bytes);
+        }
+        rec(ctx->ev_qo_filled[sl], ctx->s_h2d);
+        wait(st, ctx->ev_qo_filled[sl]);
+        kj = {kvs[sl], C, 2 * hkv, 0};
+        vj = {kvs[sl], C, 2 * hkv, hkv};
+        acc = dkvs[sl];
+      }
+      BwdArgs a;
+      a.q = qi;
+      a.dout = doi;
+      a.k = kj;
+      a.v = vj;
+      a.q_row0 = q_row0;
+      a.kv_row0 = kv_row0;
+      a.n_q_rows = (int)C;
+      a.n_kv_rows = (int)C;
+      a.q_pos0 = i * C;
+      a.kv_pos0 = j * C;
+      a.causal = 1;
+      a.hq = hq;
+      a.G = c.G;
+      a.scale = c.scale;
+      a.scale_log2 = sl2;
+      a.lse2 = lse_save + i * C;
+      a.Dstat = Dh + i * C;
+      a.stat_ld = c.S;
+      a.dq_acc = dqi;  // head-major [hq][C][d]
+      a.dq_head_stride = C * d;
+      a.dk_acc = acc;
+      a.dv_acc = acc + (size_t)C * hkv * d;
+      a.kv_acc_init = first;
+      a.kv_final = fin;
+      int part = 0;
+      if (p == 1) {
+        a.dk_out = (uint8_t*)dk + (size_t)j * C * c.Hkv * d * eb;
+        a.dv_out = (uint8_t*)dv + (size_t)j * C * c.Hkv * d * eb;
+        a.kv_out_ld = (int64_t)c.Hkv * d;
+      } else {
+        part = fin ? 1 + (nfinal++ & 1) : 0;
+        uint8_t* kvsend = qsend + (size_t)C * row_q + (size_t)(part ? part - 1 : 0) * kvpart;
+        if (fin) wait(st, ctx->ev_qo_send[part]);
+        a.dk_out = kvsend;
+        a.dv_out = kvsend + (size_t)hkv * d * eb;
+        a.kv_out_ld = (int64_t)2 * hkv * d;
+      }
+      a.kv_out_head0 = 0;
+      launch_bwd(ctx, c, a, st);
+      dkv_started[(size_t)j] = 1;
+      if (sl >= 0) {
+        if (!fin) {
+          // B6 (Q-outer): the dK_j/dV_j partial goes back to the host store
+          rec(ctx->ev_qo_done[sl], st);
+          wait(ctx->s_d2h, ctx->ev_qo_done[sl]);
+          d2h(ctx, ctx->host_dkv + (size_t)j * dkv_bytes, dkvs[sl], dkv_bytes);
+          rec(ctx->ev_dkvoff[j], ctx->s_d2h);
+          rec(ctx->ev_qo_free[sl], ctx->s_d2h);
+        } else {
+          rec(ctx->ev_qo_free[sl], st);
+        }
+      }
+      if (fin && p > 1) send_back(st, part, j);
+    }
+    if (ns > 1) {  // join: dq_i is complete when both streams' pairs are
+      rec(ctx->ev_join, ctx->s_comp2);
+      wait(cs, ctx->ev_join);
+    }
+    // dq_i is final after its last key chunk
+    if (p > 1) wait(cs, ctx->ev_qo_send[0]);
+    FPDT_CHECK_LAUNCH(launch_convert_out(dqi, C, hq, d, C * d, 1.f,
+                                         p == 1 ? (uint8_t*)dq + (size_t)i * C * c.Hq * d * eb : qsend, c.dtype,
+                                         p == 1 ? (int64_t)c.Hq * d : (int64_t)hq * d, 0, cs));
+    ctx->stats.kernel_launches++;
+    if (p > 1) send_back(cs, 0, i);
+    if (!R.q(i)) rec(ctx->ev_q_free[qsl], cs);
+  }
+  if (p > 1) {
+    rec(ctx->ev_comm_done, ctx->s_comm);
+    wait(cs, ctx->ev_comm_done);
+  }
+}
+
 void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, void* dq, void* dk, void* dv,
               cudaStream_t cs) {
   const int64_t C = c.C, u = c.u;
@@ -718,6 +1011,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   };
 
   if (!c.offload) {
+    ctx->stats.bwd_order = FPDT_BWD_KV_OUTER;
     // resident: one launch per outer j over the query range [jC, S)
     float* dq_dev = (float*)dev(ctx, B_DQDEV, (size_t)c.S * hq * d * 4);
     FPDT_CHECK_CUDA(cudaMemsetAsync(dq_dev, 0, (size_t)c.S * hq * d * 4, cs));
@@ -762,6 +1056,17 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       send_back(j);
     }
   } else {
+    const std::vector<uint8_t>& plan = ctx->saved_plan;
+    auto keep = [&](int64_t i, int64_t j) { return i == j || plan.empty() || plan[(size_t)(i * u + j)] != 0; };
+    int order = ctx->bwd_order;
+    if (order == FPDT_BWD_AUTO)
+      order = bwd_host_bytes(FPDT_BWD_Q_OUTER, c, R.rkv, R.rq, keep) < bwd_host_bytes(FPDT_BWD_KV_OUTER, c, R.rkv, R.rq, keep)
+                  ? FPDT_BWD_Q_OUTER
+                  : FPDT_BWD_KV_OUTER;
+    ctx->stats.bwd_order = order;
+    if (order == FPDT_BWD_Q_OUTER) {
+      backward_q_outer(ctx, c, R, keep, do_h, do_rows, do_heads, do_head0, dores, dq, dk, dv, cs);
+    } else {
     uint8_t* kvs[2] = {(uint8_t*)dev(ctx, B_KVSLOT0, (size_t)C * row_kv2), (uint8_t*)dev(ctx, B_KVSLOT1, (size_t)C * row_kv2)};
     uint8_t* qs[2] = {(uint8_t*)dev(ctx, B_QSLOT0, (size_t)C * row_q), (uint8_t*)dev(ctx, B_QSLOT1, (size_t)C * row_q)};
     uint8_t* dos[2] = {(uint8_t*)dev(ctx, B_DOSLOT0, (size_t)C * row_q), (uint8_t*)dev(ctx, B_DOSLOT1, (size_t)C * row_q)};
@@ -771,8 +1076,6 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       rec(ctx->ev_q_free[b], cs);
     }
     int step = 0;
-    const std::vector<uint8_t>& plan = ctx->saved_plan;
-    auto keep = [&](int64_t i, int64_t j) { return i == j || plan.empty() || plan[(size_t)(i * u + j)] != 0; };
     std::vector<char> dq_started((size_t)u, 0);  // chunk i's dq partial already holds contributions (host store)
     for (int64_t j = 0; j < u; ++j) {
       const int ks = (int)(j & 1);
@@ -882,6 +1185,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       send_back(j);  // dk_j, dv_j are final after the last inner iteration
       rec(ctx->ev_kv_free[ks], cs);
     }
+    }
   }
   rec(ctx->ev_d2h_done, ctx->s_d2h);
   wait(cs, ctx->ev_d2h_done);
@@ -940,6 +1244,14 @@ fpdt_ctx* create_ctx(int world_size, int rank, const unsigned char* nccl_id, fpd
     FPDT_CHECK_CUDA(cudaStreamCreateWithPriority(&ctx->s_comm, cudaStreamNonBlocking, hi));
     FPDT_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->s_h2d, cudaStreamNonBlocking));
     FPDT_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
+    FPDT_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->s_comp2, cudaStreamNonBlocking));
+    if (const char* e = getenv("FPDT_BWD_QO_STREAMS")) ctx->qo_streams = atoi(e) == 1 ? 1 : 2;
+    for (int b = 0; b < 4; ++b)
+      for (cudaEvent_t* e : {&ctx->ev_qo_free[b], &ctx->ev_qo_filled[b], &ctx->ev_qo_done[b]})
+        FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
+    for (int b = 0; b < 3; ++b) FPDT_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->ev_qo_send[b], cudaEventDisableTiming));
+    FPDT_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
+    FPDT_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     cudaEvent_t* evs[] = {&ctx->ev_enter, &ctx->ev_o_ready, &ctx->ev_comm_done, &ctx->ev_d2h_done, &ctx->ev_h2d_done,
                           &ctx->ev_tmp};
     for (auto e : evs) FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
@@ -1011,13 +1323,15 @@ int fpdt_ctx_destroy(fpdt_ctx* ctx) {
     for (auto& b : ctx->bufs)
       if (b.ptr) cudaFree(b.ptr);
     if (ctx->host) cudaFreeHost(ctx->host);
-    for (auto v : {&ctx->ev_off, &ctx->ev_doff, &ctx->ev_dqoff, &ctx->ev_a2a})
+    if (ctx->host_dkv) cudaFreeHost(ctx->host_dkv);
+    for (auto v : {&ctx->ev_off, &ctx->ev_doff, &ctx->ev_dqoff, &ctx->ev_dkvoff, &ctx->ev_a2a})
       for (auto e : *v) cudaEventDestroy(e);
     for (auto& pr : ctx->t_fwd) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
     for (auto& pr : ctx->t_bwd) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
     cudaStreamDestroy(ctx->s_comm);
     cudaStreamDestroy(ctx->s_h2d);
     cudaStreamDestroy(ctx->s_d2h);
+    cudaStreamDestroy(ctx->s_comp2);
   });
   delete ctx;
   return rc;
@@ -1082,6 +1396,13 @@ int fpdt_set_residency(fpdt_ctx* ctx, int64_t kv_chunks, int64_t q_chunks) {
     if (!ctx || kv_chunks < 0 || q_chunks < 0) fail(FPDT_ERR_ARG, "bad residency arguments");
     ctx->res_kv = kv_chunks;
     ctx->res_q = q_chunks;
+  });
+}
+
+int fpdt_set_bwd_order(fpdt_ctx* ctx, int order) {
+  return run([&] {
+    if (!ctx || order < FPDT_BWD_KV_OUTER || order > FPDT_BWD_AUTO) fail(FPDT_ERR_ARG, "bad backward order");
+    ctx->bwd_order = order;
   });
 }
 

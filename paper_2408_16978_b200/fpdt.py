@@ -14,6 +14,7 @@ from ._lib import c_float, c_int, c_int64, c_void_p
 FPDT_OK, FPDT_ERR_ARG, FPDT_ERR_DIVISIBILITY, FPDT_ERR_UNSUPPORTED, FPDT_ERR_HOST_OOM, FPDT_ERR_DEVICE_OOM, \
     FPDT_ERR_STATE, FPDT_ERR_CUDA, FPDT_ERR_NCCL = range(9)
 FPDT_BF16, FPDT_FP32 = 0, 1
+FPDT_BWD_KV_OUTER, FPDT_BWD_Q_OUTER, FPDT_BWD_AUTO = 0, 1, 2
 STATUS_NAMES = {0: "FPDT_OK", 1: "FPDT_ERR_ARG", 2: "FPDT_ERR_DIVISIBILITY", 3: "FPDT_ERR_UNSUPPORTED",
                 4: "FPDT_ERR_HOST_OOM", 5: "FPDT_ERR_DEVICE_OOM", 6: "FPDT_ERR_STATE", 7: "FPDT_ERR_CUDA",
                 8: "FPDT_ERR_NCCL"}
@@ -23,6 +24,7 @@ EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_a
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair", "fpdt_group_create",
             "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity", "fpdt_set_residency",
+            "fpdt_set_bwd_order",
             "fpdt_selftest_softmax", "fpdt_selftest_reduce")
 
 
@@ -35,7 +37,8 @@ class FpdtError(RuntimeError):
 class Stats(ctypes.Structure):
     _fields_ = [("bytes_h2d", c_int64), ("bytes_d2h", c_int64), ("bytes_a2a", c_int64),
                 ("kernel_launches", c_int64), ("attn_launches", c_int64), ("fetch_slots_highwater", c_int64),
-                ("host_arena_bytes", c_int64), ("device_bytes", c_int64)]
+                ("host_arena_bytes", c_int64), ("device_bytes", c_int64), ("bwd_order", c_int64),
+                ("host_dkv_bytes", c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -69,6 +72,8 @@ def _declare(lib):
     lib.fpdt_set_sparsity.restype = c_int
     lib.fpdt_set_residency.argtypes = [P, c_int64, c_int64]
     lib.fpdt_set_residency.restype = c_int
+    lib.fpdt_set_bwd_order.argtypes = [P, c_int]
+    lib.fpdt_set_bwd_order.restype = c_int
     lib.fpdt_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
     lib.fpdt_get_stats.restype = c_int
     lib.fpdt_set_kernel_timing.argtypes = [P, c_int]
@@ -179,6 +184,12 @@ class FPDTContext:
         """HBM residency budget for the following forward calls (offload = 1): key/value chunks i < kv_chunks and
         query-side chunks i >= u - q_chunks stay in device memory (include/fpdt.h)."""
         _check(lib().fpdt_set_residency(self.handle, int(kv_chunks), int(q_chunks)))
+
+    def set_bwd_order(self, order: int):
+        """Backward loop order for the following backward calls: FPDT_BWD_KV_OUTER (the paper's), FPDT_BWD_Q_OUTER
+        (GQA-aware: the dK/dV partials round-trip the host instead of the dq partials) or FPDT_BWD_AUTO
+        (include/fpdt.h)."""
+        _check(lib().fpdt_set_bwd_order(self.handle, int(order)))
 
     def set_kernel_timing(self, enable: bool):
         _check(lib().fpdt_set_kernel_timing(self.handle, int(enable)))

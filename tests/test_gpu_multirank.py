@@ -16,7 +16,8 @@ from fpdt_testlib import TOL, oracle_full, rel_err
 pytestmark = pytest.mark.gpu
 
 
-def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None, residency=None) -> dict:
+def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None, residency=None, bwd_order=None,
+              stats=None) -> dict:
     """Shard the global inputs x by the rank-ordinal contract, run fwd+bwd on p local ranks, unshard."""
     from paper_2408_16978_b200 import fpdt
     S, Hq, d = x["q"].shape
@@ -45,11 +46,15 @@ def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None, resi
                 ctx.set_sparsity(keep)
             if residency is not None:
                 ctx.set_residency(*residency)
+            if bwd_order is not None:
+                ctx.set_bwd_order(bwd_order)
             fpdt.fpdt_attn_fwd(ctx, q, k, v, o, lse, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
             fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
             stream.synchronize()
             for n, t in (("o", o), ("lse", lse), ("dq", dq), ("dk", dk), ("dv", dv)):
                 out[n][rows[r]] = t.float().cpu().numpy()
+            if stats is not None:
+                stats[r] = ctx.stats()
             ctx.close()
         except Exception as e:  # surfaced in the main thread
             errors.append((r, e))

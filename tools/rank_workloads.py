@@ -40,7 +40,7 @@ WORKLOADS = [
 ]
 
 
-def run_one(name, text, S, Hq, Hkv, d, p, C, steps, genlib):
+def run_one(name, text, S, Hq, Hkv, d, p, C, steps, genlib, bwd_order=0):
     hq, hkv = Hq // p, Hkv // p
     rec = {"config": name, "text": text, "S": S, "world_size_emulated": p, "heads_q_per_rank": hq,
            "heads_kv_per_rank": hkv, "head_dim": d, "chunk": C, "chunks": S // C, "offload": 1}
@@ -57,6 +57,7 @@ def run_one(name, text, S, Hq, Hkv, d, p, C, steps, genlib):
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     ctx = fpdt.FPDTContext()
     ctx.set_kernel_timing(True)
+    ctx.set_bwd_order(bwd_order)
     stream = torch.cuda.current_stream()
     times = []
     for s in range(steps):
@@ -87,7 +88,8 @@ def run_one(name, text, S, Hq, Hkv, d, p, C, steps, genlib):
                tokens_per_s_p_gpus=S / dt, h2d_bytes=h2d, d2h_bytes=d2h, h2d_GBps=h2d / dt / 1e9,
                d2h_GBps=d2h / dt / 1e9, device_bytes_caller=sum(t.numel() * 2 for t in (q, k, v, do, o, dq, dk, dv)),
                device_bytes_library=st["device_bytes"], host_pinned_bytes=st["host_arena_bytes"],
-               first_step_s=times[0][0])
+               first_step_s=times[0][0], bwd_order=["kv_outer", "q_outer"][st["bwd_order"]],
+               host_dkv_pinned_bytes=st["host_dkv_bytes"])
     ctx.close()
     del q, k, v, do, o, dq, dk, dv
     torch.cuda.empty_cache()
@@ -99,7 +101,10 @@ def main():
     ap.add_argument("--only", nargs="+", default=None)
     ap.add_argument("--steps", type=int, default=1)
     ap.add_argument("--chunks", type=int, nargs="+", default=None, help="restrict the chunk sizes (in K tokens)")
+    ap.add_argument("--bwd-order", default="kv", choices=["kv", "q", "auto"],
+                    help="backward loop order (fpdt_set_bwd_order)")
     args = ap.parse_args()
+    order = {"kv": fpdt.FPDT_BWD_KV_OUTER, "q": fpdt.FPDT_BWD_Q_OUTER, "auto": fpdt.FPDT_BWD_AUTO}[args.bwd_order]
     torch.cuda.set_device(0)
     genlib = _lib.load_generator()
     for name, text, S, Hq, Hkv, d, p, chunks in WORKLOADS:
@@ -109,7 +114,7 @@ def main():
             if args.chunks and C // K not in args.chunks:
                 continue
             try:
-                rec = run_one(name, text, S, Hq, Hkv, d, p, C, args.steps, genlib)
+                rec = run_one(name, text, S, Hq, Hkv, d, p, C, args.steps, genlib, order)
             except Exception as e:  # report and continue with the next workload
                 rec = {"config": name, "chunk": C, "ok": False, "error": f"{type(e).__name__}: {str(e)[:200]}"}
                 torch.cuda.empty_cache()
