@@ -698,7 +698,8 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
   // two at a time on two compute streams: the second kernel's CTAs fill the SMs the first one's last wave leaves
   // idle (a full pair is 512 CTAs, 3.5 waves, when one kv head per rank is left: configs[4] at p = 8).
   // Key/value slots: two per stream (fetch of the next pair while the current one computes).
-  const int ns = ctx->qo_streams, nslots = 2 * ns;
+  // (bf16 only: the fp32 validation kernels add dQ with a plain read-modify-write, one owner per launch)
+  const int ns = c.dtype == FPDT_BF16 ? ctx->qo_streams : 1, nslots = 2 * ns;
   cudaStream_t streams[2] = {cs, ctx->s_comp2};
   static const int kv_ids[4] = {B_KVSLOT0, B_KVSLOT1, B_KVSLOT2, B_KVSLOT3};
   static const int dkv_ids[4] = {B_DKVSLOT0, B_DKVSLOT1, B_DKVSLOT2, B_DKVSLOT3};

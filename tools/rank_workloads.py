@@ -88,7 +88,10 @@ def run_one(name, text, S, Hq, Hkv, d, p, C, steps, genlib, bwd_order=0):
                tokens_per_s_p_gpus=S / dt, h2d_bytes=h2d, d2h_bytes=d2h, h2d_GBps=h2d / dt / 1e9,
                d2h_GBps=d2h / dt / 1e9, device_bytes_caller=sum(t.numel() * 2 for t in (q, k, v, do, o, dq, dk, dv)),
                device_bytes_library=st["device_bytes"], host_pinned_bytes=st["host_arena_bytes"],
-               first_step_s=times[0][0], bwd_order=["kv_outer", "q_outer"][st["bwd_order"]],
+               first_step_s=times[0][0],
+               # Q-outer runs two pair kernels at a time on two streams: the summed per-launch times then overlap
+               # and the *_kernel_tflops fields undercount; step_s is the measure
+               concurrent_pairs=st["bwd_order"] == 1 and os.environ.get("FPDT_BWD_QO_STREAMS", "2") != "1", bwd_order=["kv_outer", "q_outer"][st["bwd_order"]],
                host_dkv_pinned_bytes=st["host_dkv_bytes"])
     ctx.close()
     del q, k, v, do, o, dq, dk, dv
