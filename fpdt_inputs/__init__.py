@@ -34,8 +34,8 @@ from __future__ import annotations
 
 import numpy as np
 
-Q, K, V, DO = 0, 1, 2, 3
-TENSOR_IDS = {"q": Q, "k": K, "v": V, "do": DO}
+Q, K, V, DO, X, W = 0, 1, 2, 3, 4, 5
+TENSOR_IDS = {"q": Q, "k": K, "v": V, "do": DO, "x": X, "w": W}
 DISTRIBUTIONS = ("normal", "peaky", "drift", "sink", "same", "class")
 DIST_IDS = {name: i for i, name in enumerate(DISTRIBUTIONS)}
 N_CLASSES = 4
@@ -162,3 +162,21 @@ def sparsity_plan(n_chunks: int, rho: float, seed: int = 0) -> np.ndarray:
         for idx in rng.permutation(len(off))[:n_drop]:
             keep[off[idx]] = False
     return keep
+
+
+def make_block_inputs(dist: str, seed: int, seq_len: int, hidden: int, n_q_heads: int, n_kv_heads: int,
+                      head_dim: int, tokens: np.ndarray | None = None) -> dict:
+    """Inputs of the attention block with the fused QKV projection: the hidden state
+    x [T, hidden] (rows = global tokens), the projection weight w [hidden, (Hq + 2 Hkv) * head_dim] (columns: q heads,
+    then k heads, then v heads, head_dim fastest) scaled by 2^-round(log2(sqrt(hidden))) (exact in bf16) so the
+    projected q, k, v have about unit variance, and the upstream gradient do [T, Hq, head_dim] of the attention
+    output.  `dist` shapes x only through the base generator (normal); the attention-level distributions apply to
+    q, k, v, which are now computed."""
+    if tokens is None:
+        tokens = np.arange(seq_len, dtype=np.int64)
+    n_cols = (n_q_heads + 2 * n_kv_heads) * head_dim
+    x = generate("x", "normal", seed, tokens, 1, hidden, seq_len).reshape(len(tokens), hidden)
+    w = generate("w", "normal", seed, np.arange(hidden), 1, n_cols, seq_len).reshape(hidden, n_cols)
+    w = (w * np.float32(2.0 ** -round(np.log2(np.sqrt(hidden))))).astype(np.float32)
+    do = generate("do", dist, seed, tokens, n_q_heads, head_dim, seq_len)
+    return {"x": x, "w": w, "do": do}

@@ -1,0 +1,54 @@
+"""Attention block with the chunked QKV projection fused in front, fp64.
+
+TEST INFRASTRUCTURE ONLY (see oracle/__init__.py).
+
+PAPER.md P:L206: "For the first QKV projection, since tokens are processed elementwise, we directly slice the local
+sequence tensor into u chunks ... T_i is projected to query q_i, key k_i, and value v_i.  Then, we perform the
+Alltoall"; after dq_0, dk_0, dv_0 are final and all-to-all'd back, they "are used to compute the gradient of
+the input hidden state dc_0".  The projection is token-wise, so chunking does not change it; the plain definition
+over the whole sequence is the oracle:
+
+    [q | k | v] = x W                        x [S, hidden], W [hidden, (Hq + 2 Hkv) d] (columns q heads, k, v)
+    O, lse      = attention(q, k, v)         (oracle/attention.py, §8(c) c.1)
+    dq, dk, dv  = attention backward for dO
+    dqkv        = [dq | dk | dv]             [S, (Hq + 2 Hkv) d]
+    dx          = dqkv W^T                   (the hidden-state gradient, "dc" in P:L365)
+    dW          = x^T dqkv                   (summed over every token of the sequence shard)
+
+(no bias: the paper states none).  Pinned in tests/test_oracle_block.py by central finite differences of the
+scalar loss L = <dO, O> in x and W, and by reduction to the attention oracle when W selects x's columns.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+from . import attention
+
+
+def split_qkv(qkv: np.ndarray, n_q_heads: int, n_kv_heads: int, head_dim: int):
+    S = qkv.shape[0]
+    nq, nk = n_q_heads * head_dim, n_kv_heads * head_dim
+    q = qkv[:, :nq].reshape(S, n_q_heads, head_dim)
+    k = qkv[:, nq:nq + nk].reshape(S, n_kv_heads, head_dim)
+    v = qkv[:, nq + nk:].reshape(S, n_kv_heads, head_dim)
+    return q, k, v
+
+
+def block_forward(x, w, n_q_heads: int, n_kv_heads: int, head_dim: int, scale: float | None = None):
+    """O [S, Hq, d], lse [S, Hq] of attention over the projected q, k, v (causal)."""
+    x = np.asarray(x, np.float64)
+    w = np.asarray(w, np.float64)
+    q, k, v = split_qkv(x @ w, n_q_heads, n_kv_heads, head_dim)
+    return attention.attention_forward(q, k, v, scale)
+
+
+def block_backward(x, w, do, n_q_heads: int, n_kv_heads: int, head_dim: int, scale: float | None = None):
+    """dx [S, hidden], dW [hidden, (Hq + 2 Hkv) d] for upstream dO of the attention output."""
+    x = np.asarray(x, np.float64)
+    w = np.asarray(w, np.float64)
+    S = x.shape[0]
+    q, k, v = split_qkv(x @ w, n_q_heads, n_kv_heads, head_dim)
+    o, lse = attention.attention_forward(q, k, v, scale)
+    dq, dk, dv = attention.attention_backward(q, k, v, o, lse, np.asarray(do, np.float64), scale)
+    dqkv = np.concatenate([dq.reshape(S, -1), dk.reshape(S, -1), dv.reshape(S, -1)], axis=1)
+    return dqkv @ w.T, x.T @ dqkv
