@@ -115,6 +115,28 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
                   int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
                   int dtype, int offload, float softmax_scale, void* stream);
 
+/* Attention block with the chunked QKV projection fused in front.  PAPER.md P:L206: "we
+ * directly slice the local sequence tensor into u chunks ... T_i is projected to query q_i, key k_i, and value v_i.
+ * Then, we perform the Alltoall"; the final dq_j, dk_j, dv_j, all-to-all'd back, "are used to compute the
+ * gradient of the input hidden state".  Per chunk the projection is a plain GEMM (cuBLAS, fp32 accumulation; fp32
+ * mode without TF32) on the comm stream just before the chunk's all-to-all, so the full-sequence q, k, v never exist;
+ * in the backward each chunk's projection gradient runs as soon as its dq, dk, dv are final (the paper's KV-outer
+ * order; fpdt_set_bwd_order is ignored here).
+ *   x      [s_local][hidden]                         hidden state, rank-ordinal rows (as q of fpdt_attn_fwd)
+ *   w_qkv  [hidden][(n_q_heads + 2 n_kv_heads) * head_dim]  row-major projection weight; columns are the q heads,
+ *          then the k heads, then the v heads, head_dim fastest: [q | k | v] = x w_qkv (no bias)
+ *   o, lse as fpdt_attn_fwd.  dx [s_local][hidden] (output, overwritten), dw_qkv fp32 [hidden][(Hq + 2 Hkv) d]
+ *   (output, overwritten: the sum over this rank's rows of x^T dqkv; a data-parallel caller all-reduces it).
+ * x, w_qkv must be unchanged between the two calls.  All pointers are device pointers; dtype FPDT_BF16 (x, w, dx
+ * bf16) or FPDT_FP32.  Errors: as fpdt_attn_fwd/bwd; hidden * elem bytes % 16 != 0: FPDT_ERR_ARG; offload = 0 or a
+ * residency budget: FPDT_ERR_UNSUPPORTED; fpdt_attn_bwd after fpdt_block_fwd (or the reverse): FPDT_ERR_STATE. */
+int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, void* o, float* lse, int64_t s_local, int hidden,
+                   int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
+                   int dtype, int offload, float softmax_scale, void* stream);
+int fpdt_block_bwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* o, const void* dout, void* dx,
+                   float* dw_qkv, int64_t s_local, int hidden, int n_q_heads, int n_kv_heads, int head_dim, int causal,
+                   int64_t chunk_size, int world_size, int dtype, int offload, float softmax_scale, void* stream);
+
 /* Block-sparse attention (§5.6, Table "MFU at different attention sparsity": "only part of the tokens in
  * key and value will be fetched from the host memory, while the query will always be the entire sequence").
  *   keep: host array [n_chunks][n_chunks], row m = query chunk, column i = key chunk (GLOBAL chunk indices, chunk

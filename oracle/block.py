@@ -15,7 +15,14 @@ over the whole sequence is the oracle:
     dx          = dqkv W^T                   (the hidden-state gradient, "dc" in P:L365)
     dW          = x^T dqkv                   (summed over every token of the sequence shard)
 
-(no bias: the paper states none).  Pinned in tests/test_oracle_block.py by central finite differences of the
+(no bias: the paper states none).
+
+bf16 mode (reading R27 in DESIGN.md; the paper states no precision, R15): in a bf16 block the projected q, k, v and
+the attention gradients dq, dk, dv that enter the projection backward are bf16 tensors, as every activation of a
+bf16 layer is.  `bf16_intermediates=True` rounds them (RNE, via fp32) at exactly those two points; every product
+and sum stays fp64.
+
+Pinned in tests/test_oracle_block.py by central finite differences of the
 scalar loss L = <dO, O> in x and W, and by reduction to the attention oracle when W selects x's columns.
 """
 from __future__ import annotations
@@ -23,6 +30,13 @@ from __future__ import annotations
 import numpy as np
 
 from . import attention
+
+
+def _bf16(x: np.ndarray) -> np.ndarray:
+    """Round to the nearest bf16 (ties to even) through fp32, returned as fp64."""
+    u = np.ascontiguousarray(np.asarray(x, np.float64).astype(np.float32)).view(np.uint32)
+    r = (u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) & np.uint32(0xFFFF0000)
+    return r.view(np.float32).astype(np.float64)
 
 
 def split_qkv(qkv: np.ndarray, n_q_heads: int, n_kv_heads: int, head_dim: int):
@@ -34,21 +48,29 @@ def split_qkv(qkv: np.ndarray, n_q_heads: int, n_kv_heads: int, head_dim: int):
     return q, k, v
 
 
-def block_forward(x, w, n_q_heads: int, n_kv_heads: int, head_dim: int, scale: float | None = None):
+def _project(x, w, bf16_intermediates: bool):
+    qkv = np.asarray(x, np.float64) @ np.asarray(w, np.float64)
+    return _bf16(qkv) if bf16_intermediates else qkv
+
+
+def block_forward(x, w, n_q_heads: int, n_kv_heads: int, head_dim: int, scale: float | None = None,
+                  bf16_intermediates: bool = False):
     """O [S, Hq, d], lse [S, Hq] of attention over the projected q, k, v (causal)."""
-    x = np.asarray(x, np.float64)
-    w = np.asarray(w, np.float64)
-    q, k, v = split_qkv(x @ w, n_q_heads, n_kv_heads, head_dim)
+    q, k, v = split_qkv(_project(x, w, bf16_intermediates), n_q_heads, n_kv_heads, head_dim)
     return attention.attention_forward(q, k, v, scale)
 
 
-def block_backward(x, w, do, n_q_heads: int, n_kv_heads: int, head_dim: int, scale: float | None = None):
-    """dx [S, hidden], dW [hidden, (Hq + 2 Hkv) d] for upstream dO of the attention output."""
+def block_backward(x, w, do, n_q_heads: int, n_kv_heads: int, head_dim: int, scale: float | None = None,
+                   bf16_intermediates: bool = False, keep=None, chunk: int = 0):
+    """dx [S, hidden], dW [hidden, (Hq + 2 Hkv) d] for upstream dO of the attention output (and O, lse)."""
     x = np.asarray(x, np.float64)
     w = np.asarray(w, np.float64)
     S = x.shape[0]
-    q, k, v = split_qkv(x @ w, n_q_heads, n_kv_heads, head_dim)
-    o, lse = attention.attention_forward(q, k, v, scale)
-    dq, dk, dv = attention.attention_backward(q, k, v, o, lse, np.asarray(do, np.float64), scale)
+    q, k, v = split_qkv(_project(x, w, bf16_intermediates), n_q_heads, n_kv_heads, head_dim)
+    o, lse = attention.attention_forward(q, k, v, scale, keep=keep, chunk=chunk)
+    dq, dk, dv = attention.attention_backward(q, k, v, o, lse, np.asarray(do, np.float64), scale, keep=keep,
+                                              chunk=chunk)
     dqkv = np.concatenate([dq.reshape(S, -1), dk.reshape(S, -1), dv.reshape(S, -1)], axis=1)
+    if bf16_intermediates:
+        dqkv = _bf16(dqkv)
     return dqkv @ w.T, x.T @ dqkv

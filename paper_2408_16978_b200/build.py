@@ -33,6 +33,19 @@ def _nccl_dirs():
     raise RuntimeError("NCCL headers not found (expected the torch-bundled nvidia-nccl wheel)")
 
 
+def _cublas_lib():
+    """The torch-bundled libcublas.so.12 (the copy torch itself loads, so the process holds one cuBLAS); the
+    fused QKV projection GEMMs of fpdt_block_fwd/bwd call it.  Headers come from the CUDA toolkit."""
+    import importlib.util
+    spec = importlib.util.find_spec("nvidia")
+    roots = list(spec.submodule_search_locations) if spec and spec.submodule_search_locations else []
+    for r in roots:
+        lib = os.path.join(r, "cublas", "lib")
+        if os.path.exists(os.path.join(lib, "libcublas.so.12")):
+            return lib
+    return "/usr/local/cuda/lib64"
+
+
 def _stale(target, sources):
     if not os.path.exists(target):
         return True
@@ -71,7 +84,8 @@ def build_product(force: bool = False) -> str:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed")
     _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", out] + objs +
-         ["-L", nccl_lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={nccl_lib}", "-lpthread"])
+         ["-L", nccl_lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={nccl_lib}", "-L", _cublas_lib(), "-l:libcublas.so.12",
+          f"-Xlinker=-rpath={_cublas_lib()}", "-lpthread"])
     return out
 
 

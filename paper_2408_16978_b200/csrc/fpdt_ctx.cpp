@@ -15,6 +15,7 @@
 // Streams: compute (= the caller's stream), comm, h2d, d2h; every cross-stream dependency is an event.
 #include <cuda_runtime.h>
 #include <nccl.h>
+#include <cublas_v2.h>
 
 #include <cmath>
 #include <condition_variable>
@@ -67,6 +68,15 @@ struct Fail {
     }                                                                                               \
   } while (0)
 
+#define FPDT_CHECK_CUBLAS(x)                                                                        \
+  do {                                                                                              \
+    cublasStatus_t r_ = (x);                                                                        \
+    if (r_ != CUBLAS_STATUS_SUCCESS) {                                                              \
+      g_last_error = std::string(#x) + ": cublas status " + std::to_string((int)r_);                \
+      throw Fail{FPDT_ERR_CUDA};                                                                    \
+    }                                                                                               \
+  } while (0)
+
 [[noreturn]] void fail(int code, const std::string& msg) {
   g_last_error = msg;
   throw Fail{code};
@@ -87,6 +97,16 @@ struct Config {
   }
 };
 
+// Fused QKV projection of fpdt_block_fwd / fpdt_block_bwd; nullptr = the
+// attention-only calls.  Row-major: x, dx [s_local][hidden]; w [hidden][(Hq + 2 Hkv) * d] (q heads, k, v); dw fp32.
+struct Proj {
+  const void* x = nullptr;
+  const void* w = nullptr;
+  void* dx = nullptr;
+  float* dw = nullptr;
+  int hidden = 0;
+};
+
 struct DevBuf {
   void* ptr = nullptr;
   size_t bytes = 0;
@@ -96,7 +116,8 @@ enum BufId {
   B_OACC, B_LSEACC, B_LSESAVE, B_OHAT, B_KVSLOT0, B_KVSLOT1, B_A2A_SEND0, B_A2A_SEND1, B_A2A_RECV0, B_A2A_RECV1,
   B_STORE, B_D, B_DQDEV, B_QSLOT0, B_QSLOT1, B_DOSLOT0, B_DOSLOT1, B_DQSLOT0, B_DQSLOT1, B_DKACC, B_DVACC,
   B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_RESSTORE, B_DORES, B_DQRES, B_DKVSLOT0,
-  B_DKVSLOT1, B_DKVRES, B_KVSLOT2, B_KVSLOT3, B_DKVSLOT2, B_DKVSLOT3, B_QOSEND, B_QORECV, B_NUM
+  B_DKVSLOT1, B_DKVRES, B_KVSLOT2, B_KVSLOT3, B_DKVSLOT2, B_DKVSLOT3, B_QOSEND, B_QORECV, B_PROJ0, B_PROJ1,
+  B_PROJ2, B_NUM
 };
 
 }  // namespace
@@ -132,6 +153,7 @@ struct fpdt_ctx {
   cudaStream_t s_comm = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   // Q-outer backward: second compute stream (pairs of one query chunk run two at a time) and its slot events
   cudaStream_t s_comp2 = nullptr;
+  cublasHandle_t blas = nullptr;  // fused QKV projection GEMMs (created by the first block call)
   int qo_streams = 2;  // FPDT_BWD_QO_STREAMS (1 or 2)
   cudaEvent_t ev_qo_free[4] = {}, ev_qo_filled[4] = {}, ev_qo_done[4] = {}, ev_qo_send[3] = {}, ev_fork = nullptr,
               ev_join = nullptr;
@@ -149,6 +171,7 @@ struct fpdt_ctx {
   // saved state
   bool fwd_done = false;
   Config saved;
+  int saved_hidden = 0;  // > 0: the saved forward was fpdt_block_fwd with this hidden size
   // block-sparsity plan (fpdt_set_sparsity): keep[m*u + i] over (query chunk m, key chunk i); empty = dense.
   // The forward copies it into saved_plan; the backward of that forward uses the copy.
   std::vector<uint8_t> plan, saved_plan;
@@ -414,9 +437,53 @@ void launch_bwd(fpdt_ctx* ctx, const Config& c, const BwdArgs& a, cudaStream_t s
   ctx->stats.attn_launches++;
 }
 
+// ------------------------------------------------------------------------------------------ projection GEMMs
+// Plain library GEMMs (cuBLAS, fp32 accumulation; the fp32 mode uses pedantic FP32, no TF32) on row-major
+// operands, expressed as column-major products of the transposes.
+cublasHandle_t blas_on(fpdt_ctx* ctx, cudaStream_t s) {
+  if (!ctx->blas) FPDT_CHECK_CUBLAS(cublasCreate(&ctx->blas));
+  FPDT_CHECK_CUBLAS(cublasSetStream(ctx->blas, s));
+  return ctx->blas;
+}
+cudaDataType_t blas_type(int dtype) { return dtype == FPDT_BF16 ? CUDA_R_16BF : CUDA_R_32F; }
+cublasComputeType_t blas_compute(int dtype) {
+  return dtype == FPDT_BF16 ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC;
+}
+// Y[rows][n] (row stride ldy) = X[rows][k] (ldx) W[k][n] (ldw)       (forward projection)
+void gemm_xw(fpdt_ctx* ctx, int dtype, const void* X, int64_t ldx, const void* W, int64_t ldw, void* Y, int64_t ldy,
+             int64_t rows, int64_t k, int64_t n, cudaStream_t s) {
+  const float one = 1.f, zero = 0.f;
+  const cudaDataType_t t = blas_type(dtype);
+  FPDT_CHECK_CUBLAS(cublasGemmEx(blas_on(ctx, s), CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)rows, (int)k, &one, W, t,
+                                 (int)ldw, X, t, (int)ldx, &zero, Y, t, (int)ldy, blas_compute(dtype),
+                                 CUBLAS_GEMM_DEFAULT));
+  ctx->stats.kernel_launches++;
+}
+// dX[rows][k] (ldx) = dY[rows][n] (ldy) W^T                            (hidden-state gradient)
+void gemm_dx(fpdt_ctx* ctx, int dtype, const void* dY, int64_t ldy, const void* W, int64_t ldw, void* dX, int64_t ldx,
+             int64_t rows, int64_t k, int64_t n, cudaStream_t s) {
+  const float one = 1.f, zero = 0.f;
+  const cudaDataType_t t = blas_type(dtype);
+  FPDT_CHECK_CUBLAS(cublasGemmEx(blas_on(ctx, s), CUBLAS_OP_T, CUBLAS_OP_N, (int)k, (int)rows, (int)n, &one, W, t,
+                                 (int)ldw, dY, t, (int)ldy, &zero, dX, t, (int)ldx, blas_compute(dtype),
+                                 CUBLAS_GEMM_DEFAULT));
+  ctx->stats.kernel_launches++;
+}
+// dW[k][n] fp32 (= or +=) X[rows][k]^T dY[rows][n]                       (weight gradient, summed over chunks)
+void gemm_dw(fpdt_ctx* ctx, int dtype, const void* X, int64_t ldx, const void* dY, int64_t ldy, float* dW, int64_t rows,
+             int64_t k, int64_t n, bool accumulate, cudaStream_t s) {
+  const float one = 1.f, beta = accumulate ? 1.f : 0.f;
+  const cudaDataType_t t = blas_type(dtype);
+  FPDT_CHECK_CUBLAS(cublasGemmEx(blas_on(ctx, s), CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)k, (int)rows, &one, dY, t,
+                                 (int)ldy, X, t, (int)ldx, &beta, dW, CUDA_R_32F, (int)n,
+                                 dtype == FPDT_BF16 ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC,
+                                 CUBLAS_GEMM_DEFAULT));
+  ctx->stats.kernel_launches++;
+}
+
 // ------------------------------------------------------------------------------------------ forward
 void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const void* v, void* o, float* lse,
-             cudaStream_t cs) {
+             cudaStream_t cs, const Proj* pj = nullptr) {
   const int64_t C = c.C, u = c.u;
   const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
   const size_t row_q = (size_t)hq * d * eb, row_kv2 = (size_t)2 * hkv * d * eb;
@@ -451,6 +518,15 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       if (c.offload) a2a_recv[b] = (uint8_t*)dev(ctx, B_A2A_RECV0 + b, (size_t)C * hcomb * d * eb);
     }
   }
+  // fused projection (fpdt_block_fwd): chunk m of the hidden state is projected on the comm stream just before
+  // its all-to-all; at p = 1 the GEMM writes the combined head layout [C][Hq + 2Hkv][d] directly, at p > 1
+  // it writes the chunk's sequence rows [c][Hq + 2Hkv][d], which the pack kernels read with that row stride.
+  const bool proj = pj != nullptr, headbuf = p > 1 || proj;
+  const int64_t ntot = (int64_t)(c.Hq + 2 * c.Hkv) * d;
+  uint8_t* pbuf = nullptr;
+  if (proj && p == 1)
+    for (int b = 0; b < 2; ++b) a2a_recv[b] = (uint8_t*)dev(ctx, B_A2A_RECV0 + b, (size_t)C * hcomb * d * eb);
+  if (proj && p > 1) pbuf = (uint8_t*)dev(ctx, B_PROJ0, (size_t)c.c * ntot * eb);
   const Residency R = make_residency(u, c.offload ? ctx->saved_res_kv : 0, c.offload ? ctx->saved_res_q : 0);
   uint8_t* resstore = (p > 1 && R.n > 0) ? (uint8_t*)dev(ctx, B_RESSTORE, (size_t)R.n * C * hcomb * d * eb) : nullptr;
   auto res_chunk = [&](int64_t m) { return resstore + (size_t)R.slot[(size_t)m] * C * hcomb * d * eb; };
@@ -465,7 +541,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     rec(ctx->ev_recv_used_d[b], cs);
   }
   // p == 1 with offload: the head-layout chunk IS the caller's rows; offload all chunks up front
-  if (p == 1 && c.offload) {
+  if (p == 1 && c.offload && !proj) {
     for (int64_t m = 0; m < u; ++m) {
       if (!R.q(m)) d2h(ctx, ctx->host + hl.q(m), (const uint8_t*)q + (size_t)m * C * row_q, (size_t)C * row_q);
       if (!R.kv(m)) {
@@ -488,7 +564,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     // ---- views of the current chunk's q, k, v in the head layout
     HeadView qv, kv, vv;
     int64_t q_row0, kv_row0_cur;
-    if (p == 1) {
+    if (!headbuf) {
       qv = {q, c.S, hq, 0};
       kv = {k, c.S, hkv, 0};
       vv = {v, c.S, hkv, 0};
@@ -502,14 +578,29 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       wait(ctx->s_comm, ctx->ev_recv_used_c[b]);
       wait(ctx->s_comm, ctx->ev_recv_used_d[b]);
       const size_t per_peer = (size_t)c.c * hcomb * d;
-      FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)q + (size_t)m * c.c * c.Hq * d * eb, c.c, c.Hq, d, p, eb,
-                                             a2a_send[b], per_peer, (int64_t)hcomb * d, 0, ctx->s_comm));
-      FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)k + (size_t)m * c.c * c.Hkv * d * eb, c.c, c.Hkv, d, p,
-                                             eb, a2a_send[b], per_peer, (int64_t)hcomb * d, hq, ctx->s_comm));
-      FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)v + (size_t)m * c.c * c.Hkv * d * eb, c.c, c.Hkv, d, p,
-                                             eb, a2a_send[b], per_peer, (int64_t)hcomb * d, hq + hkv, ctx->s_comm));
-      ctx->stats.kernel_launches += 3;
-      alltoall(ctx, a2a_send[b], recv, per_peer, c.dtype);
+      const uint8_t *qm = (const uint8_t*)q + (size_t)m * c.c * c.Hq * d * eb,
+                    *km = (const uint8_t*)k + (size_t)m * c.c * c.Hkv * d * eb,
+                    *vm = (const uint8_t*)v + (size_t)m * c.c * c.Hkv * d * eb;
+      int64_t src_ld = 0;  // dense caller rows
+      if (proj) {
+        const uint8_t* xm = (const uint8_t*)pj->x + (size_t)m * c.c * pj->hidden * eb;
+        gemm_xw(ctx, c.dtype, xm, pj->hidden, pj->w, ntot, p == 1 ? recv : pbuf, ntot, c.c, pj->hidden, ntot,
+                ctx->s_comm);
+        qm = pbuf;
+        km = pbuf + (size_t)c.Hq * d * eb;
+        vm = pbuf + (size_t)(c.Hq + c.Hkv) * d * eb;
+        src_ld = ntot;
+      }
+      if (p > 1) {
+        FPDT_CHECK_LAUNCH(launch_pack_seq2head(qm, c.c, c.Hq, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d, 0,
+                                               ctx->s_comm, src_ld));
+        FPDT_CHECK_LAUNCH(launch_pack_seq2head(km, c.c, c.Hkv, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d, hq,
+                                               ctx->s_comm, src_ld));
+        FPDT_CHECK_LAUNCH(launch_pack_seq2head(vm, c.c, c.Hkv, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d,
+                                               hq + hkv, ctx->s_comm, src_ld));
+        ctx->stats.kernel_launches += 3;
+        alltoall(ctx, a2a_send[b], recv, per_peer, c.dtype);
+      }
       rec(ctx->ev_a2a[m], ctx->s_comm);
       if (c.offload) {
         // F5: offload q_m, kv_m from the receive buffer
@@ -572,7 +663,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       a.has_prev = 0;
       a.is_final = (last_kept < 0);
       launch_fwd(ctx, c, a, cs);
-      if (p > 1) rec(ctx->ev_recv_used_c[m & 1], cs);
+      if (headbuf) rec(ctx->ev_recv_used_c[m & 1], cs);
       // F7/F8: earlier chunks fetched from the host store, double-buffered
       for (int64_t i = 0; i < m; ++i) {
         if (!keep(m, i)) continue;
@@ -580,7 +671,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
         a.has_prev = 1;
         a.is_final = (i == last_kept);
         if (R.kv(i)) {  // resident key/value chunk: no fetch
-          if (p == 1) {
+          if (!headbuf) {
             a.k = {k, c.S, hkv, 0};
             a.v = {v, c.S, hkv, 0};
             a.kv_row0 = i * C;
@@ -888,7 +979,7 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
 }
 
 void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, void* dq, void* dk, void* dv,
-              cudaStream_t cs) {
+              cudaStream_t cs, const Proj* pj = nullptr) {
   const int64_t C = c.C, u = c.u;
   const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
   const int hcomb = hq + 2 * hkv;
@@ -968,10 +1059,31 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   uint8_t* bsend = p > 1 ? (uint8_t*)dev(ctx, B_BWD_SEND, (size_t)C * hcomb * d * eb) : nullptr;
   uint8_t* brecv = p > 1 ? (uint8_t*)dev(ctx, B_BWD_RECV, (size_t)C * hcomb * d * eb) : nullptr;
 
+  // fused projection (fpdt_block_bwd): chunk j's final dq, dk, dv land in a chunk buffer of sequence rows
+  // [c][Hq + 2Hkv][d] (double-buffered by j), from which the projection backward forms dx_j and adds x_j^T dqkv_j
+  // to dW as soon as the chunk is final ("dq_0, dk_0, dv_0 are used to compute the gradient of the input
+  // hidden state")
+  const bool proj = pj != nullptr;
+  const int64_t ntot = (int64_t)(c.Hq + 2 * c.Hkv) * d;
+  uint8_t* dqkv_buf[2] = {nullptr, nullptr};
+  if (proj)
+    for (int b = 0; b < 2; ++b) dqkv_buf[b] = (uint8_t*)dev(ctx, B_PROJ1 + b, (size_t)c.c * ntot * eb);
+  int proj_chunks_done = 0;
+  auto proj_bwd = [&](int64_t j, cudaStream_t st) {
+    if (!proj) return;
+    const uint8_t* dy = dqkv_buf[j & 1];
+    const size_t xoff = (size_t)j * c.c * pj->hidden * eb;
+    gemm_dx(ctx, c.dtype, dy, ntot, pj->w, ntot, (uint8_t*)pj->dx + xoff, pj->hidden, c.c, pj->hidden, ntot, st);
+    gemm_dw(ctx, c.dtype, (const uint8_t*)pj->x + xoff, pj->hidden, dy, ntot, pj->dw, c.c, pj->hidden, ntot,
+            proj_chunks_done++ > 0, st);
+  };
   // B6: dq_j final (fp32, already scaled) -> the caller's rows (p == 1) or the head-side send buffer (p > 1)
   // dq_final: head-major fp32 rows of chunk j, heads head_stride elements apart
   auto emit_dq = [&](int64_t j, const float* dq_final, int64_t head_stride) {
-    if (p == 1)
+    if (p == 1 && proj)
+      FPDT_CHECK_LAUNCH(launch_convert_out(dq_final, C, hq, d, head_stride, 1.f, dqkv_buf[j & 1], c.dtype, ntot, 0,
+                                           cs));
+    else if (p == 1)
       FPDT_CHECK_LAUNCH(launch_convert_out(dq_final, C, hq, d, head_stride, 1.f,
                                            (uint8_t*)dq + (size_t)j * C * c.Hq * d * eb, c.dtype, (int64_t)c.Hq * d,
                                            0, cs));
@@ -982,23 +1094,39 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   };
   // B7: after outer iteration j, dq_j, dk_j, dv_j (in bsend) go back to their owner ranks (p > 1)
   auto send_back = [&](int64_t j) {
-    if (p == 1) return;
+    if (p == 1) {
+      proj_bwd(j, cs);
+      return;
+    }
     rec(ctx->ev_o_ready, cs);
     wait(ctx->s_comm, ctx->ev_o_ready);
     alltoall(ctx, bsend, brecv, (size_t)c.c * hcomb * d, c.dtype);
     const int64_t pst = (int64_t)c.c * hcomb * d, rld = (int64_t)hcomb * d;
-    FPDT_CHECK_LAUNCH(launch_unpack_head2seq(brecv, pst, rld, 0, c.c, c.Hq, d, p, eb,
-                                             (uint8_t*)dq + (size_t)j * c.c * c.Hq * d * eb, ctx->s_comm));
-    FPDT_CHECK_LAUNCH(launch_unpack_head2seq(brecv, pst, rld, hq, c.c, c.Hkv, d, p, eb,
-                                             (uint8_t*)dk + (size_t)j * c.c * c.Hkv * d * eb, ctx->s_comm));
-    FPDT_CHECK_LAUNCH(launch_unpack_head2seq(brecv, pst, rld, hq + hkv, c.c, c.Hkv, d, p, eb,
-                                             (uint8_t*)dv + (size_t)j * c.c * c.Hkv * d * eb, ctx->s_comm));
+    uint8_t *dqj = (uint8_t*)dq + (size_t)j * c.c * c.Hq * d * eb, *dkj = (uint8_t*)dk + (size_t)j * c.c * c.Hkv * d * eb,
+            *dvj = (uint8_t*)dv + (size_t)j * c.c * c.Hkv * d * eb;
+    int64_t dst_ld = 0;
+    if (proj) {
+      dqj = dqkv_buf[j & 1];
+      dkj = dqj + (size_t)c.Hq * d * eb;
+      dvj = dqj + (size_t)(c.Hq + c.Hkv) * d * eb;
+      dst_ld = ntot;
+    }
+    FPDT_CHECK_LAUNCH(launch_unpack_head2seq(brecv, pst, rld, 0, c.c, c.Hq, d, p, eb, dqj, ctx->s_comm, dst_ld));
+    FPDT_CHECK_LAUNCH(launch_unpack_head2seq(brecv, pst, rld, hq, c.c, c.Hkv, d, p, eb, dkj, ctx->s_comm, dst_ld));
+    FPDT_CHECK_LAUNCH(launch_unpack_head2seq(brecv, pst, rld, hq + hkv, c.c, c.Hkv, d, p, eb, dvj, ctx->s_comm,
+                                             dst_ld));
     ctx->stats.kernel_launches += 3;
+    proj_bwd(j, ctx->s_comm);  // projection backward of chunk j overlaps the next outer iteration
     rec(ctx->ev_comm_done, ctx->s_comm);
     wait(cs, ctx->ev_comm_done);  // bsend / brecv reuse by the next outer iteration
   };
   auto set_kv_out = [&](BwdArgs& a, int64_t j) {
-    if (p == 1) {
+    if (p == 1 && proj) {
+      a.dk_out = dqkv_buf[j & 1];
+      a.dv_out = dqkv_buf[j & 1] + (size_t)hkv * d * eb;
+      a.kv_out_ld = ntot;
+      a.kv_out_head0 = hq;  // as the p > 1 send buffer: dk heads [hq, hq + hkv), dv pre-offset by hkv heads
+    } else if (p == 1) {
       a.dk_out = (uint8_t*)dk + (size_t)j * C * c.Hkv * d * eb;
       a.dv_out = (uint8_t*)dv + (size_t)j * C * c.Hkv * d * eb;
       a.kv_out_ld = (int64_t)c.Hkv * d;
@@ -1064,8 +1192,9 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       order = bwd_host_bytes(FPDT_BWD_Q_OUTER, c, R.rkv, R.rq, keep) < bwd_host_bytes(FPDT_BWD_KV_OUTER, c, R.rkv, R.rq, keep)
                   ? FPDT_BWD_Q_OUTER
                   : FPDT_BWD_KV_OUTER;
+    if (proj) order = FPDT_BWD_KV_OUTER;  // the fused projection backward runs per final chunk j
     ctx->stats.bwd_order = order;
-    if (order == FPDT_BWD_Q_OUTER) {
+    if (order == FPDT_BWD_Q_OUTER && !proj) {
       backward_q_outer(ctx, c, R, keep, do_h, do_rows, do_heads, do_head0, dores, dq, dk, dv, cs);
     } else {
     uint8_t* kvs[2] = {(uint8_t*)dev(ctx, B_KVSLOT0, (size_t)C * row_kv2), (uint8_t*)dev(ctx, B_KVSLOT1, (size_t)C * row_kv2)};
@@ -1321,6 +1450,7 @@ int fpdt_ctx_destroy(fpdt_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->blas) cublasDestroy(ctx->blas);
     for (auto& b : ctx->bufs)
       if (b.ptr) cudaFree(b.ptr);
     if (ctx->host) cudaFreeHost(ctx->host);
@@ -1358,6 +1488,7 @@ int fpdt_attn_fwd(fpdt_ctx* ctx, const void* q, const void* k, const void* v, vo
     ctx->saved_res_q = ctx->res_q;
     ctx->fwd_done = false;
     forward(ctx, c, q, k, v, o, lse, static_cast<cudaStream_t>(stream));
+    ctx->saved_hidden = 0;
     ctx->saved = c;
     ctx->saved_q = q;
     ctx->saved_k = k;
@@ -1376,8 +1507,71 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
                            softmax_scale);
     if (!ctx->fwd_done) fail(FPDT_ERR_STATE, "fpdt_attn_bwd without a preceding fpdt_attn_fwd on this context");
     if (!(c == ctx->saved)) fail(FPDT_ERR_STATE, "backward arguments differ from the saved forward's");
+    if (ctx->saved_hidden) fail(FPDT_ERR_STATE, "the saved forward was fpdt_block_fwd: use fpdt_block_bwd");
     FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
     backward(ctx, c, o, dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+  });
+}
+
+namespace {
+void check_block_args(fpdt_ctx* ctx, const Config& c, int hidden) {
+  if (hidden <= 0 || (hidden * c.eb) % 16) fail(FPDT_ERR_ARG, "hidden must be positive and a multiple of 16 bytes");
+  if (!c.offload) fail(FPDT_ERR_UNSUPPORTED, "fpdt_block_fwd/bwd need offload = 1 (per-chunk projection schedule)");
+  if (ctx->res_kv || ctx->res_q)
+    fail(FPDT_ERR_UNSUPPORTED, "fpdt_block_fwd/bwd do not take an HBM residency budget (chunks are projected)");
+}
+}  // namespace
+
+int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, void* o, float* lse, int64_t s_local, int hidden,
+                   int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
+                   int dtype, int offload, float softmax_scale, void* stream) {
+  return run([&] {
+    if (!ctx || !x || !w_qkv || !o) fail(FPDT_ERR_ARG, "null pointer argument");
+    if (world_size != ctx->p) fail(FPDT_ERR_ARG, "world_size differs from the context's");
+    Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
+                           softmax_scale);
+    check_block_args(ctx, c, hidden);
+    FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
+    if (!ctx->plan.empty()) {
+      if (ctx->plan_u != c.u) fail(FPDT_ERR_ARG, "sparsity plan has " + std::to_string(ctx->plan_u) + " chunks, the call " + std::to_string(c.u));
+      for (int64_t m = 0; m < c.u; ++m)
+        if (!ctx->plan[(size_t)(m * c.u + m)]) fail(FPDT_ERR_ARG, "sparsity plan drops a diagonal block");
+    }
+    ctx->saved_plan = ctx->plan;
+    ctx->saved_res_kv = 0;
+    ctx->saved_res_q = 0;
+    ctx->fwd_done = false;
+    Proj pj;
+    pj.x = x;
+    pj.w = w_qkv;
+    pj.hidden = hidden;
+    forward(ctx, c, nullptr, nullptr, nullptr, o, lse, static_cast<cudaStream_t>(stream), &pj);
+    ctx->saved = c;
+    ctx->saved_q = ctx->saved_k = ctx->saved_v = nullptr;
+    ctx->saved_hidden = hidden;
+    ctx->fwd_done = true;
+  });
+}
+
+int fpdt_block_bwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* o, const void* dout, void* dx,
+                   float* dw_qkv, int64_t s_local, int hidden, int n_q_heads, int n_kv_heads, int head_dim, int causal,
+                   int64_t chunk_size, int world_size, int dtype, int offload, float softmax_scale, void* stream) {
+  return run([&] {
+    if (!ctx || !x || !w_qkv || !o || !dout || !dx || !dw_qkv) fail(FPDT_ERR_ARG, "null pointer argument");
+    if (world_size != ctx->p) fail(FPDT_ERR_ARG, "world_size differs from the context's");
+    Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
+                           softmax_scale);
+    if (!ctx->fwd_done) fail(FPDT_ERR_STATE, "fpdt_block_bwd without a preceding fpdt_block_fwd on this context");
+    if (!(c == ctx->saved) || ctx->saved_hidden != hidden)
+      fail(FPDT_ERR_STATE, "backward arguments differ from the saved block forward's");
+    FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
+    Proj pj;
+    pj.x = x;
+    pj.w = w_qkv;
+    pj.dx = dx;
+    pj.dw = dw_qkv;
+    pj.hidden = hidden;
+    backward(ctx, c, o, dout, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), &pj);
   });
 }
 

@@ -92,12 +92,15 @@ int launch_bwd_preprocess_D(const void* o, const void* dout, int dtype, int64_t 
 // fp32 head-major src[h*src_head_stride + row*d + e] * scale -> bf16/fp32 dst[row*dst_ld + (dst_head0+h)*d + e]
 int launch_convert_out(const float* src, int64_t rows, int heads, int head_dim, int64_t src_head_stride, float scale,
                        void* dst, int dtype, int64_t dst_ld, int dst_head0, cudaStream_t s);
-// pack rows [c][H][d] of a sequence-layout tensor into send[p][c][H/p][d] (elem_bytes 2 or 4)
+// pack rows [c][H][d] of a sequence-layout tensor into send[p][c][H/p][d] (elem_bytes 2 or 4); source rows
+// src_row_ld elements apart (0 = H*head_dim, dense)
 int launch_pack_seq2head(const void* src, int64_t c, int H, int head_dim, int p, int elem_bytes, void* dst,
-                         int64_t dst_peer_stride_elems, int64_t dst_row_ld, int dst_head0, cudaStream_t s);
-// unpack recv[p][c][H/p][d] into sequence-layout rows [c][H][d]
+                         int64_t dst_peer_stride_elems, int64_t dst_row_ld, int dst_head0, cudaStream_t s,
+                         int64_t src_row_ld = 0);
+// unpack recv[p][c][H/p][d] into sequence-layout rows [c][H][d], rows dst_row_ld elements apart (0 = dense)
 int launch_unpack_head2seq(const void* src, int64_t src_peer_stride_elems, int64_t src_row_ld, int src_head0,
-                           int64_t c, int H, int head_dim, int p, int elem_bytes, void* dst, cudaStream_t s);
+                           int64_t c, int H, int head_dim, int p, int elem_bytes, void* dst, cudaStream_t s,
+                           int64_t dst_row_ld = 0);
 // lse transpose: src[h*ld + t] (log2-domain) -> dst[t*dst_ld + dst_head0 + h] (natural log)
 int launch_lse_to_user(const float* src, int64_t ld, int64_t rows, int heads, float* dst, int64_t dst_ld,
                        int dst_head0, cudaStream_t s);

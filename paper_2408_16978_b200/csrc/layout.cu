@@ -84,7 +84,8 @@ __global__ void convert_out_kernel(const float* __restrict__ src, int64_t rows, 
 // Element (peer, t, hh, e) of the head-sharded side <-> (t, peer*hp + hh, e) of the sequence side.
 template <bool kPack>
 __global__ void relayout_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int64_t c, int H, int p,
-                                int vec_per_head, int64_t hs_peer_stride_v, int64_t hs_row_ld_v, int hs_head0) {
+                                int vec_per_head, int64_t hs_peer_stride_v, int64_t hs_row_ld_v, int hs_head0,
+                                int64_t seq_row_ld_v) {
   const int hp = H / p;
   const int64_t n = c * H * (int64_t)vec_per_head;
   for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
@@ -93,7 +94,7 @@ __global__ void relayout_kernel(const uint4* __restrict__ src, uint4* __restrict
     const int hg = (int)(rem / vec_per_head);
     const int e = (int)(rem - (int64_t)hg * vec_per_head);
     const int peer = hg / hp, hh = hg - peer * hp;
-    const int64_t seq_off = idx;  // sequence side is dense [c][H][d]
+    const int64_t seq_off = t * seq_row_ld_v + rem;  // sequence side [c][H][d], rows seq_row_ld apart
     const int64_t hs_off = peer * hs_peer_stride_v + t * hs_row_ld_v + (int64_t)(hs_head0 + hh) * vec_per_head + e;
     if (kPack)
       dst[hs_off] = src[seq_off];
@@ -142,22 +143,28 @@ int launch_convert_out(const float* src, int64_t rows, int heads, int head_dim, 
 }
 
 int launch_pack_seq2head(const void* src, int64_t c, int H, int head_dim, int p, int elem_bytes, void* dst,
-                         int64_t dst_peer_stride_elems, int64_t dst_row_ld, int dst_head0, cudaStream_t s) {
+                         int64_t dst_peer_stride_elems, int64_t dst_row_ld, int dst_head0, cudaStream_t s,
+                         int64_t src_row_ld) {
   const int vph = head_dim * elem_bytes / 16;
   const int epv = 16 / elem_bytes;
   const int64_t n = c * H * (int64_t)vph;
+  const int64_t seq_ld = src_row_ld > 0 ? src_row_ld : (int64_t)H * head_dim;
   relayout_kernel<true><<<grid_for(n), kBlock, 0, s>>>((const uint4*)src, (uint4*)dst, c, H, p, vph,
-                                                       dst_peer_stride_elems / epv, dst_row_ld / epv, dst_head0);
+                                                       dst_peer_stride_elems / epv, dst_row_ld / epv, dst_head0,
+                                                       seq_ld / epv);
   return (int)cudaGetLastError();
 }
 
 int launch_unpack_head2seq(const void* src, int64_t src_peer_stride_elems, int64_t src_row_ld, int src_head0,
-                           int64_t c, int H, int head_dim, int p, int elem_bytes, void* dst, cudaStream_t s) {
+                           int64_t c, int H, int head_dim, int p, int elem_bytes, void* dst, cudaStream_t s,
+                           int64_t dst_row_ld) {
   const int vph = head_dim * elem_bytes / 16;
   const int epv = 16 / elem_bytes;
   const int64_t n = c * H * (int64_t)vph;
+  const int64_t seq_ld = dst_row_ld > 0 ? dst_row_ld : (int64_t)H * head_dim;
   relayout_kernel<false><<<grid_for(n), kBlock, 0, s>>>((const uint4*)src, (uint4*)dst, c, H, p, vph,
-                                                        src_peer_stride_elems / epv, src_row_ld / epv, src_head0);
+                                                        src_peer_stride_elems / epv, src_row_ld / epv, src_head0,
+                                                        seq_ld / epv);
   return (int)cudaGetLastError();
 }
 

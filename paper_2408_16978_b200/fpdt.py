@@ -24,7 +24,7 @@ EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_a
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair", "fpdt_group_create",
             "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity", "fpdt_set_residency",
-            "fpdt_set_bwd_order",
+            "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd",
             "fpdt_selftest_softmax", "fpdt_selftest_reduce")
 
 
@@ -72,6 +72,12 @@ def _declare(lib):
     lib.fpdt_set_sparsity.restype = c_int
     lib.fpdt_set_residency.argtypes = [P, c_int64, c_int64]
     lib.fpdt_set_residency.restype = c_int
+    lib.fpdt_block_fwd.argtypes = [P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int64, c_int, c_int,
+                                   c_int, c_float, P]
+    lib.fpdt_block_fwd.restype = c_int
+    lib.fpdt_block_bwd.argtypes = [P, P, P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int64, c_int,
+                                   c_int, c_int, c_float, P]
+    lib.fpdt_block_bwd.restype = c_int
     lib.fpdt_set_bwd_order.argtypes = [P, c_int]
     lib.fpdt_set_bwd_order.restype = c_int
     lib.fpdt_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
@@ -216,6 +222,22 @@ def fpdt_attn_bwd(ctx: FPDTContext, o, dout, dq, dk, dv, s_local: int, n_q_heads
     _check(lib().fpdt_attn_bwd(ctx.handle, _ptr(o), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), s_local, n_q_heads,
                                n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload, softmax_scale,
                                _stream(stream)))
+
+
+def fpdt_block_fwd(ctx: FPDTContext, x, w_qkv, o, lse, s_local: int, hidden: int, n_q_heads: int, n_kv_heads: int,
+                   head_dim: int, causal: int, chunk_size: int, world_size: int, dtype: int, offload: int,
+                   softmax_scale: float = 0.0, stream=None):
+    _check(lib().fpdt_block_fwd(ctx.handle, _ptr(x), _ptr(w_qkv), _ptr(o), _ptr(lse), s_local, hidden, n_q_heads,
+                                n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload, softmax_scale,
+                                _stream(stream)))
+
+
+def fpdt_block_bwd(ctx: FPDTContext, x, w_qkv, o, dout, dx, dw_qkv, s_local: int, hidden: int, n_q_heads: int,
+                   n_kv_heads: int, head_dim: int, causal: int, chunk_size: int, world_size: int, dtype: int,
+                   offload: int, softmax_scale: float = 0.0, stream=None):
+    _check(lib().fpdt_block_bwd(ctx.handle, _ptr(x), _ptr(w_qkv), _ptr(o), _ptr(dout), _ptr(dx), _ptr(dw_qkv),
+                                s_local, hidden, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size,
+                                dtype, offload, softmax_scale, _stream(stream)))
 
 
 def dtype_code(torch_dtype) -> int:

@@ -1,0 +1,137 @@
+"""Attention block with the fused chunked QKV projection (include/fpdt.h fpdt_block_fwd / fpdt_block_bwd;
+SURVEY §8(f) NEXT-3) against oracle/block.py (fp64): O, lse, the hidden-state gradient dx
+and the weight gradient dW, normwise max relative error <= 1e-2 (bf16) / 1e-4 (fp32); p = 1 and, through the
+single-GPU local group, p = 2 and 4 (dW summed over ranks, as a data-parallel all-reduce would)."""
+import threading
+
+import numpy as np
+import pytest
+import torch
+
+import fpdt_inputs as gen
+from fpdt_testlib import TOL, rel_err
+from oracle import attention, block
+
+pytestmark = pytest.mark.gpu
+
+
+def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, keep=None) -> dict:
+    from paper_2408_16978_b200 import fpdt
+    S, hidden = xin["x"].shape
+    s_local = S // p
+    tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
+    code = fpdt.dtype_code(tdt)
+    group = fpdt.LocalGroup(p) if p > 1 else None
+    rows = [gen.global_tokens_of_rank(r, p, s_local, C) for r in range(p)]
+    out = {"o": np.zeros((S, Hq, d), np.float32), "lse": np.zeros((S, Hq), np.float32),
+           "dx": np.zeros((S, hidden), np.float32), "dw": [None] * p}
+    errors = []
+
+    def rank_main(r):
+        try:
+            torch.cuda.set_device(0)
+            stream = torch.cuda.Stream()
+            with torch.cuda.stream(stream):
+                x = torch.tensor(xin["x"][rows[r]]).to(tdt).cuda().contiguous()
+                w = torch.tensor(xin["w"]).to(tdt).cuda().contiguous()
+                do = torch.tensor(xin["do"][rows[r]]).to(tdt).cuda().contiguous()
+                o = torch.empty(s_local, Hq, d, dtype=tdt, device="cuda")
+                lse = torch.empty(s_local, Hq, dtype=torch.float32, device="cuda")
+                dx = torch.empty_like(x)
+                dw = torch.full(tuple(w.shape), float("nan"), dtype=torch.float32, device="cuda")
+            stream.synchronize()
+            ctx = fpdt.FPDTContext(p, r, group=group) if p > 1 else fpdt.FPDTContext()
+            if keep is not None:
+                ctx.set_sparsity(keep)
+            fpdt.fpdt_block_fwd(ctx, x, w, o, lse, s_local, hidden, Hq, Hkv, d, 1, C, p, code, 1, 0.0, stream)
+            fpdt.fpdt_block_bwd(ctx, x, w, o, do, dx, dw, s_local, hidden, Hq, Hkv, d, 1, C, p, code, 1, 0.0, stream)
+            stream.synchronize()
+            out["o"][rows[r]] = o.float().cpu().numpy()
+            out["lse"][rows[r]] = lse.cpu().numpy()
+            out["dx"][rows[r]] = dx.float().cpu().numpy()
+            out["dw"][r] = dw.cpu().numpy()
+            ctx.close()
+        except Exception as e:  # surfaced in the main thread
+            errors.append((r, e))
+
+    threads = [threading.Thread(target=rank_main, args=(r,)) for r in range(p)]
+    for t in threads:
+        t.start()
+    for t in threads:
+        t.join(timeout=300)
+    assert not any(t.is_alive() for t in threads), "a rank hung"
+    if group is not None:
+        group.close()
+    assert not errors, errors
+    out["dw"] = np.sum(out["dw"], axis=0)
+    return out
+
+
+def oracle_block(xin, Hq, Hkv, d, dtype, keep=None, C=0):
+    """bf16 mode: q, k, v and dq, dk, dv are bf16 tensors (reading R27, oracle/block.py)."""
+    r = dtype == "bf16"
+    dx, dw = block.block_backward(xin["x"], xin["w"], xin["do"], Hq, Hkv, d, bf16_intermediates=r, keep=keep,
+                                  chunk=C)
+    q, k, v = block.split_qkv(block._project(xin["x"], xin["w"], r), Hq, Hkv, d)
+    o, lse = attention.attention_forward(q, k, v, keep=keep, chunk=C)
+    return {"o": o, "lse": lse, "dx": dx, "dw": dw}
+
+
+@pytest.mark.parametrize("p,S,hidden,Hq,Hkv,d,C", [
+    (1, 2048, 256, 4, 2, 64, 512),
+    (1, 2048, 320, 4, 4, 80, 512),
+    (1, 1024, 256, 8, 2, 128, 256),
+    (2, 2048, 256, 4, 2, 80, 512),
+    (4, 2048, 512, 8, 4, 64, 1024),
+])
+def test_block_bf16(p, S, hidden, Hq, Hkv, d, C):
+    xin = gen.make_block_inputs("normal", 41, S, hidden, Hq, Hkv, d)
+    got = run_block(xin, p, C, "bf16", Hq, Hkv, d)
+    ref = oracle_block(xin, Hq, Hkv, d, "bf16")
+    errs = {n: rel_err(got[n], ref[n]) for n in ref}
+    assert all(e <= TOL["bf16"] for e in errs.values()), errs
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_block_fp32(p):
+    S, hidden, Hq, Hkv, d, C = 1024, 128, 4, 2, 64, 256
+    xin = gen.make_block_inputs("normal", 42, S, hidden, Hq, Hkv, d)
+    got = run_block(xin, p, C, "fp32", Hq, Hkv, d)
+    ref = oracle_block(xin, Hq, Hkv, d, "fp32")
+    errs = {n: rel_err(got[n], ref[n]) for n in ref}
+    assert all(e <= TOL["fp32"] for e in errs.values()), errs
+
+
+def test_block_sparse():
+    S, hidden, Hq, Hkv, d, C = 2048, 256, 4, 2, 64, 256
+    keep = gen.sparsity_plan(S // C, 0.4, seed=9)
+    xin = gen.make_block_inputs("normal", 43, S, hidden, Hq, Hkv, d)
+    got = run_block(xin, 1, C, "bf16", Hq, Hkv, d, keep=keep)
+    ref = oracle_block(xin, Hq, Hkv, d, "bf16", keep=keep, C=C)
+    errs = {n: rel_err(got[n], ref[n]) for n in ref}
+    assert all(e <= TOL["bf16"] for e in errs.values()), errs
+
+
+def test_block_errors():
+    from paper_2408_16978_b200 import fpdt
+    S, hidden, Hq, Hkv, d, C = 512, 128, 2, 2, 64, 256
+    x = torch.zeros(S, hidden, dtype=torch.bfloat16, device="cuda")
+    w = torch.zeros(hidden, (Hq + 2 * Hkv) * d, dtype=torch.bfloat16, device="cuda")
+    o = torch.empty(S, Hq, d, dtype=torch.bfloat16, device="cuda")
+    dx, dw = torch.empty_like(x), torch.empty(tuple(w.shape), dtype=torch.float32, device="cuda")
+    q = torch.zeros(S, Hq, d, dtype=torch.bfloat16, device="cuda")
+    ctx = fpdt.FPDTContext()
+    with pytest.raises(fpdt.FpdtError) as e:
+        fpdt.fpdt_block_fwd(ctx, x, w, o, None, S, hidden, Hq, Hkv, d, 1, C, 1, fpdt.FPDT_BF16, 0)
+    assert e.value.code == fpdt.FPDT_ERR_UNSUPPORTED
+    fpdt.fpdt_attn_fwd(ctx, q, q, q, o, None, S, Hq, Hkv, d, 1, C, 1, fpdt.FPDT_BF16, 1)
+    with pytest.raises(fpdt.FpdtError) as e:
+        fpdt.fpdt_block_bwd(ctx, x, w, o, o, dx, dw, S, hidden, Hq, Hkv, d, 1, C, 1, fpdt.FPDT_BF16, 1)
+    assert e.value.code == fpdt.FPDT_ERR_STATE
+    fpdt.fpdt_block_fwd(ctx, x, w, o, None, S, hidden, Hq, Hkv, d, 1, C, 1, fpdt.FPDT_BF16, 1)
+    dq = torch.empty_like(q)
+    with pytest.raises(fpdt.FpdtError) as e:
+        fpdt.fpdt_attn_bwd(ctx, o, o, dq, dq, dq, S, Hq, Hkv, d, 1, C, 1, fpdt.FPDT_BF16, 1)
+    assert e.value.code == fpdt.FPDT_ERR_STATE
+    torch.cuda.synchronize()
+    ctx.close()

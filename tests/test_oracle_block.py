@@ -61,3 +61,26 @@ def test_block_inputs_bf16_exact_and_scaled():
         assert np.array_equal(gen.bf16_round(x[n]), x[n]), n
     qkv = x["x"].astype(np.float64) @ x["w"]
     assert 0.7 < qkv.std() < 1.5
+
+
+def test_bf16_rounding_helper():
+    """The oracle's bf16 rounding (R27) against hand-worked bit patterns: ties to even, carries into the exponent,
+    and the identity on bf16-representable values."""
+    x = np.array([1.0, 1.0 + 2.0 ** -8, 1.0 + 3 * 2.0 ** -8, 1.0 + 2.0 ** -7 + 2.0 ** -9, 2.0 - 2.0 ** -9, -3.5])
+    want = np.array([1.0, 1.0, 1.0 + 2.0 ** -6, 1.0 + 2.0 ** -7, 2.0, -3.5])
+    assert np.array_equal(block._bf16(x), want)
+
+
+def test_bf16_intermediates_identity_weight():
+    """With W = I and bf16 x, the projected q, k, v are already bf16: rounding them changes nothing in the forward;
+    the backward then differs from the unrounded one only by the bf16 rounding of dq, dk, dv."""
+    S, Hq, Hkv, d = 32, 2, 1, 8
+    n = (Hq + 2 * Hkv) * d
+    x = gen.make_inputs("normal", 5, S, Hq, Hkv, d)
+    xs = np.concatenate([x["q"].reshape(S, -1), x["k"].reshape(S, -1), x["v"].reshape(S, -1)], axis=1)
+    o1, l1 = block.block_forward(xs, np.eye(n), Hq, Hkv, d, bf16_intermediates=True)
+    o0, l0 = block.block_forward(xs, np.eye(n), Hq, Hkv, d)
+    assert np.array_equal(o1, o0) and np.array_equal(l1, l0)
+    dx1, _ = block.block_backward(xs, np.eye(n), x["do"], Hq, Hkv, d, bf16_intermediates=True)
+    dx0, _ = block.block_backward(xs, np.eye(n), x["do"], Hq, Hkv, d)
+    assert np.array_equal(dx1, block._bf16(dx0))
