@@ -74,3 +74,27 @@ def block_backward(x, w, do, n_q_heads: int, n_kv_heads: int, head_dim: int, sca
     if bf16_intermediates:
         dqkv = _bf16(dqkv)
     return dqkv @ w.T, x.T @ dqkv
+
+
+# Output projection after the attention (the other side of the path; the paper's block ends in
+# the attention output's projection before the FFN): y = O W_o with O flattened per token to [S, Hq d]
+# (head-major, head_dim fastest) and W_o [Hq d, hidden]; backward dO = dY W_o^T, dW_o = O^T dY.  bf16 mode (R27):
+# O and dO are bf16 tensors.
+def output_forward(o, w_o, bf16_intermediates: bool = False):
+    of = np.asarray(o, np.float64).reshape(np.shape(o)[0], -1)
+    if bf16_intermediates:
+        of = _bf16(of)
+    return of @ np.asarray(w_o, np.float64)
+
+
+def output_backward(o, w_o, dy, bf16_intermediates: bool = False):
+    """dO [S, Hq, d] (the upstream gradient of the attention output) and dW_o [Hq d, hidden]."""
+    S = np.shape(o)[0]
+    of = np.asarray(o, np.float64).reshape(S, -1)
+    if bf16_intermediates:
+        of = _bf16(of)
+    dy = np.asarray(dy, np.float64)
+    do = dy @ np.asarray(w_o, np.float64).T
+    if bf16_intermediates:
+        do = _bf16(do)
+    return do.reshape(np.shape(o)), of.T @ dy

@@ -84,3 +84,33 @@ def test_bf16_intermediates_identity_weight():
     dx1, _ = block.block_backward(xs, np.eye(n), x["do"], Hq, Hkv, d, bf16_intermediates=True)
     dx0, _ = block.block_backward(xs, np.eye(n), x["do"], Hq, Hkv, d)
     assert np.array_equal(dx1, block._bf16(dx0))
+
+
+def test_block_with_output_projection_finite_differences():
+    """y = attention(x W) W_o: dx, dW, dW_o of L = <dY, y> against central finite differences."""
+    S, hidden, d, Hq, Hkv = 8, 6, 4, 2, 1
+    rng = np.random.default_rng(12)
+    x = rng.standard_normal((S, hidden))
+    w = rng.standard_normal((hidden, (Hq + 2 * Hkv) * d)) * 0.5
+    wo = rng.standard_normal((Hq * d, hidden)) * 0.5
+    dy = rng.standard_normal((S, hidden))
+
+    def loss(x_, w_, wo_):
+        o, _ = block.block_forward(x_, w_, Hq, Hkv, d)
+        return float(np.sum(dy * block.output_forward(o, wo_)))
+
+    o, _ = block.block_forward(x, w, Hq, Hkv, d)
+    do, dwo = block.output_backward(o, wo, dy)
+    dx, dw = block.block_backward(x, w, do, Hq, Hkv, d)
+    eps = 1e-5
+    for arr, grad, which in ((x, dx, 0), (w, dw, 1), (wo, dwo, 2)):
+        fd = np.zeros_like(arr)
+        for idx in np.ndindex(*arr.shape):
+            ap, am = arr.copy(), arr.copy()
+            ap[idx] += eps
+            am[idx] -= eps
+            args_p = [x, w, wo]
+            args_m = [x, w, wo]
+            args_p[which], args_m[which] = ap, am
+            fd[idx] = (loss(*args_p) - loss(*args_m)) / (2 * eps)
+        assert np.abs(grad - fd).max() / np.abs(fd).max() < 1e-6, which
