@@ -34,8 +34,8 @@ from __future__ import annotations
 
 import numpy as np
 
-Q, K, V, DO, X, W = 0, 1, 2, 3, 4, 5
-TENSOR_IDS = {"q": Q, "k": K, "v": V, "do": DO, "x": X, "w": W}
+Q, K, V, DO, X, W, WO, DY = 0, 1, 2, 3, 4, 5, 6, 7
+TENSOR_IDS = {"q": Q, "k": K, "v": V, "do": DO, "x": X, "w": W, "wo": WO, "dy": DY}
 DISTRIBUTIONS = ("normal", "peaky", "drift", "sink", "same", "class")
 DIST_IDS = {name: i for i, name in enumerate(DISTRIBUTIONS)}
 N_CLASSES = 4
@@ -180,3 +180,16 @@ def make_block_inputs(dist: str, seed: int, seq_len: int, hidden: int, n_q_heads
     w = (w * np.float32(2.0 ** -round(np.log2(np.sqrt(hidden))))).astype(np.float32)
     do = generate("do", dist, seed, tokens, n_q_heads, head_dim, seq_len)
     return {"x": x, "w": w, "do": do}
+
+
+def make_output_proj_inputs(seed: int, seq_len: int, hidden: int, n_q_heads: int, head_dim: int,
+                            tokens: np.ndarray | None = None) -> dict:
+    """Output projection weight wo [Hq * head_dim, hidden] (scaled by 2^-round(log2(sqrt(Hq * head_dim)))) and the
+    upstream gradient dy [T, hidden] of the block output y = o wo (rows = global tokens)."""
+    if tokens is None:
+        tokens = np.arange(seq_len, dtype=np.int64)
+    k = n_q_heads * head_dim
+    wo = generate("wo", "normal", seed, np.arange(k), 1, hidden, seq_len).reshape(k, hidden)
+    wo = (wo * np.float32(2.0 ** -round(np.log2(np.sqrt(k))))).astype(np.float32)
+    dy = generate("dy", "normal", seed, tokens, 1, hidden, seq_len).reshape(len(tokens), hidden)
+    return {"wo": wo, "dy": dy}

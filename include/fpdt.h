@@ -125,16 +125,22 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
  *   x      [s_local][hidden]                         hidden state, rank-ordinal rows (as q of fpdt_attn_fwd)
  *   w_qkv  [hidden][(n_q_heads + 2 n_kv_heads) * head_dim]  row-major projection weight; columns are the q heads,
  *          then the k heads, then the v heads, head_dim fastest: [q | k | v] = x w_qkv (no bias)
- *   o, lse as fpdt_attn_fwd.  dx [s_local][hidden] (output, overwritten), dw_qkv fp32 [hidden][(Hq + 2 Hkv) d]
- *   (output, overwritten: the sum over this rank's rows of x^T dqkv; a data-parallel caller all-reduces it).
- * x, w_qkv must be unchanged between the two calls.  All pointers are device pointers; dtype FPDT_BF16 (x, w, dx
+ *   w_o    [n_q_heads * head_dim][hidden] or NULL: the output projection after the attention, y = o w_o (o flattened
+ *          per token, head-major), computed per chunk as soon as the chunk's o is final; NULL = no output projection
+ *   o, lse as fpdt_attn_fwd (o is always written: the backward needs it); y [s_local][hidden] (output; with w_o)
+ *   dout   without w_o: dL/do [s_local][n_q_heads][head_dim]; with w_o: dL/dy [s_local][hidden], from which the
+ *          library forms dL/do = dy w_o^T and dw_o = o^T dy (fp32 [Hq d][hidden], output, overwritten)
+ *   dx [s_local][hidden] (output, overwritten), dw_qkv fp32 [hidden][(Hq + 2 Hkv) d] (output, overwritten: the sum
+ *   over this rank's rows of x^T dqkv; a data-parallel caller all-reduces dw_qkv and dw_o).
+ * x, w_qkv, w_o must be unchanged between the two calls, and w_o NULL in both or in neither.  All pointers are device pointers; dtype FPDT_BF16 (x, w, dx
  * bf16) or FPDT_FP32.  Errors: as fpdt_attn_fwd/bwd; hidden * elem bytes % 16 != 0: FPDT_ERR_ARG; offload = 0 or a
  * residency budget: FPDT_ERR_UNSUPPORTED; fpdt_attn_bwd after fpdt_block_fwd (or the reverse): FPDT_ERR_STATE. */
-int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, void* o, float* lse, int64_t s_local, int hidden,
+int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* w_o, void* o, float* lse, void* y,
+                   int64_t s_local, int hidden,
                    int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
                    int dtype, int offload, float softmax_scale, void* stream);
-int fpdt_block_bwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* o, const void* dout, void* dx,
-                   float* dw_qkv, int64_t s_local, int hidden, int n_q_heads, int n_kv_heads, int head_dim, int causal,
+int fpdt_block_bwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* w_o, const void* o, const void* dout,
+                   void* dx, float* dw_qkv, float* dw_o, int64_t s_local, int hidden, int n_q_heads, int n_kv_heads, int head_dim, int causal,
                    int64_t chunk_size, int world_size, int dtype, int offload, float softmax_scale, void* stream);
 
 /* Block-sparse attention (§5.6, Table "MFU at different attention sparsity": "only part of the tokens in

@@ -99,12 +99,17 @@ struct Config {
 
 // Fused QKV projection of fpdt_block_fwd / fpdt_block_bwd; nullptr = the
 // attention-only calls.  Row-major: x, dx [s_local][hidden]; w [hidden][(Hq + 2 Hkv) * d] (q heads, k, v); dw fp32.
+// Optional output projection after the attention: w_o [Hq * d][hidden], y = o w_o [s_local][hidden]; backward from
+// dy: dO = dy w_o^T, dw_o = o^T dy (fp32).
 struct Proj {
   const void* x = nullptr;
   const void* w = nullptr;
   void* dx = nullptr;
   float* dw = nullptr;
   int hidden = 0;
+  const void* w_o = nullptr;
+  void* y = nullptr;
+  float* dw_o = nullptr;
 };
 
 struct DevBuf {
@@ -117,7 +122,7 @@ enum BufId {
   B_STORE, B_D, B_DQDEV, B_QSLOT0, B_QSLOT1, B_DOSLOT0, B_DOSLOT1, B_DQSLOT0, B_DQSLOT1, B_DKACC, B_DVACC,
   B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_RESSTORE, B_DORES, B_DQRES, B_DKVSLOT0,
   B_DKVSLOT1, B_DKVRES, B_KVSLOT2, B_KVSLOT3, B_DKVSLOT2, B_DKVSLOT3, B_QOSEND, B_QORECV, B_PROJ0, B_PROJ1,
-  B_PROJ2, B_NUM
+  B_PROJ2, B_DOUT, B_NUM
 };
 
 }  // namespace
@@ -172,6 +177,7 @@ struct fpdt_ctx {
   bool fwd_done = false;
   Config saved;
   int saved_hidden = 0;  // > 0: the saved forward was fpdt_block_fwd with this hidden size
+  bool saved_has_wo = false;  // ... with the output projection
   // block-sparsity plan (fpdt_set_sparsity): keep[m*u + i] over (query chunk m, key chunk i); empty = dense.
   // The forward copies it into saved_plan; the backward of that forward uses the copy.
   std::vector<uint8_t> plan, saved_plan;
@@ -701,6 +707,11 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
         ++fetch;
       }
     }
+    // output projection of chunk m (fpdt_block_fwd with w_o): y_m = o_m w_o once O_m is final in the sequence layout
+    const int64_t od = (int64_t)c.Hq * d;
+    if (proj && pj->w_o && p == 1)
+      gemm_xw(ctx, c.dtype, (const uint8_t*)o + (size_t)m * C * od * eb, od, pj->w_o, pj->hidden,
+              (uint8_t*)pj->y + (size_t)m * C * pj->hidden * eb, pj->hidden, C, od, pj->hidden, cs);
     if (p > 1) {
       // F10: all-to-all of O_m back to the sequence layout, then unpack into the caller's rows of slot m
       rec(ctx->ev_o_ready, cs);
@@ -710,6 +721,9 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       FPDT_CHECK_LAUNCH(launch_unpack_head2seq(back, (int64_t)c.c * hq * d, (int64_t)hq * d, 0, c.c, c.Hq, d, p, eb,
                                                (uint8_t*)o + (size_t)m * c.c * c.Hq * d * eb, ctx->s_comm));
       ctx->stats.kernel_launches++;
+      if (proj && pj->w_o)
+        gemm_xw(ctx, c.dtype, (const uint8_t*)o + (size_t)m * c.c * od * eb, od, pj->w_o, pj->hidden,
+                (uint8_t*)pj->y + (size_t)m * c.c * pj->hidden * eb, pj->hidden, c.c, od, pj->hidden, ctx->s_comm);
       if (lse) {
         // lse of this chunk: [hq][C] log2 -> [C][hq] natural, all-to-all (fp32), unpack to [c][Hq]
         float* lt = (float*)dev(ctx, B_LSE_T, (size_t)C * hq * 4);
@@ -988,6 +1002,15 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   float* lse_save = (float*)ctx->bufs[B_LSESAVE].ptr;
   float* Dh = (float*)dev(ctx, B_D, (size_t)hq * c.S * 4);
   const __nv_bfloat16* o_resid = c.dtype == FPDT_BF16 ? (const __nv_bfloat16*)ctx->bufs[B_ORESID].ptr : nullptr;
+  if (pj && pj->w_o) {
+    // output projection backward (fpdt_block_bwd with w_o): `dout` is dy [s_local][hidden]; dO = dy w_o^T for every
+    // local row and dw_o = o^T dy, before the attention backward needs dO
+    const int64_t od = (int64_t)c.Hq * d;
+    void* dO = dev(ctx, B_DOUT, (size_t)c.s_local * od * eb);
+    gemm_dx(ctx, c.dtype, dout, pj->hidden, pj->w_o, pj->hidden, dO, od, c.s_local, od, pj->hidden, cs);
+    gemm_dw(ctx, c.dtype, o, od, dout, pj->hidden, pj->dw_o, c.s_local, od, pj->hidden, false, cs);
+    dout = dO;
+  }
   ensure_events(ctx->ev_doff, u);
   ensure_events(ctx->ev_dqoff, u);
   ensure_events(ctx->ev_a2a, u);
@@ -1522,11 +1545,12 @@ void check_block_args(fpdt_ctx* ctx, const Config& c, int hidden) {
 }
 }  // namespace
 
-int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, void* o, float* lse, int64_t s_local, int hidden,
+int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* w_o, void* o, float* lse, void* y,
+                   int64_t s_local, int hidden,
                    int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
                    int dtype, int offload, float softmax_scale, void* stream) {
   return run([&] {
-    if (!ctx || !x || !w_qkv || !o) fail(FPDT_ERR_ARG, "null pointer argument");
+    if (!ctx || !x || !w_qkv || !o || (w_o && !y)) fail(FPDT_ERR_ARG, "null pointer argument");
     if (world_size != ctx->p) fail(FPDT_ERR_ARG, "world_size differs from the context's");
     Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
                            softmax_scale);
@@ -1545,24 +1569,28 @@ int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, void* o, flo
     pj.x = x;
     pj.w = w_qkv;
     pj.hidden = hidden;
+    pj.w_o = w_o;
+    pj.y = y;
     forward(ctx, c, nullptr, nullptr, nullptr, o, lse, static_cast<cudaStream_t>(stream), &pj);
     ctx->saved = c;
     ctx->saved_q = ctx->saved_k = ctx->saved_v = nullptr;
     ctx->saved_hidden = hidden;
+    ctx->saved_has_wo = w_o != nullptr;
     ctx->fwd_done = true;
   });
 }
 
-int fpdt_block_bwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* o, const void* dout, void* dx,
-                   float* dw_qkv, int64_t s_local, int hidden, int n_q_heads, int n_kv_heads, int head_dim, int causal,
+int fpdt_block_bwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* w_o, const void* o, const void* dout,
+                   void* dx, float* dw_qkv, float* dw_o, int64_t s_local, int hidden, int n_q_heads, int n_kv_heads, int head_dim, int causal,
                    int64_t chunk_size, int world_size, int dtype, int offload, float softmax_scale, void* stream) {
   return run([&] {
-    if (!ctx || !x || !w_qkv || !o || !dout || !dx || !dw_qkv) fail(FPDT_ERR_ARG, "null pointer argument");
+    if (!ctx || !x || !w_qkv || !o || !dout || !dx || !dw_qkv || (w_o && !dw_o))
+      fail(FPDT_ERR_ARG, "null pointer argument");
     if (world_size != ctx->p) fail(FPDT_ERR_ARG, "world_size differs from the context's");
     Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
                            softmax_scale);
     if (!ctx->fwd_done) fail(FPDT_ERR_STATE, "fpdt_block_bwd without a preceding fpdt_block_fwd on this context");
-    if (!(c == ctx->saved) || ctx->saved_hidden != hidden)
+    if (!(c == ctx->saved) || ctx->saved_hidden != hidden || ctx->saved_has_wo != (w_o != nullptr))
       fail(FPDT_ERR_STATE, "backward arguments differ from the saved block forward's");
     FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
     Proj pj;
@@ -1571,6 +1599,8 @@ int fpdt_block_bwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* 
     pj.dx = dx;
     pj.dw = dw_qkv;
     pj.hidden = hidden;
+    pj.w_o = w_o;
+    pj.dw_o = dw_o;
     backward(ctx, c, o, dout, nullptr, nullptr, nullptr, static_cast<cudaStream_t>(stream), &pj);
   });
 }

@@ -72,10 +72,10 @@ def _declare(lib):
     lib.fpdt_set_sparsity.restype = c_int
     lib.fpdt_set_residency.argtypes = [P, c_int64, c_int64]
     lib.fpdt_set_residency.restype = c_int
-    lib.fpdt_block_fwd.argtypes = [P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int64, c_int, c_int,
+    lib.fpdt_block_fwd.argtypes = [P, P, P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int64, c_int, c_int,
                                    c_int, c_float, P]
     lib.fpdt_block_fwd.restype = c_int
-    lib.fpdt_block_bwd.argtypes = [P, P, P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int64, c_int,
+    lib.fpdt_block_bwd.argtypes = [P, P, P, P, P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int64, c_int,
                                    c_int, c_int, c_float, P]
     lib.fpdt_block_bwd.restype = c_int
     lib.fpdt_set_bwd_order.argtypes = [P, c_int]
@@ -226,16 +226,19 @@ def fpdt_attn_bwd(ctx: FPDTContext, o, dout, dq, dk, dv, s_local: int, n_q_heads
 
 def fpdt_block_fwd(ctx: FPDTContext, x, w_qkv, o, lse, s_local: int, hidden: int, n_q_heads: int, n_kv_heads: int,
                    head_dim: int, causal: int, chunk_size: int, world_size: int, dtype: int, offload: int,
-                   softmax_scale: float = 0.0, stream=None):
-    _check(lib().fpdt_block_fwd(ctx.handle, _ptr(x), _ptr(w_qkv), _ptr(o), _ptr(lse), s_local, hidden, n_q_heads,
+                   softmax_scale: float = 0.0, stream=None, w_o=None, y=None):
+    _check(lib().fpdt_block_fwd(ctx.handle, _ptr(x), _ptr(w_qkv), _ptr(w_o), _ptr(o), _ptr(lse), _ptr(y), s_local,
+                                hidden, n_q_heads,
                                 n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload, softmax_scale,
                                 _stream(stream)))
 
 
 def fpdt_block_bwd(ctx: FPDTContext, x, w_qkv, o, dout, dx, dw_qkv, s_local: int, hidden: int, n_q_heads: int,
                    n_kv_heads: int, head_dim: int, causal: int, chunk_size: int, world_size: int, dtype: int,
-                   offload: int, softmax_scale: float = 0.0, stream=None):
-    _check(lib().fpdt_block_bwd(ctx.handle, _ptr(x), _ptr(w_qkv), _ptr(o), _ptr(dout), _ptr(dx), _ptr(dw_qkv),
+                   offload: int, softmax_scale: float = 0.0, stream=None, w_o=None, dw_o=None):
+    """dout: dL/do, or dL/dy [s_local, hidden] when w_o is given (include/fpdt.h)."""
+    _check(lib().fpdt_block_bwd(ctx.handle, _ptr(x), _ptr(w_qkv), _ptr(w_o), _ptr(o), _ptr(dout), _ptr(dx),
+                                _ptr(dw_qkv), _ptr(dw_o),
                                 s_local, hidden, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size,
                                 dtype, offload, softmax_scale, _stream(stream)))
 

@@ -15,7 +15,8 @@ from oracle import attention, block
 pytestmark = pytest.mark.gpu
 
 
-def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, keep=None) -> dict:
+def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, keep=None, oproj=None) -> dict:
+    """oproj: {"wo", "dy"} for the output projection (y = o wo; the backward starts from dy)."""
     from paper_2408_16978_b200 import fpdt
     S, hidden = xin["x"].shape
     s_local = S // p
@@ -24,7 +25,8 @@ def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, 
     group = fpdt.LocalGroup(p) if p > 1 else None
     rows = [gen.global_tokens_of_rank(r, p, s_local, C) for r in range(p)]
     out = {"o": np.zeros((S, Hq, d), np.float32), "lse": np.zeros((S, Hq), np.float32),
-           "dx": np.zeros((S, hidden), np.float32), "dw": [None] * p}
+           "dx": np.zeros((S, hidden), np.float32), "dw": [None] * p, "y": np.zeros((S, hidden), np.float32),
+           "dwo": [None] * p}
     errors = []
 
     def rank_main(r):
@@ -35,6 +37,12 @@ def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, 
                 x = torch.tensor(xin["x"][rows[r]]).to(tdt).cuda().contiguous()
                 w = torch.tensor(xin["w"]).to(tdt).cuda().contiguous()
                 do = torch.tensor(xin["do"][rows[r]]).to(tdt).cuda().contiguous()
+                wo = y = dwo = None
+                if oproj is not None:
+                    wo = torch.tensor(oproj["wo"]).to(tdt).cuda().contiguous()
+                    do = torch.tensor(oproj["dy"][rows[r]]).to(tdt).cuda().contiguous()   # dL/dy
+                    y = torch.empty(s_local, hidden, dtype=tdt, device="cuda")
+                    dwo = torch.full(tuple(wo.shape), float("nan"), dtype=torch.float32, device="cuda")
                 o = torch.empty(s_local, Hq, d, dtype=tdt, device="cuda")
                 lse = torch.empty(s_local, Hq, dtype=torch.float32, device="cuda")
                 dx = torch.empty_like(x)
@@ -43,13 +51,18 @@ def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, 
             ctx = fpdt.FPDTContext(p, r, group=group) if p > 1 else fpdt.FPDTContext()
             if keep is not None:
                 ctx.set_sparsity(keep)
-            fpdt.fpdt_block_fwd(ctx, x, w, o, lse, s_local, hidden, Hq, Hkv, d, 1, C, p, code, 1, 0.0, stream)
-            fpdt.fpdt_block_bwd(ctx, x, w, o, do, dx, dw, s_local, hidden, Hq, Hkv, d, 1, C, p, code, 1, 0.0, stream)
+            fpdt.fpdt_block_fwd(ctx, x, w, o, lse, s_local, hidden, Hq, Hkv, d, 1, C, p, code, 1, 0.0, stream,
+                                w_o=wo, y=y)
+            fpdt.fpdt_block_bwd(ctx, x, w, o, do, dx, dw, s_local, hidden, Hq, Hkv, d, 1, C, p, code, 1, 0.0, stream,
+                                w_o=wo, dw_o=dwo)
             stream.synchronize()
             out["o"][rows[r]] = o.float().cpu().numpy()
             out["lse"][rows[r]] = lse.cpu().numpy()
             out["dx"][rows[r]] = dx.float().cpu().numpy()
             out["dw"][r] = dw.cpu().numpy()
+            if oproj is not None:
+                out["y"][rows[r]] = y.float().cpu().numpy()
+                out["dwo"][r] = dwo.cpu().numpy()
             ctx.close()
         except Exception as e:  # surfaced in the main thread
             errors.append((r, e))
@@ -64,6 +77,7 @@ def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, 
         group.close()
     assert not errors, errors
     out["dw"] = np.sum(out["dw"], axis=0)
+    out["dwo"] = np.sum(out["dwo"], axis=0) if oproj is not None else None
     return out
 
 
@@ -135,3 +149,20 @@ def test_block_errors():
     assert e.value.code == fpdt.FPDT_ERR_STATE
     torch.cuda.synchronize()
     ctx.close()
+
+
+@pytest.mark.parametrize("p,dtype", [(1, "bf16"), (2, "bf16"), (1, "fp32"), (2, "fp32")])
+def test_block_with_output_projection(p, dtype):
+    """y = attention(x W_qkv) W_o and the backward from dL/dy: y, dx, dW_qkv, dW_o against the oracle."""
+    S, hidden, Hq, Hkv, d, C = 1024, 256, 4, 2, 64, 256
+    xin = gen.make_block_inputs("normal", 44, S, hidden, Hq, Hkv, d)
+    op = gen.make_output_proj_inputs(44, S, hidden, Hq, d)
+    got = run_block(xin, p, C, dtype, Hq, Hkv, d, oproj=op)
+    r = dtype == "bf16"
+    o, lse = block.block_forward(xin["x"], xin["w"], Hq, Hkv, d, bf16_intermediates=r)
+    y = block.output_forward(o, op["wo"], bf16_intermediates=r)
+    do, dwo = block.output_backward(o, op["wo"], op["dy"], bf16_intermediates=r)
+    dx, dw = block.block_backward(xin["x"], xin["w"], do, Hq, Hkv, d, bf16_intermediates=r)
+    ref = {"o": o, "lse": lse, "y": y, "dx": dx, "dw": dw, "dwo": dwo}
+    errs = {n: rel_err(got[n], ref[n]) for n in ref}
+    assert all(e <= TOL[dtype] for e in errs.values()), errs

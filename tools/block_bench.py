@@ -41,6 +41,10 @@ def main():
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     dx = torch.empty_like(x)
     dw = torch.empty(hidden, N, dtype=torch.float32, device="cuda")
+    wo = (torch.randn(H * d, hidden, dtype=bf, device="cuda") * ((H * d) ** -0.5)).to(bf)
+    y = torch.empty(S, hidden, dtype=bf, device="cuda")
+    dy = torch.randn(S, hidden, dtype=bf, device="cuda")
+    dwo = torch.empty(H * d, hidden, dtype=torch.float32, device="cuda")
     stream = torch.cuda.current_stream()
     B = fpdt.FPDT_BF16
     ctx = fpdt.FPDTContext()
@@ -52,6 +56,11 @@ def main():
     def block_step():
         fpdt.fpdt_block_fwd(ctx, x, w, o, None, S, hidden, H, H, d, 1, C, 1, B, 1, 0.0, stream)
         fpdt.fpdt_block_bwd(ctx, x, w, o, do, dx, dw, S, hidden, H, H, d, 1, C, 1, B, 1, 0.0, stream)
+
+    def block_o_step():
+        fpdt.fpdt_block_fwd(ctx, x, w, o, None, S, hidden, H, H, d, 1, C, 1, B, 1, 0.0, stream, w_o=wo, y=y)
+        fpdt.fpdt_block_bwd(ctx, x, w, o, dy, dx, dw, S, hidden, H, H, d, 1, C, 1, B, 1, 0.0, stream, w_o=wo,
+                            dw_o=dwo)
 
     def timed(step):
         for _ in range(args.warmup):
@@ -69,6 +78,7 @@ def main():
 
     t_attn, l_attn = timed(attn_step)
     t_block, l_block = timed(block_step)
+    t_block_o, l_block_o = timed(block_o_step)
     f_attn = 14 * d * H * S * (S + 1) / 2
     f_proj = 6 * S * hidden * N  # fwd x W, bwd dx = dqkv W^T and dW = x^T dqkv
     rec = {"tool": "block_bench", "S": S, "chunk": C, "heads": H, "head_dim": d, "hidden": hidden, "offload": 1,
@@ -77,6 +87,9 @@ def main():
            "attn_tflops": f_attn / t_attn / 1e12, "block_tflops": (f_attn + f_proj) / t_block / 1e12,
            "block_tokens_per_s": S / t_block, "attn_tokens_per_s": S / t_attn,
            "launches_attn": l_attn, "launches_block": l_block,
+           "block_with_out_proj_step_s": t_block_o, "out_proj_flops": 6 * S * hidden * H * d,
+           "block_with_out_proj_tflops": (f_attn + f_proj + 6 * S * hidden * H * d) / t_block_o / 1e12,
+           "launches_block_with_out_proj": l_block_o, "dwo_finite": bool(torch.isfinite(dwo).all()),
            "dx_finite": bool(torch.isfinite(dx).all()), "dw_finite": bool(torch.isfinite(dw).all())}
     print(json.dumps(rec), flush=True)
     ctx.close()
