@@ -5,6 +5,7 @@ query heads and Hkv/p kv heads; that is a p = 1 call with those head counts (too
 d = 128 backward kernel (attn_bwd_q64) with host offload:
   c5: 70B layer at p = 8 -> S = 1,048,576, 8 q heads / 1 kv head (G = 8), d = 128, chunk 65,536 (u = 16)
   c3: 8B layer at p = 4  -> S = 2,097,152, 8 q heads / 2 kv heads (G = 4), d = 128, chunk 65,536 (u = 32)
+c5 also runs with the Q-outer backward order (include/fpdt.h fpdt_set_bwd_order).
 Checks: sampled rows of O, lse, dQ (first/last row of every chunk plus seeded random rows)
 against oracle/sampled.rows_dq, and the exact identities sum_j dK_j = 0, sum_j dV_j = sum over the group of sum_i
 dO_i on every kv head.  Bar: 1e-2 (north_star, bf16)."""
@@ -28,7 +29,7 @@ CASES = {
 D = 128
 
 
-def _run(S, hq, hkv, rows):
+def _run(S, hq, hkv, rows, order=0):
     from paper_2408_16978_b200 import _lib, fpdt
     torch.cuda.set_device(0)
     genlib = _lib.load_generator()
@@ -45,9 +46,11 @@ def _run(S, hq, hkv, rows):
     lse = torch.empty(S, hq, dtype=torch.float32, device="cuda")
     dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
     ctx = fpdt.FPDTContext()
+    ctx.set_bwd_order(order)
     fpdt.fpdt_attn_fwd(ctx, q, k, v, o, lse, S, hq, hkv, D, 1, K64, 1, fpdt.FPDT_BF16, 1)
     fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, S, hq, hkv, D, 1, K64, 1, fpdt.FPDT_BF16, 1)
     torch.cuda.synchronize()
+    assert ctx.stats()["bwd_order"] == order
     ctx.close()
     ridx = torch.tensor(rows, device="cuda")
     G = hq // hkv
@@ -64,14 +67,15 @@ def _run(S, hq, hkv, rows):
     return out
 
 
-@pytest.mark.parametrize("cfg", ["c5", "c3"])
-def test_fullsize_per_rank_gqa(cfg):
+# order 1: the GQA-aware Q-outer backward (fpdt_set_bwd_order), two pair kernels at a time on two streams
+@pytest.mark.parametrize("cfg,order", [("c5", 0), ("c3", 0), ("c5", 1)])
+def test_fullsize_per_rank_gqa(cfg, order):
     c = CASES[cfg]
     S, hq, hkv = c["S"], c["hq"], c["hkv"]
     rng = np.random.default_rng(1)
     rows = sorted(set([0, S - 1] + [m * K64 for m in range(S // K64)] + [m * K64 + K64 - 1 for m in range(S // K64)]
                       + rng.integers(0, S, c["n_random"]).tolist()))
-    got = _run(S, hq, hkv, rows)
+    got = _run(S, hq, hkv, rows, order)
     # identities on every kv head, over all S rows
     assert np.max(np.abs(got["dk_sum"]) / got["dk_abs"]) <= TOL["bf16"]
     assert np.max(np.abs(got["dv_sum"] - got["do_group_sum"]) / got["dv_abs"]) <= TOL["bf16"]
