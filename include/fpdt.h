@@ -186,6 +186,15 @@ int fpdt_set_residency(fpdt_ctx* ctx, int64_t kv_chunks, int64_t q_chunks);
 enum { FPDT_BWD_KV_OUTER = 0, FPDT_BWD_Q_OUTER = 1, FPDT_BWD_AUTO = 2 };
 int fpdt_set_bwd_order(fpdt_ctx* ctx, int order);
 
+/* The host-link bytes (host-to-device plus device-to-host) that the offloaded backward's chunk loop moves per rank
+ * in `order` (FPDT_BWD_KV_OUTER or FPDT_BWD_Q_OUTER), for the given shape, residency budget (kv_chunks, q_chunks)
+ * and sparsity plan (keep [n_chunks][n_chunks] host array as fpdt_set_sparsity, or NULL = dense): the model
+ * FPDT_BWD_AUTO compares.  Host-only arithmetic (no device, no context).  Errors: FPDT_ERR_ARG,
+ * FPDT_ERR_DIVISIBILITY / FPDT_ERR_UNSUPPORTED as fpdt_attn_fwd. */
+int fpdt_bwd_host_bytes(int order, int64_t s_local, int n_q_heads, int n_kv_heads, int head_dim, int64_t chunk_size,
+                        int world_size, int dtype, int64_t kv_chunks, int64_t q_chunks, const uint8_t* keep,
+                        int64_t n_chunks, int64_t* out);
+
 /* Message of the last non-OK status returned on this thread ("" if none). */
 const char* fpdt_last_error(void);
 

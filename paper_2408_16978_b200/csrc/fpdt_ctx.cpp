@@ -1631,6 +1631,20 @@ int fpdt_set_bwd_order(fpdt_ctx* ctx, int order) {
   });
 }
 
+int fpdt_bwd_host_bytes(int order, int64_t s_local, int n_q_heads, int n_kv_heads, int head_dim, int64_t chunk_size,
+                        int world_size, int dtype, int64_t kv_chunks, int64_t q_chunks, const uint8_t* keep,
+                        int64_t n_chunks, int64_t* out) {
+  return run([&] {
+    if (!out || (order != FPDT_BWD_KV_OUTER && order != FPDT_BWD_Q_OUTER) || kv_chunks < 0 || q_chunks < 0)
+      fail(FPDT_ERR_ARG, "bad arguments");
+    const Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, 1, chunk_size, world_size, dtype, 1, 0.f);
+    if (keep && n_chunks != c.u) fail(FPDT_ERR_ARG, "sparsity plan size differs from the chunk count");
+    const int64_t u = c.u;
+    auto kept = [&](int64_t i, int64_t j) { return i == j || !keep || keep[(size_t)(i * u + j)] != 0; };
+    *out = bwd_host_bytes(order, c, std::min(kv_chunks, u), std::min(q_chunks, u), kept);
+  });
+}
+
 int fpdt_get_stats(const fpdt_ctx* ctx, fpdt_stats* out) {
   if (!ctx || !out) return FPDT_ERR_ARG;
   *out = ctx->stats;

@@ -24,7 +24,7 @@ EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_a
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair", "fpdt_group_create",
             "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity", "fpdt_set_residency",
-            "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd",
+            "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes",
             "fpdt_selftest_softmax", "fpdt_selftest_reduce")
 
 
@@ -78,6 +78,9 @@ def _declare(lib):
     lib.fpdt_block_bwd.argtypes = [P, P, P, P, P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int, c_int64, c_int,
                                    c_int, c_int, c_float, P]
     lib.fpdt_block_bwd.restype = c_int
+    lib.fpdt_bwd_host_bytes.argtypes = [c_int, c_int64, c_int, c_int, c_int, c_int64, c_int, c_int, c_int64, c_int64,
+                                        P, c_int64, ctypes.POINTER(c_int64)]
+    lib.fpdt_bwd_host_bytes.restype = c_int
     lib.fpdt_set_bwd_order.argtypes = [P, c_int]
     lib.fpdt_set_bwd_order.restype = c_int
     lib.fpdt_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
@@ -241,6 +244,21 @@ def fpdt_block_bwd(ctx: FPDTContext, x, w_qkv, o, dout, dx, dw_qkv, s_local: int
                                 _ptr(dw_qkv), _ptr(dw_o),
                                 s_local, hidden, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size,
                                 dtype, offload, softmax_scale, _stream(stream)))
+
+
+def fpdt_bwd_host_bytes(order: int, s_local: int, n_q_heads: int, n_kv_heads: int, head_dim: int, chunk_size: int,
+                        world_size: int, dtype: int, kv_chunks: int = 0, q_chunks: int = 0, keep=None) -> int:
+    """Host-link bytes of the backward chunk loop in `order` (the model FPDT_BWD_AUTO compares; host-only)."""
+    out = c_int64()
+    plan, n = None, 0
+    if keep is not None:
+        import numpy as np
+        plan = np.ascontiguousarray(np.asarray(keep, dtype=np.uint8))
+        n = plan.shape[0]
+    _check(lib().fpdt_bwd_host_bytes(order, s_local, n_q_heads, n_kv_heads, head_dim, chunk_size, world_size, dtype,
+                                     kv_chunks, q_chunks, None if plan is None else c_void_p(plan.ctypes.data), n,
+                                     ctypes.byref(out)))
+    return out.value
 
 
 def dtype_code(torch_dtype) -> int:

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import fpdt_inputs as gen
-from fpdt_testlib import TOL, inputs, oracle_full, rel_err, run_cuda
+from fpdt_testlib import TOL, expected_bwd_bytes, inputs, oracle_full, rel_err, run_cuda
 
 pytestmark = pytest.mark.gpu
 
@@ -18,40 +18,6 @@ KV_OUTER, Q_OUTER, AUTO = 0, 1, 2
 # dQ of the two orders: the same fp32 sums in a different reduce-add order, then bf16 RNE; one rounding flip on the
 # largest element is 2^-8 of the max (normwise), so the bound is that ulp
 DQ_ORDER_TOL = 2.0 ** -8
-
-
-def expected_bwd_bytes(order, u, C, Hq, Hkv, d, eb, keep=None, rkv=0, rq=0):
-    """(H2D, D2H) bytes of the backward chunk loop, world size 1, excluding the dO offload of the preamble."""
-    kv, qc = C * 2 * Hkv * d * eb, C * Hq * d * eb
-    dqc, dkvc = C * Hq * d * 4, C * 2 * Hkv * d * 4
-    kept = lambda i, j: i == j or keep is None or bool(keep[i][j])
-    kres = lambda j: j < rkv
-    qres = lambda i: i >= u - rq
-    h2d = d2h = 0
-    if order == KV_OUTER:
-        started = set()
-        for j in range(u):
-            h2d += 0 if kres(j) else kv
-            for i in range(j, u):
-                if not kept(i, j):
-                    continue
-                if not qres(i):
-                    h2d += 2 * qc + (dqc if i in started else 0)
-                    d2h += dqc if i != j else 0
-                started.add(i)
-    else:
-        last = {j: max(i for i in range(j, u) if kept(i, j)) for j in range(u)}
-        started = set()
-        for i in range(u):
-            h2d += 0 if qres(i) else 2 * qc
-            for j in range(i + 1):
-                if not kept(i, j):
-                    continue
-                if not kres(j):
-                    h2d += kv + (dkvc if j in started else 0)
-                    d2h += dkvc if i != last[j] else 0
-                started.add(j)
-    return h2d, d2h
 
 
 def run_order(x, C, dtype, order, keep=None, residency=None):
