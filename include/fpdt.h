@@ -251,6 +251,12 @@ int fpdt_selftest_softmax(int what, int threads, int every, int iters, float* ou
  * out[0] = SM cycles per tile (device fp32).  Returns 0 or an error code. */
 int fpdt_selftest_reduce(int mode, int iters, int inflight, int shared_target, float* gbuf, float* out, void* stream);
 
+/* Diagnostic micro-benchmark of the CTA-pair MMA (groundwork for a CTA-pair backward): 148 CTAs in
+ * clusters of 2, one per SM; mode 0: every CTA issues SS tcgen05.mma.cta_group::1 M=128 N=n K=16; mode 1: each
+ * pair's leader issues SS tcgen05.mma.cta_group::2 M=256 N=n K=16 (each CTA supplies 128 rows of A and n/2 rows of B).
+ * n: 16..256, multiple of 16.  out[0] = SM cycles per MMA (device fp32).  Returns 0, FPDT_ERR_ARG or a CUDA error. */
+int fpdt_selftest_pair(int mode, int n, int iters, float* out, void* stream);
+
 /* Diagnostic: launch ONE bf16 chunk-pair kernel directly (no scheduler) on caller device buffers, rows
  * [0, n_rows) of q/k/v/dout against each other (the diagonal pair when causal = 1).
  *   which 0 (forward):  out0 = o bf16 [n_rows][n_q_heads][head_dim], out1 = log2-domain lse fp32 [n_q_heads][n_rows]
