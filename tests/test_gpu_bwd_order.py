@@ -107,12 +107,12 @@ def test_q_outer_sparse_and_resident(residency):
     assert (got["bwd_h2d"], got["bwd_d2h"]) == (h2d, d2h + do_off)
 
 
-@pytest.mark.parametrize("p,Hq,Hkv", [(2, 8, 2), (4, 8, 4)])
+@pytest.mark.parametrize("p,Hq,Hkv", [(2, 8, 2), (4, 8, 4), (8, 16, 8)])
 def test_q_outer_multirank(p, Hq, Hkv):
     """p > 1 through the local group: dq_i and (dk_j, dv_j) return by separate all-to-alls; world-size invariance
     against the p = 1 paper-order run (bitwise for O, lse, dK, dV) and oracle parity."""
     from test_gpu_multirank import run_group
-    S, d, C = 2048, 128, 512
+    S, d, C = 2048 * max(1, p // 4), 128, 512 * max(1, p // 4)   # p = 8: the 70B shape, one kv head per rank
     x = gen.make_inputs("drift", 35, S, Hq, Hkv, d)
     base = run_group(x, 1, C, "bf16", 1)
     stats = {}
