@@ -7,7 +7,7 @@ work — every chunk pair, offload and prefetch included — is exactly a p = 1 
 is what this tool runs.  Only the all-to-alls are missing (one B200 on this pool), so the numbers are the
 per-GPU compute + host-offload part of the multi-GPU configs, not a multi-GPU measurement.
 
-    python tools/rank_workloads.py [--only c3 c4 c5] [--steps 1]
+    python tools/rank_workloads.py [--only c2p1 c2p8 c3 c4 c5] [--steps 1]
 
 Prints one JSON line per (config, chunk): step seconds (CUDA events), pair-kernel seconds, TFLOPS/GPU,
 host bytes and host-link GB/s, device and pinned-host footprint.
@@ -31,6 +31,12 @@ K = 1024
 M = 1024 * 1024
 # (name, BASELINE.json config text, S, Hq, Hkv, d, p, chunks)
 WORKLOADS = [
+    # configs[1] (GPT-2.7B, 32 heads x 80, S = 512K, C = 64K) per rank at p = 1, 2, 4, 8: the compute side of its
+    # strong scaling (the all-to-alls excluded)
+    ("c2p1", "GPT-2.7B layer (32 heads, d=80), S=512K, one GPU", 512 * K, 32, 32, 80, 1, [64 * K]),
+    ("c2p2", "GPT-2.7B layer (32 heads, d=80), S=512K across 2 GPUs", 512 * K, 32, 32, 80, 2, [64 * K]),
+    ("c2p4", "GPT-2.7B layer (32 heads, d=80), S=512K across 4 GPUs", 512 * K, 32, 32, 80, 4, [64 * K]),
+    ("c2p8", "GPT-2.7B layer (32 heads, d=80), S=512K across 8 GPUs", 512 * K, 32, 32, 80, 8, [64 * K]),
     ("c3", "Llama-3 8B layer (32 q / 8 kv heads, d=128), S=2M across 4 GPUs, host-offloaded KV", 2 * M, 32, 8, 128,
      4, [64 * K]),
     ("c4", "13B layer (40 heads, d=128), S=4M across 8 GPUs, chunk-size sweep 32K-256K", 4 * M, 40, 40, 128, 8,
