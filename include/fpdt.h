@@ -129,7 +129,8 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
  *          per token, head-major), computed per chunk as soon as the chunk's o is final; NULL = no output projection
  *   o, lse as fpdt_attn_fwd (o is always written: the backward needs it); y [s_local][hidden] (output; with w_o)
  *   dout   without w_o: dL/do [s_local][n_q_heads][head_dim]; with w_o: dL/dy [s_local][hidden], from which the
- *          library forms dL/do = dy w_o^T and dw_o = o^T dy (fp32 [Hq d][hidden], output, overwritten)
+ *          library forms dL/do = dy w_o^T (held in library device memory, s_local * Hq * head_dim elements, for
+ *          the duration of the call) and dw_o = o^T dy (fp32 [Hq d][hidden], output, overwritten)
  *   dx [s_local][hidden] (output, overwritten), dw_qkv fp32 [hidden][(Hq + 2 Hkv) d] (output, overwritten: the sum
  *   over this rank's rows of x^T dqkv; a data-parallel caller all-reduces dw_qkv and dw_o).
  * x, w_qkv, w_o must be unchanged between the two calls, and w_o NULL in both or in neither.  All pointers are device pointers; dtype FPDT_BF16 (x, w, dx
