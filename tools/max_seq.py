@@ -31,6 +31,8 @@ def main():
     ap.add_argument("--d", type=int, default=80)
     ap.add_argument("--chunk", type=int, default=65536)
     ap.add_argument("--s", type=int, nargs="+", default=[1 << 20, 2 << 20, 3 << 20])
+    ap.add_argument("--steps", type=int, default=1, help="steps per length (the first includes pinned allocation)")
+    ap.add_argument("--bwd-order", default="kv", choices=["kv", "q", "auto"])
     args = ap.parse_args()
     torch.cuda.set_device(0)
     genlib = _lib.load_generator()
@@ -48,16 +50,21 @@ def main():
             o = torch.empty_like(q)
             dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
             ctx = fpdt.FPDTContext()
-            torch.cuda.synchronize()
-            t0 = time.perf_counter()
-            fpdt.fpdt_attn_fwd(ctx, q, k, v, o, None, S, H, Hkv, d, 1, C, 1, fpdt.FPDT_BF16, 1)
-            fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, S, H, Hkv, d, 1, C, 1, fpdt.FPDT_BF16, 1)
-            torch.cuda.synchronize()
-            dt = time.perf_counter() - t0
+            ctx.set_bwd_order({"kv": 0, "q": 1, "auto": 2}[args.bwd_order])
+            steps = []
+            for _ in range(args.steps):
+                torch.cuda.synchronize()
+                t0 = time.perf_counter()
+                fpdt.fpdt_attn_fwd(ctx, q, k, v, o, None, S, H, Hkv, d, 1, C, 1, fpdt.FPDT_BF16, 1)
+                fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, S, H, Hkv, d, 1, C, 1, fpdt.FPDT_BF16, 1)
+                torch.cuda.synchronize()
+                steps.append(time.perf_counter() - t0)
+            dt = steps[-1]
             st = ctx.stats()
             flops = 14 * d * H * S * (S + 1) / 2
             ok = bool(torch.isfinite(dq[-1].float()).all() and torch.isfinite(o[-1].float()).all())
-            rec.update(ok=ok, step_s=dt, tflops=flops / dt / 1e12, tokens_per_s=S / dt,
+            rec.update(ok=ok, steps_s=steps, bwd_order=["kv_outer", "q_outer"][st["bwd_order"]],
+                       host_dkv_pinned_bytes=st["host_dkv_bytes"], step_s=dt, tflops=flops / dt / 1e12, tokens_per_s=S / dt,
                        device_bytes_caller=sum(t.numel() * 2 for t in (q, k, v, do, o, dq, dk, dv)),
                        device_bytes_library=st["device_bytes"], host_pinned_bytes=st["host_arena_bytes"])
             ctx.close()
