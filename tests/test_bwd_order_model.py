@@ -44,3 +44,31 @@ def test_model_errors():
     assert e.value.code == fpdt.FPDT_ERR_DIVISIBILITY
     with pytest.raises(fpdt.FpdtError):
         fpdt.fpdt_bwd_host_bytes(0, 4096, 4, 4, 64, 1024, 1, 0, keep=np.ones((3, 3), bool))
+
+
+@pytest.mark.parametrize("args,code", [
+    ((0, 0, 4, 4, 64, 1024, 1, 0), "FPDT_ERR_ARG"),            # empty shard
+    ((0, 4096, 0, 4, 64, 1024, 1, 0), "FPDT_ERR_ARG"),         # no heads
+    ((0, 4096, 4, 4, 96, 1024, 1, 0), "FPDT_ERR_UNSUPPORTED"),  # head_dim without a kernel
+    ((0, 4096, 4, 4, 64, 1024, 1, 7), "FPDT_ERR_UNSUPPORTED"),  # dtype
+    ((0, 4096, 4, 4, 64, 1000, 1, 0), "FPDT_ERR_DIVISIBILITY"),  # C % 256
+    ((0, 4096, 4, 4, 64, 1024, 3, 0), "FPDT_ERR_DIVISIBILITY"),  # C % p
+    ((0, 4096, 6, 4, 64, 1024, 1, 0), "FPDT_ERR_DIVISIBILITY"),  # Hq % Hkv
+    ((0, 4096, 4, 2, 64, 1024, 4, 0), "FPDT_ERR_DIVISIBILITY"),  # Hkv % p
+])
+def test_shape_validation_host_only(args, code):
+    """The divisibility / support rules of include/fpdt.h on the host path every call shares."""
+    from paper_2408_16978_b200 import fpdt
+    with pytest.raises(fpdt.FpdtError) as e:
+        fpdt.fpdt_bwd_host_bytes(*args)
+    assert e.value.code == getattr(fpdt, code)
+
+
+def test_single_chunk_degenerate():
+    """u = 1: the backward is one diagonal pair in either order and moves nothing through the host but kv_0 and
+    q_0, dO_0 once each."""
+    from paper_2408_16978_b200 import fpdt
+    C, Hq, Hkv, d = 1024, 4, 2, 64
+    for order in (0, 1):
+        got = fpdt.fpdt_bwd_host_bytes(order, C, Hq, Hkv, d, C, 1, 0)
+        assert got == C * 2 * Hkv * d * 2 + 2 * C * Hq * d * 2
