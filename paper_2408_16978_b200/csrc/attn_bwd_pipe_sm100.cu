@@ -14,8 +14,8 @@
 // the tensor pipe, is the scarce resource here (128 B/clk/SM; an SS-MMA with M = 128, N <= 128 already needs all
 // of it), so per query tile only dQ = dS K (A = the dS smem tile) reads two smem operands.  Shared-memory bytes per
 // tile (d = 80): TMA Q, dO 40K + MMA operands 172K + dS 32K + dQ staging 80K.
-// Element-wise math uses packed f32x2 FMA-pipe instructions (FFMA2/FADD2/FMUL2); a fraction of the
-// exponentials run as a polynomial on the FMA pipe (FA4-style MUFU offload).
+// Element-wise math uses packed f32x2 FMA-pipe instructions (FFMA2/FADD2/FMUL2); the exponentials all run on MUFU
+// (an FA4-style polynomial offload of a fraction of them measured slower here, FPDT_BWD_POLY_EVERY).
 //
 // Warps (512 threads = 4 warpgroups, registers rebalanced with setmaxnreg):
 //   WG0 (0-3)   softmax-gradient, query columns [0,64)   (thread = key row = TMEM lane); final dK    168 regs
@@ -49,7 +49,10 @@ static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs -
                        // 6 dQ reduce every other tile only, 8 only even key tiles reduce
 #endif
 #ifndef FPDT_BWD_POLY_EVERY
-#define FPDT_BWD_POLY_EVERY 4  // one exponential pair in FPDT_BWD_POLY_EVERY goes to the FMA-pipe polynomial
+// one exponential pair in FPDT_BWD_POLY_EVERY goes to the FMA-pipe polynomial; 0 = all on MUFU.  Measured on the
+// C = 64K, 32 x 80 diagonal pair (tools/gpu_poly_sweep.sh): 4 -> 848-858, 8 -> 868, 16 -> 871, 0 -> 872-875 TFLOP/s
+// (the backward is not MUFU-bound, so the extra FMA-pipe instructions only cost issue slots)
+#define FPDT_BWD_POLY_EVERY 0
 #endif
 
 template <int D>
@@ -342,7 +345,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
               __ffma2_rn(make_float2(p[i + 2], p[i + 3]), make_float2(sl2, sl2), make_float2(-l.z, -l.w));
           p[i] = ex2(x0.x);
           p[i + 1] = ex2(x0.y);
-          if ((i / 4) % (FPDT_BWD_POLY_EVERY / 2) == (FPDT_BWD_POLY_EVERY / 2) - 1) {
+          if (FPDT_BWD_POLY_EVERY >= 2 && (i / 4) % (FPDT_BWD_POLY_EVERY / 2 > 0 ? FPDT_BWD_POLY_EVERY / 2 : 1) == (FPDT_BWD_POLY_EVERY / 2) - 1) {
             const float2 e = ex2_poly2(x1);
             p[i + 2] = e.x;
             p[i + 3] = e.y;

@@ -348,7 +348,7 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
               __ffma2_rn(make_float2(p[i + 2], p[i + 3]), make_float2(sl2, sl2), make_float2(-l.z, -l.w));
           p[i] = ex2(x0.x);
           p[i + 1] = ex2(x0.y);
-          if ((i / 4) % (FPDT_BWD_POLY_EVERY / 2) == (FPDT_BWD_POLY_EVERY / 2) - 1) {
+          if (FPDT_BWD_POLY_EVERY >= 2 && (i / 4) % (FPDT_BWD_POLY_EVERY / 2 > 0 ? FPDT_BWD_POLY_EVERY / 2 : 1) == (FPDT_BWD_POLY_EVERY / 2) - 1) {
             const float2 e = ex2_poly2(x1);
             p[i + 2] = e.x;
             p[i + 3] = e.y;
