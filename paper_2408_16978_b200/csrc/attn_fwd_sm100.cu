@@ -18,7 +18,8 @@
 // also guarantees PV_t_j has finished (so the softmax warps may rescale O_t in TMEM then).
 // Softmax (the bottleneck at d <= 80: per (row, key) the exponential costs more than the 4d MMA FLOPs):
 //   * row max with three-input FMNMX3, scale/subtract with packed FFMA2;
-//   * a quarter of the exponentials (every 4th pair) as a degree-3 polynomial on the FMA pipe, the rest on MUFU;
+//   * a fifth (d = 80) / an eighth (d = 128) of the exponential pairs as a degree-3 polynomial on the FMA pipe, the
+//     rest on MUFU (FwdCfg::kPolyEvery);
 //   * d = 80: the row sum of P comes from the tensor core — each V stage carries a 16-column atom of ones,
 //     so PV has N = 96 and O column 80 accumulates sum(P) with the same rescaling as O (and the same bf16 P
 //     the numerator uses); d = 64 / 128 sum with packed FADD2.
@@ -45,8 +46,15 @@ constexpr float kRescaleThreshold = 8.0f;
 #ifndef FPDT_FWD_EX2_F16
 #define FPDT_FWD_EX2_F16 0  // 1: MUFU exponentials as ex2.approx.f16x2 (2x MUFU rate, more instructions: measured 924 vs 956 TF)
 #endif
+// One exponential pair in N on the FMA pipe, the rest on MUFU (0 = all MUFU), per head_dim.  Measured on the
+// C = 64K, 32-head diagonal pair (tools/gpu_poly_sweep_fwd.sh, two sessions; run-to-run noise about 2%):
+//   d = 80:  0, 1, 2, 3 -> 800, 669, 811, 865; 4 -> 940-948 / 966-985; 5 -> 954-955 / 957-987; 6 -> 915-935; 8 -> 902-941
+//   d = 128: 0 -> 1147-1149; 4 -> 1142-1145; 5 -> 1147-1148; 6 -> 1151-1159; 8 -> 1147-1162; 12, 16 -> 1139-1152
 #ifndef FPDT_FWD_POLY_EVERY
-#define FPDT_FWD_POLY_EVERY 4  // one exponential pair in 4 on the FMA pipe (measured: 0, 1, 2, 3, 4 -> 800, 669, 811, 865, 873 TF)
+#define FPDT_FWD_POLY_EVERY 5
+#endif
+#ifndef FPDT_FWD_POLY_EVERY_D128
+#define FPDT_FWD_POLY_EVERY_D128 8
 #endif
 
 template <int D>
@@ -59,6 +67,7 @@ struct FwdCfg {
   static constexpr bool kSepP = 2 * 128 + 64 + 2 * NO <= 512;
   static constexpr uint32_t tP = 256, tO0 = kSepP ? 320 : 256, tOstride = kSepP ? NO : 128;
   static constexpr int kStages = (D == 128) ? 2 : 3;
+  static constexpr int kPolyEvery = (D == 128) ? FPDT_FWD_POLY_EVERY_D128 : FPDT_FWD_POLY_EVERY;
   static constexpr int kQBytes = 2 * T::kBytes;
   static constexpr int kOnes = kSumMMA ? 128 * 16 * 2 : 0;      // the ones atom right after each V tile
   static constexpr int kStageBytes = 2 * T::kBytes + kOnes;       // K + V (+ ones)
@@ -113,8 +122,8 @@ __device__ __forceinline__ float2 ex2_f16x2(float2 x) {
 }
 
 // P = exp2(x*sl2 - mb) for the 128 columns of a row, packed to bf16 and stored to TMEM columns [tS, tS+64); returns
-// the sum of the fp32 values when kSum (else 0).  kPoly: every FPDT_FWD_POLY_EVERY-th pair on the FMA pipe.
-template <bool kPoly, bool kSum, bool kStore = true>
+// the sum of the fp32 values when kSum (else 0).  kEvery > 0: every kEvery-th pair on the FMA pipe.
+template <int kEvery, bool kSum, bool kStore = true>
 __device__ __forceinline__ float exp_pack_store(const float* x, float sl2, float mb, uint32_t tS,
                                                 uint32_t* pko = nullptr) {
   float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
@@ -127,7 +136,7 @@ __device__ __forceinline__ float exp_pack_store(const float* x, float sl2, float
     for (int i = 0; i < 32; i += 2) {
       const float2 e = __ffma2_rn(make_float2(x[c + i], x[c + i + 1]), s2, nm);
       float2 pr;
-      if (kPoly && FPDT_FWD_POLY_EVERY > 0 && (i / 2) % FPDT_FWD_POLY_EVERY == FPDT_FWD_POLY_EVERY - 1) {
+      if (kEvery > 0 && (i / 2) % (kEvery > 0 ? kEvery : 1) == kEvery - 1) {
         pr = ex2_poly2(e);
       } else if (FPDT_FWD_EX2_F16) {
         pr = ex2_f16x2(e);
@@ -421,16 +430,16 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
       if constexpr (C::kSepP) {
         // P in registers first; then the shared P buffer: P_0(j) after PV_1(j-1) has read it, P_1(j) after PV_0(j)
         uint32_t pk[64];
-        sum = any_masked ? exp_pack_store<false, kSumHere, false>(x, sl2, mb, 0, pk)
-                         : exp_pack_store<true, kSumHere, false>(x, sl2, mb, 0, pk);
+        sum = any_masked ? exp_pack_store<0, kSumHere, false>(x, sl2, mb, 0, pk)
+                         : exp_pack_store<C::kPolyEvery, kSumHere, false>(x, sl2, mb, 0, pk);
         if (t == 0 && j > 0) mbar_wait(smem_u32(&bar_pvdone[1]), (j - 1) & 1);
         if (t == 1) mbar_wait(smem_u32(&bar_pvdone[0]), j & 1);
         tc_fence_after();
 #pragma unroll
         for (int c = 0; c < 64; c += 16) tmem_st16(tPw + c, pk + c);
       } else {
-        sum = any_masked ? exp_pack_store<false, kSumHere>(x, sl2, mb, tPw)
-                         : exp_pack_store<true, kSumHere>(x, sl2, mb, tPw);
+        sum = any_masked ? exp_pack_store<0, kSumHere>(x, sl2, mb, tPw)
+                         : exp_pack_store<C::kPolyEvery, kSumHere>(x, sl2, mb, tPw);
       }
       if constexpr (kSumHere) l_run += sum;
       if ((warp & 3) == 0 && lane == 0) TRACE(10 + 4 * t, j);
