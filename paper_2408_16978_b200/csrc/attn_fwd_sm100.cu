@@ -53,6 +53,9 @@ constexpr float kRescaleThreshold = 8.0f;
 #ifndef FPDT_FWD_POLY_EVERY
 #define FPDT_FWD_POLY_EVERY 5
 #endif
+#ifndef FPDT_FWD_STAGES
+#define FPDT_FWD_STAGES 3  // K/V ring depth at d <= 80 (d = 128: 2, the shared-memory limit)
+#endif
 #ifndef FPDT_FWD_POLY_EVERY_D128
 #define FPDT_FWD_POLY_EVERY_D128 8
 #endif
@@ -66,7 +69,7 @@ struct FwdCfg {
   // softmax of S_t(j) runs; d = 128 keeps P aliased onto S_t (S_t(j+1) then waits for PV_t(j))
   static constexpr bool kSepP = 2 * 128 + 64 + 2 * NO <= 512;
   static constexpr uint32_t tP = 256, tO0 = kSepP ? 320 : 256, tOstride = kSepP ? NO : 128;
-  static constexpr int kStages = (D == 128) ? 2 : 3;
+  static constexpr int kStages = (D == 128) ? 2 : FPDT_FWD_STAGES;
   static constexpr int kPolyEvery = (D == 128) ? FPDT_FWD_POLY_EVERY_D128 : FPDT_FWD_POLY_EVERY;
   static constexpr int kQBytes = 2 * T::kBytes;
   static constexpr int kOnes = kSumMMA ? 128 * 16 * 2 : 0;      // the ones atom right after each V tile
