@@ -41,7 +41,14 @@ using namespace ptx;
 constexpr int kThreads = 512;
 // setmaxnreg budget: the softmax warpgroups grow only by what WG2 / WG3 give back (pool = launch allocation)
 constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 128
-constexpr int kRegsSoftmax = 168, kRegsDQ = 104, kRegsCtl = 72;
+// measured (tools/gpu_regs_sweep.sh, d = 80 C = 64K pair): 168/104/72 -> 872-876, 176/96/64 -> 863-865,
+// 160/120/72 -> 837-841 TFLOP/s
+#ifndef FPDT_BWD_REGS_SOFTMAX
+#define FPDT_BWD_REGS_SOFTMAX 168
+#define FPDT_BWD_REGS_DQ 104
+#define FPDT_BWD_REGS_CTL 72
+#endif
+constexpr int kRegsSoftmax = FPDT_BWD_REGS_SOFTMAX, kRegsDQ = FPDT_BWD_REGS_DQ, kRegsCtl = FPDT_BWD_REGS_CTL;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
 #ifndef FPDT_BWD_EXP
 #define FPDT_BWD_EXP 0  // timing experiments only (wrong results): 1 no dQ reduce, 2 no dQ staging/reduce,

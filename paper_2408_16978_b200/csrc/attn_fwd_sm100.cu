@@ -40,7 +40,12 @@ constexpr int kThreads = 384;
 // setmaxnreg budget: the CTA's register pool is what the launch allocated (kLaunchRegs per thread); the two
 // softmax warpgroups may only grow by what WG2 gives back (an over-subscribed setmaxnreg.inc never returns)
 constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 168
-constexpr int kRegsSoftmax = 200, kRegsOther = 88;
+// measured (tools/gpu_regs_sweep.sh, d = 80 C = 64K pair): 200/88 -> 958-988, 208/88 -> 943-968 TFLOP/s
+#ifndef FPDT_FWD_REGS_SOFTMAX
+#define FPDT_FWD_REGS_SOFTMAX 200
+#define FPDT_FWD_REGS_OTHER 88
+#endif
+constexpr int kRegsSoftmax = FPDT_FWD_REGS_SOFTMAX, kRegsOther = FPDT_FWD_REGS_OTHER;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (kLaunchRegs - kRegsOther), "register pool");
 constexpr float kRescaleThreshold = 8.0f;
 #ifndef FPDT_FWD_EX2_F16
