@@ -32,7 +32,14 @@ using namespace ptx;
 
 constexpr int kThreads = 512;
 constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 128
-constexpr int kRegsSoftmax = 168, kRegsDQ = 104, kRegsCtl = 72;
+// measured (tools/gpu_regs_q64.sh, d = 128 C = 64K pair): 168/104/72 -> ~1016, 160/120/72 -> 1012-1015,
+// 176/96/64 -> 1002-1006, 184/88/56 -> 993-996 TFLOP/s
+#ifndef FPDT_Q64_REGS_SOFTMAX
+#define FPDT_Q64_REGS_SOFTMAX 168
+#define FPDT_Q64_REGS_DQ 104
+#define FPDT_Q64_REGS_CTL 72
+#endif
+constexpr int kRegsSoftmax = FPDT_Q64_REGS_SOFTMAX, kRegsDQ = FPDT_Q64_REGS_DQ, kRegsCtl = FPDT_Q64_REGS_CTL;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
 #ifndef FPDT_BWD_POLY_EVERY
 #define FPDT_BWD_POLY_EVERY 4
