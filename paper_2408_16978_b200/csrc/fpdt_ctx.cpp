@@ -750,6 +750,40 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
 }
 
 // ------------------------------------------------------------------------------------------ backward
+// Arguments of the backward pair kernel for (query chunk i, key chunk j) of the offloaded schedule, both
+// loop orders: q/dO/k/v views, the chunk's saved lse2 and D, its fp32 dq accumulator and dK/dV accumulators.  The
+// caller sets the final-output pointers (dk_out, dv_out, kv_out_ld, kv_out_head0).
+BwdArgs pair_bwd_args(const Config& c, const HeadView& qi, const HeadView& doi, const HeadView& kj, const HeadView& vj,
+                      int64_t q_row0, int64_t kv_row0, int64_t i, int64_t j, const float* lse_save, const float* Dh,
+                      float* dq_acc, float* dk_acc, float* dv_acc, bool acc_init, bool kv_final) {
+  BwdArgs a;
+  a.q = qi;
+  a.dout = doi;
+  a.k = kj;
+  a.v = vj;
+  a.q_row0 = q_row0;
+  a.kv_row0 = kv_row0;
+  a.n_q_rows = (int)c.C;
+  a.n_kv_rows = (int)c.C;
+  a.q_pos0 = i * c.C;
+  a.kv_pos0 = j * c.C;
+  a.causal = 1;
+  a.hq = c.hq;
+  a.G = c.G;
+  a.scale = c.scale;
+  a.scale_log2 = c.scale * 1.4426950408889634f;
+  a.lse2 = lse_save + i * c.C;
+  a.Dstat = Dh + i * c.C;
+  a.stat_ld = c.S;
+  a.dq_acc = dq_acc;  // head-major [hq][C][d]
+  a.dq_head_stride = c.C * c.d;
+  a.dk_acc = dk_acc;
+  a.dv_acc = dv_acc;
+  a.kv_acc_init = acc_init;
+  a.kv_final = kv_final;
+  return a;
+}
+
 // Q-outer chunk loop of the offloaded backward (fpdt_set_bwd_order FPDT_BWD_Q_OUTER).  The pair
 // kernels and their arguments are the paper order's; only the loop nesting and what round-trips the host
 // differ: for query chunk i (outer) fetch q_i, dO_i once and keep the fp32 dq_i accumulator on the device; for each
@@ -766,7 +800,6 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
   const int hcomb = hq + 2 * hkv;
   const size_t row_q = (size_t)hq * d * eb, row_kv2 = (size_t)2 * hkv * d * eb;
   const size_t dkv_elems = (size_t)C * 2 * hkv * d, dkv_bytes = dkv_elems * 4;
-  const float sl2 = c.scale * 1.4426950408889634f;
   float* lse_save = (float*)ctx->bufs[B_LSESAVE].ptr;
   float* Dh = (float*)ctx->bufs[B_D].ptr;
   const HostLayout hl = host_layout(c);
@@ -918,31 +951,8 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
         vj = {kvs[sl], C, 2 * hkv, hkv};
         acc = dkvs[sl];
       }
-      BwdArgs a;
-      a.q = qi;
-      a.dout = doi;
-      a.k = kj;
-      a.v = vj;
-      a.q_row0 = q_row0;
-      a.kv_row0 = kv_row0;
-      a.n_q_rows = (int)C;
-      a.n_kv_rows = (int)C;
-      a.q_pos0 = i * C;
-      a.kv_pos0 = j * C;
-      a.causal = 1;
-      a.hq = hq;
-      a.G = c.G;
-      a.scale = c.scale;
-      a.scale_log2 = sl2;
-      a.lse2 = lse_save + i * C;
-      a.Dstat = Dh + i * C;
-      a.stat_ld = c.S;
-      a.dq_acc = dqi;  // head-major [hq][C][d]
-      a.dq_head_stride = C * d;
-      a.dk_acc = acc;
-      a.dv_acc = acc + (size_t)C * hkv * d;
-      a.kv_acc_init = first;
-      a.kv_final = fin;
+      BwdArgs a = pair_bwd_args(c, qi, doi, kj, vj, q_row0, kv_row0, i, j, lse_save, Dh, dqi, acc,
+                                acc + (size_t)C * hkv * d, first, fin);
       int part = 0;
       if (p == 1) {
         a.dk_out = (uint8_t*)dk + (size_t)j * C * c.Hkv * d * eb;
@@ -1291,31 +1301,8 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
           doi = {dos[sl], C, hq, 0};
           dqi = dqs[sl];
         }
-        BwdArgs a;
-        a.q = qi;
-        a.dout = doi;
-        a.k = kj;
-        a.v = vj;
-        a.q_row0 = q_row0;
-        a.kv_row0 = kv_row0;
-        a.n_q_rows = (int)C;
-        a.n_kv_rows = (int)C;
-        a.q_pos0 = i * C;
-        a.kv_pos0 = j * C;
-        a.causal = 1;
-        a.hq = hq;
-        a.G = c.G;
-        a.scale = c.scale;
-        a.scale_log2 = sl2;
-        a.lse2 = lse_save + i * C;
-        a.Dstat = Dh + i * C;
-        a.stat_ld = c.S;
-        a.dq_acc = dqi;  // head-major [hq][C][d]
-        a.dq_head_stride = C * d;
-        a.dk_acc = dk_acc;
-        a.dv_acc = dv_acc;
-        a.kv_acc_init = (i == j);
-        a.kv_final = (i == last_i);
+        BwdArgs a = pair_bwd_args(c, qi, doi, kj, vj, q_row0, kv_row0, i, j, lse_save, Dh, dqi, dk_acc, dv_acc,
+                                  i == j, i == last_i);
         set_kv_out(a, j);
         launch_bwd(ctx, c, a, cs);
         if (qres) {
