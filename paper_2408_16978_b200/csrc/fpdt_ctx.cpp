@@ -160,6 +160,10 @@ struct fpdt_ctx {
   cudaStream_t s_comp2 = nullptr;
   cublasHandle_t blas = nullptr;  // fused QKV projection GEMMs (created by the first block call)
   int qo_streams = 2;  // FPDT_BWD_QO_STREAMS (1 or 2)
+  // scheduler stress (debug, FPDT_STRESS_NS > 0): a random sleep kernel of up to stress_ns ns goes onto the stream of
+  // every copy, all-to-all, GEMM and attention launch, before it (SURVEY §4 tier 5)
+  uint32_t stress_ns = 0;
+  uint64_t stress_state = 0x9E3779B97F4A7C15ull;
   cudaEvent_t ev_qo_free[4] = {}, ev_qo_filled[4] = {}, ev_qo_done[4] = {}, ev_qo_send[3] = {}, ev_fork = nullptr,
               ev_join = nullptr;
   uint8_t* host = nullptr;
@@ -252,6 +256,15 @@ void ensure_events(std::vector<cudaEvent_t>& v, size_t n) {
 }
 
 void rec(cudaEvent_t e, cudaStream_t s) { FPDT_CHECK_CUDA(cudaEventRecord(e, s)); }
+// scheduler stress: a sleep of a random length in [0, stress_ns) on stream s (no-op unless FPDT_STRESS_NS is set)
+void stress(fpdt_ctx* ctx, cudaStream_t s) {
+  if (!ctx->stress_ns) return;
+  uint64_t& x = ctx->stress_state;
+  x ^= x << 13;
+  x ^= x >> 7;
+  x ^= x << 17;
+  FPDT_CHECK_LAUNCH(launch_stress_sleep((uint32_t)(x % ctx->stress_ns), s));
+}
 void wait(cudaStream_t s, cudaEvent_t e) { FPDT_CHECK_CUDA(cudaStreamWaitEvent(s, e, 0)); }
 
 Config make_config(int64_t s_local, int Hq, int Hkv, int d, int causal, int64_t C, int p, int dtype, int offload,
@@ -360,14 +373,17 @@ void ensure_host(fpdt_ctx* ctx, size_t bytes) {
 }
 
 void h2d(fpdt_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  stress(ctx, ctx->s_h2d);
   FPDT_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->s_h2d));
   ctx->stats.bytes_h2d += (int64_t)bytes;
 }
 void d2h(fpdt_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  stress(ctx, ctx->s_d2h);
   FPDT_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
   ctx->stats.bytes_d2h += (int64_t)bytes;
 }
 void d2h_2d(fpdt_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows) {
+  stress(ctx, ctx->s_d2h);
   FPDT_CHECK_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, ctx->s_d2h));
   ctx->stats.bytes_d2h += (int64_t)(width * rows);
 }
@@ -375,6 +391,7 @@ void d2h_2d(fpdt_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spi
 // All-to-all on the comm stream: send [p][count] -> recv [p][count], recv block q = rank q's send block `rank`.
 void alltoall(fpdt_ctx* ctx, const void* send, void* recv, size_t count_per_peer, int dtype) {
   const size_t eb = dtype == FPDT_BF16 ? 2 : 4;
+  stress(ctx, ctx->s_comm);
   if (!ctx->group) {
     FPDT_CHECK_NCCL(ncclAlltoAll(send, recv, count_per_peer, dtype == FPDT_BF16 ? ncclBfloat16 : ncclFloat32,
                                  ctx->comm, ctx->s_comm));
@@ -425,6 +442,7 @@ struct TimedScope {
 };
 
 void launch_fwd(fpdt_ctx* ctx, const Config& c, const FwdArgs& a, cudaStream_t s) {
+  stress(ctx, s);
   TimedScope t(ctx, true, s);
   if (c.dtype == FPDT_BF16)
     FPDT_CHECK_LAUNCH(launch_attn_fwd_bf16(a, c.d, s));
@@ -434,6 +452,7 @@ void launch_fwd(fpdt_ctx* ctx, const Config& c, const FwdArgs& a, cudaStream_t s
   ctx->stats.attn_launches++;
 }
 void launch_bwd(fpdt_ctx* ctx, const Config& c, const BwdArgs& a, cudaStream_t s) {
+  stress(ctx, s);
   TimedScope t(ctx, false, s);
   if (c.dtype == FPDT_BF16)
     FPDT_CHECK_LAUNCH(launch_attn_bwd_bf16(a, c.d, s));
@@ -447,6 +466,7 @@ void launch_bwd(fpdt_ctx* ctx, const Config& c, const BwdArgs& a, cudaStream_t s
 // Plain library GEMMs (cuBLAS, fp32 accumulation; the fp32 mode uses pedantic FP32, no TF32) on row-major
 // operands, expressed as column-major products of the transposes.
 cublasHandle_t blas_on(fpdt_ctx* ctx, cudaStream_t s) {
+  stress(ctx, s);
   if (!ctx->blas) FPDT_CHECK_CUBLAS(cublasCreate(&ctx->blas));
   FPDT_CHECK_CUBLAS(cublasSetStream(ctx->blas, s));
   return ctx->blas;
@@ -1386,6 +1406,8 @@ fpdt_ctx* create_ctx(int world_size, int rank, const unsigned char* nccl_id, fpd
     FPDT_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->s_d2h, cudaStreamNonBlocking));
     FPDT_CHECK_CUDA(cudaStreamCreateWithFlags(&ctx->s_comp2, cudaStreamNonBlocking));
     if (const char* e = getenv("FPDT_BWD_QO_STREAMS")) ctx->qo_streams = atoi(e) == 1 ? 1 : 2;
+    if (const char* e = getenv("FPDT_STRESS_NS")) ctx->stress_ns = (uint32_t)std::max(0, atoi(e));
+    if (const char* e = getenv("FPDT_STRESS_SEED")) ctx->stress_state ^= (uint64_t)atoll(e) * 0xD1B54A32D192ED03ull;
     for (int b = 0; b < 4; ++b)
       for (cudaEvent_t* e : {&ctx->ev_qo_free[b], &ctx->ev_qo_filled[b], &ctx->ev_qo_done[b]})
         FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));

@@ -101,6 +101,8 @@ int launch_pack_seq2head(const void* src, int64_t c, int H, int head_dim, int p,
 int launch_unpack_head2seq(const void* src, int64_t src_peer_stride_elems, int64_t src_row_ld, int src_head0,
                            int64_t c, int H, int head_dim, int p, int elem_bytes, void* dst, cudaStream_t s,
                            int64_t dst_row_ld = 0);
+// debug: one thread sleeps about ns nanoseconds on stream s (scheduler stress, FPDT_STRESS_NS)
+int launch_stress_sleep(uint32_t ns, cudaStream_t s);
 // lse transpose: src[h*ld + t] (log2-domain) -> dst[t*dst_ld + dst_head0 + h] (natural log)
 int launch_lse_to_user(const float* src, int64_t ld, int64_t rows, int heads, float* dst, int64_t dst_ld,
                        int dst_head0, cudaStream_t s);

@@ -113,7 +113,18 @@ __global__ void lse_to_user_kernel(const float* __restrict__ src, int64_t ld, in
   }
 }
 
+// Scheduler stress (debug): one thread sleeps ~ns nanoseconds on its stream, perturbing the relative timing of the
+// library's streams so that a missing cross-stream event edge shows up as a parity failure (SURVEY §4 tier 5).
+__global__ void stress_sleep_kernel(uint32_t ns) {
+  for (uint32_t waited = 0; waited < ns; waited += 1000) __nanosleep(1000);
+}
+
 }  // namespace
+
+int launch_stress_sleep(uint32_t ns, cudaStream_t s) {
+  stress_sleep_kernel<<<1, 1, 0, s>>>(ns);
+  return (int)cudaGetLastError();
+}
 
 int launch_bwd_preprocess_D(const void* o, const void* dout, int dtype, int64_t rows, int heads, int head_dim,
                             int64_t row_ld, const void* resid, int64_t resid_ld, float* D, int64_t ld,
