@@ -214,6 +214,7 @@ typedef struct fpdt_stats {
   int64_t device_bytes;       /* library-owned device working set */
   int64_t bwd_order;          /* loop order of the last fpdt_attn_bwd (FPDT_BWD_KV_OUTER / FPDT_BWD_Q_OUTER) */
   int64_t host_dkv_bytes;     /* pinned store of the Q-outer backward's dK/dV partials (0 until first used) */
+  int64_t stress_sleeps;      /* debug sleep kernels enqueued by the scheduler stress mode (env FPDT_STRESS_NS) */
 } fpdt_stats;
 int fpdt_get_stats(const fpdt_ctx* ctx, fpdt_stats* out);
 

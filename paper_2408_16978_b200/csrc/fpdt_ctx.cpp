@@ -264,6 +264,7 @@ void stress(fpdt_ctx* ctx, cudaStream_t s) {
   x ^= x >> 7;
   x ^= x << 17;
   FPDT_CHECK_LAUNCH(launch_stress_sleep((uint32_t)(x % ctx->stress_ns), s));
+  ctx->stats.stress_sleeps++;
 }
 void wait(cudaStream_t s, cudaEvent_t e) { FPDT_CHECK_CUDA(cudaStreamWaitEvent(s, e, 0)); }
 

@@ -38,7 +38,7 @@ class Stats(ctypes.Structure):
     _fields_ = [("bytes_h2d", c_int64), ("bytes_d2h", c_int64), ("bytes_a2a", c_int64),
                 ("kernel_launches", c_int64), ("attn_launches", c_int64), ("fetch_slots_highwater", c_int64),
                 ("host_arena_bytes", c_int64), ("device_bytes", c_int64), ("bwd_order", c_int64),
-                ("host_dkv_bytes", c_int64)]
+                ("host_dkv_bytes", c_int64), ("stress_sleeps", c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}

@@ -74,6 +74,8 @@ def test_stress_world1(case, seed):
         ctx = _ctx(**kw)
         got = run_cuda(x, C, dtype, 1, ctx=ctx)
         ctx.close()
+    assert base["stats"]["stress_sleeps"] == 0
+    assert got["stats"]["stress_sleeps"] >= got["stats"]["attn_launches"]  # every launch (and copy) was perturbed
     if keep is None:
         ref = oracle_full(x)
     else:
