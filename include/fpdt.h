@@ -259,6 +259,15 @@ int fpdt_selftest_reduce(int mode, int iters, int inflight, int shared_target, f
  * n: 16..256, multiple of 16.  out[0] = SM cycles per MMA (device fp32).  Returns 0, FPDT_ERR_ARG or a CUDA error. */
 int fpdt_selftest_pair(int mode, int n, int iters, float* out, void* stream);
 
+/* Diagnostic: run ONE all-to-all layout kernel on caller device buffers.
+ *   which 0 (pack, sequence -> head-sharded send layout): src = c sequence rows [c][H][head_dim] (rows seq_row_ld
+ *     elements apart, 0 = H * head_dim); dst element (peer, t, hh, e) = src (t, peer * H/p + hh, e), stored at
+ *     dst[peer * hs_peer_stride + t * hs_row_ld + (hs_head0 + hh) * head_dim + e].
+ *   which 1 (unpack): the inverse, src head-sharded, dst sequence rows.
+ * elem_bytes 2 or 4 (the kernels move raw 16-byte vectors).  Returns FPDT_OK, FPDT_ERR_ARG or FPDT_ERR_CUDA. */
+int fpdt_debug_relayout(int which, const void* src, void* dst, int64_t c, int H, int head_dim, int p, int elem_bytes,
+                        int64_t hs_peer_stride, int64_t hs_row_ld, int hs_head0, int64_t seq_row_ld, void* stream);
+
 /* Diagnostic: launch ONE bf16 chunk-pair kernel directly (no scheduler) on caller device buffers, rows
  * [0, n_rows) of q/k/v/dout against each other (the diagonal pair when causal = 1).
  *   which 0 (forward):  out0 = o bf16 [n_rows][n_q_heads][head_dim], out1 = log2-domain lse fp32 [n_q_heads][n_rows]

@@ -62,3 +62,20 @@ extern "C" int fpdt_debug_pair(int which, int head_dim, int causal, const void* 
   a.trace_cta = trace_cta;
   return launch_attn_bwd_bf16(a, head_dim, s) == 0 ? FPDT_OK : FPDT_ERR_CUDA;
 }
+
+// Diagnostic: one all-to-all layout kernel (F3/F10/B2/B7) on caller device buffers (include/fpdt.h).
+extern "C" int fpdt_debug_relayout(int which, const void* src, void* dst, int64_t c, int H, int head_dim, int p,
+                                   int elem_bytes, int64_t hs_peer_stride, int64_t hs_row_ld, int hs_head0,
+                                   int64_t seq_row_ld, void* stream) {
+  using namespace fpdt;
+  if ((which != 0 && which != 1) || !src || !dst || c <= 0 || H <= 0 || p <= 0 || H % p ||
+      (elem_bytes != 2 && elem_bytes != 4) || (head_dim * elem_bytes) % 16 || hs_peer_stride <= 0 || hs_row_ld <= 0 ||
+      hs_head0 < 0 || seq_row_ld < 0)
+    return FPDT_ERR_ARG;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  const int rc = which == 0 ? launch_pack_seq2head(src, c, H, head_dim, p, elem_bytes, dst, hs_peer_stride, hs_row_ld,
+                                                   hs_head0, s, seq_row_ld)
+                            : launch_unpack_head2seq(src, hs_peer_stride, hs_row_ld, hs_head0, c, H, head_dim, p,
+                                                     elem_bytes, dst, s, seq_row_ld);
+  return rc == 0 ? FPDT_OK : FPDT_ERR_CUDA;
+}

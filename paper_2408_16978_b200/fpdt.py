@@ -24,7 +24,7 @@ EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_a
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair", "fpdt_group_create",
             "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity", "fpdt_set_residency",
-            "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes", "fpdt_selftest_pair",
+            "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes", "fpdt_selftest_pair", "fpdt_debug_relayout",
             "fpdt_selftest_softmax", "fpdt_selftest_reduce")
 
 
@@ -96,6 +96,9 @@ def _declare(lib):
     lib.fpdt_selftest_reduce.restype = c_int
     lib.fpdt_selftest_softmax.argtypes = [c_int, c_int, c_int, c_int, P, P]
     lib.fpdt_selftest_softmax.restype = c_int
+    lib.fpdt_debug_relayout.argtypes = [c_int, P, P, c_int64, c_int, c_int, c_int, c_int, c_int64, c_int64, c_int,
+                                        c_int64, P]
+    lib.fpdt_debug_relayout.restype = c_int
     lib.fpdt_selftest_pair.argtypes = [c_int, c_int, c_int, P, P]
     lib.fpdt_selftest_pair.restype = c_int
     lib.fpdt_selftest_perf.argtypes = [c_int, c_int, c_int, P, P]

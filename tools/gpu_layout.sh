@@ -1,0 +1,4 @@
+#!/bin/bash
+mkdir -p gpurun_out
+python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { tail -30 gpurun_out/build.log; exit 1; }
+timeout 600 python -m pytest tests/test_gpu_layout.py -q -m gpu > gpurun_out/pytest_layout.log 2>&1; echo "pytest rc=$?"; tail -25 gpurun_out/pytest_layout.log
