@@ -1396,6 +1396,7 @@ fpdt_ctx* create_ctx(int world_size, int rank, const unsigned char* nccl_id, fpd
                      size_t host_arena_bytes) {
     FPDT_CHECK_CUDA(cudaSetDevice(device));
     fpdt_ctx* ctx = new fpdt_ctx();
+    try {
     ctx->group = group;
     ctx->p = world_size;
     ctx->rank = rank;
@@ -1430,6 +1431,13 @@ fpdt_ctx* create_ctx(int world_size, int rank, const unsigned char* nccl_id, fpd
       FPDT_CHECK_NCCL(ncclCommInitRank(&ctx->comm, world_size, u, rank));
     }
     if (host_arena_bytes) ensure_host(ctx, host_arena_bytes);
+    } catch (...) {
+      // release what was created (streams, events, communicator) and keep the failure's status and message
+      const std::string msg = g_last_error;
+      fpdt_ctx_destroy(ctx);
+      g_last_error = msg;
+      throw;
+    }
     return ctx;
 }
 }  // namespace

@@ -38,3 +38,14 @@ def test_status_codes():
         fpdt.fpdt_attn_bwd(ctx, o, o, q, k, v, 1024, 2, 2, 64, 1, 512, 1, 0, 1)
     assert e.value.code == fpdt.FPDT_ERR_STATE
     ctx.close()
+
+
+def test_host_arena_exhaustion():
+    """A pinned host store that cannot be allocated is FPDT_ERR_HOST_OOM (SURVEY §4 tier 7), and the failed create
+    leaves the device usable."""
+    from paper_2408_16978_b200 import fpdt
+    with pytest.raises(fpdt.FpdtError) as e:
+        fpdt.FPDTContext(host_arena_bytes=1 << 50)   # 1 PiB of pinned memory
+    assert e.value.code == fpdt.FPDT_ERR_HOST_OOM
+    ctx = fpdt.FPDTContext()
+    ctx.close()
