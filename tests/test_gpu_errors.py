@@ -49,3 +49,21 @@ def test_host_arena_exhaustion():
     assert e.value.code == fpdt.FPDT_ERR_HOST_OOM
     ctx = fpdt.FPDTContext()
     ctx.close()
+
+
+def test_device_working_set_exhaustion():
+    """A working set the device cannot hold is FPDT_ERR_DEVICE_OOM before any kernel runs (the saved lse of a
+    2^40-token sequence alone is 4 TiB), and the context stays usable."""
+    from paper_2408_16978_b200 import fpdt
+    q = _t(256, 1, 64)
+    o = torch.empty_like(q)
+    ctx = fpdt.FPDTContext()
+    with pytest.raises(fpdt.FpdtError) as e:
+        fpdt.fpdt_attn_fwd(ctx, q, q, q, o, None, 1 << 40, 1, 1, 64, 1, 1 << 20, 1, fpdt.FPDT_BF16, 1)
+    assert e.value.code == fpdt.FPDT_ERR_DEVICE_OOM
+    with pytest.raises(fpdt.FpdtError) as e:   # no forward was saved
+        fpdt.fpdt_attn_bwd(ctx, o, o, q, q, q, 1 << 40, 1, 1, 64, 1, 1 << 20, 1, fpdt.FPDT_BF16, 1)
+    assert e.value.code == fpdt.FPDT_ERR_STATE
+    fpdt.fpdt_attn_fwd(ctx, q, q, q, o, None, 256, 1, 1, 64, 1, 256, 1, fpdt.FPDT_BF16, 1)
+    torch.cuda.synchronize()
+    ctx.close()
