@@ -57,7 +57,7 @@ static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs -
 #endif
 #ifndef FPDT_BWD_POLY_EVERY
 // one exponential pair in FPDT_BWD_POLY_EVERY goes to the FMA-pipe polynomial; 0 = all on MUFU.  Measured on the
-// C = 64K, 32 x 80 diagonal pair (tools/gpu_poly_sweep.sh): 4 -> 848-858, 8 -> 868, 16 -> 871, 0 -> 872-875 TFLOP/s
+// C = 64K, 32 x 80 diagonal pair (tools/gpu_poly_sweep_bwd.sh): 4 -> 848-858, 8 -> 868, 16 -> 871, 0 -> 872-875 TFLOP/s
 // (the backward is not MUFU-bound, so the extra FMA-pipe instructions only cost issue slots)
 #define FPDT_BWD_POLY_EVERY 0
 #endif
