@@ -55,6 +55,7 @@ constexpr float kRescaleThreshold = 8.0f;
 // C = 64K, 32-head diagonal pair (tools/gpu_poly_sweep_fwd.sh, two sessions; run-to-run noise about 2%):
 //   d = 80:  0, 1, 2, 3 -> 800, 669, 811, 865; 4 -> 940-948 / 966-985; 5 -> 954-955 / 957-987; 6 -> 915-935; 8 -> 902-941
 //   d = 128: 0 -> 1147-1149; 4 -> 1142-1145; 5 -> 1147-1148; 6 -> 1151-1159; 8 -> 1147-1162; 12, 16 -> 1139-1152
+// Inside the bench step on one box (tools/gpu_ab_fwdpoly.sh), d = 80: 4 -> 895, 5 -> 910, 6 -> 876 TFLOP/s.
 #ifndef FPDT_FWD_POLY_EVERY
 #define FPDT_FWD_POLY_EVERY 5
 #endif
