@@ -42,7 +42,9 @@ constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 128
 constexpr int kRegsSoftmax = FPDT_Q64_REGS_SOFTMAX, kRegsDQ = FPDT_Q64_REGS_DQ, kRegsCtl = FPDT_Q64_REGS_CTL;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
 #ifndef FPDT_BWD_POLY_EVERY
-#define FPDT_BWD_POLY_EVERY 4
+// all exponentials on MUFU (0): standalone d = 128 pair flat (4 -> 1002-1005, 0 -> 1004), c5 per-rank step on one
+// box 7.889 s -> 7.823 s (tools/gpu_ab_d128.sh)
+#define FPDT_BWD_POLY_EVERY 0
 #endif
 
 constexpr int BQ = 64;
