@@ -23,12 +23,15 @@ IEEE fp32 ops so the device twin matches bitwise):
 
     normal : x
     peaky  : q*4                                                    (sharp attention)
-    drift  : q[...,0] += 2 ;  k[t,...,0] += t*(8/S)                 (running max rises every chunk)
+    drift  : q[...,0] += 2 ;  k[t,...,0] += t*(32/S)                (running max rises every chunk: at d = 128
+             the ramp moves the logits of the last keys by ~2*32/sqrt(128) = 5.7 nats over the sequence)
     sink   : q += 0.5 ;  k[0] = 2 (all dims)                         (attention sink on token 0)
     same   : k[t] = base(K, token 0)                                (identical keys: closed form)
     class  : k[t] = base(K, token c(t)), c(t) = mix32(t^0xC1A55) % 3 for t < S/2, % 4 for t >= S/2;
              class 3 is scaled by 4 (a large-norm class that appears only in later chunks, so the
              running max jumps at chunk boundaries)
+    extreme: q*30                                                   (logits of +-100s of nats: the online rescale
+             under large max jumps, and keys far enough below the row max that exp2 underflows)
 """
 from __future__ import annotations
 
@@ -36,7 +39,7 @@ import numpy as np
 
 Q, K, V, DO, X, W, WO, DY = 0, 1, 2, 3, 4, 5, 6, 7
 TENSOR_IDS = {"q": Q, "k": K, "v": V, "do": DO, "x": X, "w": W, "wo": WO, "dy": DY}
-DISTRIBUTIONS = ("normal", "peaky", "drift", "sink", "same", "class")
+DISTRIBUTIONS = ("normal", "peaky", "drift", "sink", "same", "class", "extreme")
 DIST_IDS = {name: i for i, name in enumerate(DISTRIBUTIONS)}
 N_CLASSES = 4
 
@@ -109,11 +112,13 @@ def generate(name: str, dist: str, seed: int, tokens: np.ndarray, n_heads: int, 
     x = base_values(seed, tensor, tokens, n_heads, head_dim, heads)
     if dist == "peaky" and name == "q":
         x = x * np.float32(4.0)
+    elif dist == "extreme" and name == "q":
+        x = x * np.float32(30.0)
     elif dist == "drift":
         if name == "q":
             x[..., 0] = x[..., 0] + np.float32(2.0)
         elif name == "k":
-            step = np.float32(8.0 / seq_len)
+            step = np.float32(32.0 / seq_len)
             x[..., 0] = x[..., 0] + (tokens.astype(np.float32) * step).reshape(-1, 1)
     elif dist == "sink":
         if name == "q":

@@ -11,6 +11,7 @@ import os
 PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 _LIB = None
+_DIAG = None
 _GEN = None
 
 c_int, c_int64, c_float, c_void_p, c_char_p, c_size_t = (ctypes.c_int, ctypes.c_int64, ctypes.c_float,
@@ -35,6 +36,19 @@ def load():
             raise FpdtLibraryMissing(f"{path} not built (run python -m paper_2408_16978_b200.build)")
         _LIB = _declare(ctypes.CDLL(path))
     return _LIB
+
+
+def load_diag():
+    global _DIAG
+    if _DIAG is None:
+        load()
+        path = os.path.join(PKG, "libfpdt_diag.so")
+        if not os.path.exists(path):
+            raise FpdtLibraryMissing(f"{path} not built (run python -m paper_2408_16978_b200.build)")
+        from . import fpdt as _f
+        _DIAG = ctypes.CDLL(path)
+        _f._declare_diag(_DIAG)
+    return _DIAG
 
 
 def load_generator():

@@ -3,6 +3,8 @@
     python -m paper_2408_16978_b200.build
 
 * ``paper_2408_16978_b200/libfpdt.so`` — the product: C-ABI in include/fpdt.h.
+* ``paper_2408_16978_b200/libfpdt_diag.so`` — diagnostics (include/fpdt_diag.h: micro-benchmarks, direct pair /
+  layout kernel launches), linked against libfpdt.so; not on the FPDT path.
 * ``fpdt_inputs/libfpdt_gen.so``       — the seeded input generator's device twin (test/bench infra).
 """
 from __future__ import annotations
@@ -33,19 +35,6 @@ def _nccl_dirs():
     raise RuntimeError("NCCL headers not found (expected the torch-bundled nvidia-nccl wheel)")
 
 
-def _cublas_lib():
-    """The torch-bundled libcublas.so.12 (the copy torch itself loads, so the process holds one cuBLAS); the
-    fused QKV projection GEMMs of fpdt_block_fwd/bwd call it.  Headers come from the CUDA toolkit."""
-    import importlib.util
-    spec = importlib.util.find_spec("nvidia")
-    roots = list(spec.submodule_search_locations) if spec and spec.submodule_search_locations else []
-    for r in roots:
-        lib = os.path.join(r, "cublas", "lib")
-        if os.path.exists(os.path.join(lib, "libcublas.so.12")):
-            return lib
-    return "/usr/local/cuda/lib64"
-
-
 def _stale(target, sources):
     if not os.path.exists(target):
         return True
@@ -58,34 +47,56 @@ def _run(cmd):
     subprocess.run(cmd, check=True)
 
 
-def build_product(force: bool = False) -> str:
-    csrc = os.path.join(PKG, "csrc")
-    cu = sorted(glob.glob(os.path.join(csrc, "*.cu")))
-    cpp = sorted(glob.glob(os.path.join(csrc, "*.cpp")))
-    deps = cu + cpp + glob.glob(os.path.join(csrc, "*.cuh")) + glob.glob(os.path.join(csrc, "*.h")) + \
-        glob.glob(os.path.join(ROOT, "include", "*.h"))
-    out = os.path.join(PKG, "libfpdt.so")
-    if not force and not _stale(out, deps):
-        return out
-    nccl_inc, nccl_lib = _nccl_dirs()
-    objdir = os.path.join(PKG, "build")
+def _compile(sources, deps, objdir, force, extra_inc=()):
+    nccl_inc, _ = _nccl_dirs()
     os.makedirs(objdir, exist_ok=True)
-    objs = []
-    procs = []
-    for src in cu + cpp:
+    objs, procs = [], []
+    for src in sources:
         obj = os.path.join(objdir, os.path.basename(src) + ".o")
         objs.append(obj)
         if force or _stale(obj, [src] + deps):
-            cmd = [NVCC] + COMMON + ["-I", os.path.join(ROOT, "include"), "-I", csrc, "-I", nccl_inc,
-                                     "-c", src, "-o", obj]
+            cmd = [NVCC] + COMMON + ["-I", os.path.join(ROOT, "include"), "-I", os.path.join(PKG, "csrc"),
+                                     "-I", nccl_inc] + [a for d in extra_inc for a in ("-I", d)] + ["-c", src, "-o", obj]
             print(" ".join(cmd), flush=True)
             procs.append(subprocess.Popen(cmd))
     for p in procs:
         if p.wait() != 0:
             raise RuntimeError("nvcc failed")
+    return objs
+
+
+def _headers():
+    csrc = os.path.join(PKG, "csrc")
+    return glob.glob(os.path.join(csrc, "*.cuh")) + glob.glob(os.path.join(csrc, "*.h")) + \
+        glob.glob(os.path.join(ROOT, "include", "*.h"))
+
+
+def build_product(force: bool = False) -> str:
+    csrc = os.path.join(PKG, "csrc")
+    srcs = sorted(glob.glob(os.path.join(csrc, "*.cu"))) + sorted(glob.glob(os.path.join(csrc, "*.cpp")))
+    deps = srcs + _headers()
+    out = os.path.join(PKG, "libfpdt.so")
+    if not force and not _stale(out, deps):
+        return out
+    _, nccl_lib = _nccl_dirs()
+    objs = _compile(srcs, deps, os.path.join(PKG, "build"), force)
     _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", out] + objs +
-         ["-L", nccl_lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={nccl_lib}", "-L", _cublas_lib(), "-l:libcublas.so.12",
-          f"-Xlinker=-rpath={_cublas_lib()}", "-lpthread"])
+         ["-L", nccl_lib, "-l:libnccl.so.2", f"-Xlinker=-rpath={nccl_lib}", "-lpthread"])
+    return out
+
+
+def build_diag(force: bool = False) -> str:
+    """The diagnostics library: csrc/diag/*, linked against libfpdt.so (rpath $ORIGIN)."""
+    ddir = os.path.join(PKG, "csrc", "diag")
+    srcs = sorted(glob.glob(os.path.join(ddir, "*.cu"))) + sorted(glob.glob(os.path.join(ddir, "*.cpp")))
+    prod = build_product(force)
+    deps = srcs + _headers() + [prod]
+    out = os.path.join(PKG, "libfpdt_diag.so")
+    if not force and not _stale(out, deps):
+        return out
+    objs = _compile(srcs, srcs + _headers(), os.path.join(PKG, "build", "diag"), force)
+    _run([NVCC] + ARCH + ["-shared", "-cudart", "static", "-o", out] + objs +
+         ["-L", PKG, "-l:libfpdt.so", "-Xlinker=-rpath=$ORIGIN", "-lpthread"])
     return out
 
 
@@ -98,7 +109,7 @@ def build_generator(force: bool = False) -> str:
 
 
 def build_all(force: bool = False):
-    return build_product(force), build_generator(force)
+    return build_product(force), build_diag(force), build_generator(force)
 
 
 if __name__ == "__main__":

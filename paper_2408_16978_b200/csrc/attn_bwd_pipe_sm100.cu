@@ -15,7 +15,8 @@
 // of it), so per query tile only dQ = dS K (A = the dS smem tile) reads two smem operands.  Shared-memory bytes per
 // tile (d = 80): TMA Q, dO 40K + MMA operands 172K + dS 32K + dQ staging 80K.
 // Element-wise math uses packed f32x2 FMA-pipe instructions (FFMA2/FADD2/FMUL2); the exponentials all run on MUFU
-// (an FA4-style polynomial offload of a fraction of them measured slower here, FPDT_BWD_POLY_EVERY).
+// (an FA4-style polynomial offload of a fraction of them measured slower here: one pair in 4 / 8 / 16 on the FMA pipe
+// gave 848-858 / 868 / 871 TFLOP/s against 872-875 all on MUFU, C = 64K, 32 x 80 diagonal pair).
 //
 // Warps (512 threads = 4 warpgroups, registers rebalanced with setmaxnreg):
 //   WG0 (0-3)   softmax-gradient, query columns [0,64)   (thread = key row = TMEM lane); final dK    168 regs
@@ -29,9 +30,6 @@
 #include "kernels.h"
 #include "smem_layout.cuh"
 #include "tma_host.h"
-
-#include <cstdlib>
-#include <cstring>
 
 namespace fpdt {
 namespace {
@@ -50,18 +48,6 @@ constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 128
 #endif
 constexpr int kRegsSoftmax = FPDT_BWD_REGS_SOFTMAX, kRegsDQ = FPDT_BWD_REGS_DQ, kRegsCtl = FPDT_BWD_REGS_CTL;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
-#ifndef FPDT_BWD_EXP
-#define FPDT_BWD_EXP 0  // timing experiments only (wrong results): 1 no dQ reduce, 2 no dQ staging/reduce,
-                       // 3 no stats loads, 4 = 2 + 3, 5 no wait for the previous dQ reduce's smem read,
-                       // 6 dQ reduce every other tile only, 8 only even key tiles reduce
-#endif
-#ifndef FPDT_BWD_POLY_EVERY
-// one exponential pair in FPDT_BWD_POLY_EVERY goes to the FMA-pipe polynomial; 0 = all on MUFU.  Measured on the
-// C = 64K, 32 x 80 diagonal pair (tools/gpu_poly_sweep_bwd.sh): 4 -> 848-858, 8 -> 868, 16 -> 871, 0 -> 872-875 TFLOP/s
-// (the backward is not MUFU-bound, so the extra FMA-pipe instructions only cost issue slots)
-#define FPDT_BWD_POLY_EVERY 0
-#endif
-
 template <int D>
 struct PipeCfg {
   using T = Tile<D>;
@@ -82,29 +68,14 @@ struct PipeCfg {
 };
 
 struct TmapSet {
-  CUtensorMap q, k, v, o, dq32, dq16;  // dq32: 32-column fp32 boxes, 128B swizzle; dq16: 16 columns, 64B swizzle
-  CUtensorMap dq32h, dq16h;           // the same with 64-row boxes (cluster-pair mode: one half tile per CTA)
+  CUtensorMap q, k, v, o;
+  CUtensorMap dq32h, dq16h;  // fp32 dq_acc, 64-row boxes: 32 columns (128B swizzle) / 16 columns (64B swizzle)
 };
 
 __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-
-// 2^x for a pair on the FMA pipe: x = j + f, j = rint(x), f in [-1/2, 1/2]; degree-3 minimax for 2^f (max rel.
-// error 7.5e-5, far below bf16's 2^-9); the exponent is added as an integer.  x is clamped to >= -127.
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
-  const float2 kRnd = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
-  const float2 j = __fadd2_rn(x, kRnd);
-  const float2 f = __fadd2_rn(x, __fadd2_rn(kRnd, make_float2(-j.x, -j.y)));
-  float2 p = __ffma2_rn(f, make_float2(0.055169348f, 0.055169348f), make_float2(0.24260798f, 0.24260798f));
-  p = __ffma2_rn(p, f, make_float2(0.69326115f, 0.69326115f));
-  p = __ffma2_rn(p, f, make_float2(0.9999283f, 0.9999283f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
 }
 
 __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2) {
@@ -120,15 +91,11 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
-__device__ __forceinline__ float4 lds4(const float* p) {
-  if (FPDT_BWD_EXP >= 3) return make_float4(1.f, 2.f, 3.f, 4.f);
-  return *reinterpret_cast<const float4*>(p);
-}
+__device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 
-template <int D, bool kPair>
+template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdArgs a) {
   using T = Tile<D>;
@@ -143,7 +110,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
   constexpr int B_KV = 0, B_QF = 1, B_QE = B_QF + QS, B_OF = B_QE + QS, B_OE = B_OF + OS, B_S = B_OE + OS,
                 B_SFREE = B_S + 1, B_DP = B_SFREE + 1, B_P = B_DP + 1, B_DS = B_P + 1,
                 B_DSFREE = B_DS + 1, B_DQF = B_DSFREE + 1, B_DQE = B_DQF + 1, B_KVDONE = B_DQE + 1,
-                B_FULL = B_KVDONE + 1, B_PFREE = B_FULL + 2, B_NUM = B_PFREE + 2;
+                B_NUM = B_KVDONE + 1;
   static_assert(B_NUM <= 30, "barrier area");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::oBars + 30 * 8);
 
@@ -186,17 +153,10 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
     mbar_init(bar(B_DQF), 1);
     mbar_init(bar(B_DQE), 128);
     mbar_init(bar(B_KVDONE), 1);
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(bar(B_FULL + b), 1);
-      mbar_init(bar(B_PFREE + b), 1);
-    }
     fence_mbar_init();
   }
   tc_fence_before();
-  if constexpr (kPair)
-    cluster_sync();  // the partner CTA's barriers are initialised before any remote arrive / st.async
-  else
-    __syncthreads();
+  __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
@@ -352,14 +312,8 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
               __ffma2_rn(make_float2(p[i + 2], p[i + 3]), make_float2(sl2, sl2), make_float2(-l.z, -l.w));
           p[i] = ex2(x0.x);
           p[i + 1] = ex2(x0.y);
-          if (FPDT_BWD_POLY_EVERY >= 2 && (i / 4) % (FPDT_BWD_POLY_EVERY / 2 > 0 ? FPDT_BWD_POLY_EVERY / 2 : 1) == (FPDT_BWD_POLY_EVERY / 2) - 1) {
-            const float2 e = ex2_poly2(x1);
-            p[i + 2] = e.x;
-            p[i + 3] = e.y;
-          } else {
-            p[i + 2] = ex2(x1.x);
-            p[i + 3] = ex2(x1.y);
-          }
+          p[i + 2] = ex2(x1.x);
+          p[i + 3] = ex2(x1.y);
         }
       }
       if (warp == 0 && lane == 0) TRACE(14, n);
@@ -461,26 +415,6 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
     const int r = (warp - 8) * 32 + lane;
     uint32_t tdQ = tmem + C::tdQ + (((warp & 3) * 32) << 16);
     asm volatile("" : "+r"(tdQ));
-    // cluster pair: rank 0 holds the even key tile, rank 1 the next one; on the causal diagonal the even tile sees
-    // (qt_first_partner - qt_first) more query tiles, which it reduces alone (n < n_solo)
-    uint32_t crank = 0, peer_stg = 0, peer_full[2] = {0, 0}, peer_pfree[2] = {0, 0};
-    int n_solo = 0;
-    bool recv_rows = true;
-    if constexpr (kPair) {
-      crank = cluster_ctarank();
-      recv_rows = (r >> 6) == (int)crank;  // this thread's query row is in the half this CTA reduces
-      peer_stg = mapa(sDQ, crank ^ 1);
-      for (int b2 = 0; b2 < 2; ++b2) {
-        peer_full[b2] = mapa(bar(B_FULL + b2), crank ^ 1);
-        peer_pfree[b2] = mapa(bar(B_PFREE + b2), crank ^ 1);
-      }
-      if (crank == 0 && a.causal) {
-        const int64_t rel = kv_base + 128 - a.q_pos0;
-        int qf = rel > 0 ? (int)(rel / 128) : 0;
-        if (qf > n_qt_total) qf = n_qt_total;
-        n_solo = (qf - qt_first) * G;
-      }
-    }
     for (int n = 0; n < n_iter; ++n) {
       const int qt = qt_first + n / G, h = g * G + n % G;
       mbar_wait(bar(B_DQF), n & 1);
@@ -492,72 +426,6 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(bar(B_DQE));
-      if (FPDT_BWD_EXP == 2 || FPDT_BWD_EXP == 4) continue;
-      if constexpr (kPair) {
-        // Cluster pair (two CTAs on neighbouring key tiles of one head, same query tiles): the per-SM write path to
-        // L2 is what limits the dQ reduce-add, so each CTA reduces only HALF of the query rows of a tile — rows
-        // [64 rank, 64 rank + 64): its own partial plus the partner's, which arrives over DSMEM (st.async) — and
-        // sends its other half to the partner.  Double-buffered 64-row staging (the same 40 KB as one full tile).
-        if (n < n_solo) {  // causal diagonal: a query tile the partner does not see; rare, vector atomics
-          float4* dst = reinterpret_cast<float4*>(a.dq_acc + (int64_t)h * a.dq_head_stride + ((int64_t)qt * 128 + r) * D);
-#pragma unroll
-          for (int c = 0; c < D; c += 4)
-            atomicAdd(dst + c / 4, make_float4(v[c] * a.scale, v[c + 1] * a.scale, v[c + 2] * a.scale,
-                                               v[c + 3] * a.scale));
-          continue;
-        }
-        const int k = n - n_solo, bsel = k & 1;
-        const uint32_t par = (k >> 1) & 1;
-        const int rr = r & 63;
-        auto half_off = [&](int c) -> uint32_t {  // 64-row staging: 32-column chunks 128B-swizzled, then 16 columns
-          const int j = (c & 31) >> 2;
-          if (c < (D / 32) * 32) return (c >> 5) * 8192 + rr * 128 + ((j ^ (rr & 7)) << 4);
-          return (D / 32) * 8192 + rr * 64 + ((j ^ ((rr >> 1) & 3)) << 4);
-        };
-        constexpr uint32_t HB = 64 * D * 4;
-        const float2 sc2 = make_float2(a.scale, a.scale);
-        if (!recv_rows) {
-          mbar_wait_cluster(bar(B_PFREE + bsel), par);  // the partner's buffer has been read by its last reduce
-#pragma unroll
-          for (int c = 0; c < D; c += 4) {
-            const float2 x0 = __fmul2_rn(make_float2(v[c], v[c + 1]), sc2);
-            const float2 x1 = __fmul2_rn(make_float2(v[c + 2], v[c + 3]), sc2);
-            uint32_t dst = peer_stg + bsel * HB;
-            asm volatile("" : "+r"(dst));  // address math per store: 20 hoisted addresses would spill
-            st_async_v4(dst + half_off(c), make_float4(x0.x, x0.y, x1.x, x1.y), peer_full[bsel]);
-          }
-          continue;
-        }
-        const bool tr0 = (r & 63) == 0;
-        if (tr0) bulk_wait_read1();  // buffer bsel's reduce (2 tiles ago) has been read; the last one may run on
-        named_bar(2, 64);
-        if (tr0) {
-          mbar_expect_tx(bar(B_FULL + bsel), HB);
-          mbar_arrive_remote(peer_pfree[bsel]);
-        }
-        mbar_wait_cluster(bar(B_FULL + bsel), par);
-        uint8_t* stg = smem + C::oDQ + bsel * HB;
-#pragma unroll
-        for (int c = 0; c < D; c += 4) {
-          float4* q4 = reinterpret_cast<float4*>(stg + half_off(c));
-          const float4 pv = *q4;
-          const float2 x0 = __ffma2_rn(make_float2(v[c], v[c + 1]), sc2, make_float2(pv.x, pv.y));
-          const float2 x1 = __ffma2_rn(make_float2(v[c + 2], v[c + 3]), sc2, make_float2(pv.z, pv.w));
-          *q4 = make_float4(x0.x, x0.y, x1.x, x1.y);
-        }
-        fence_async_shared();
-        named_bar(2, 64);
-        if (tr0) {
-          const uint32_t sb = sDQ + bsel * HB;
-          const int row0 = qt * 128 + 64 * (int)crank;
-#pragma unroll
-          for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_3d(&tm.dq32h, sb + cc * 8192, cc * 32, row0, h);
-          if (D % 32) tma_reduce_add_3d(&tm.dq16h, sb + (D / 32) * 8192, (D / 32) * 32, row0, h);
-          bulk_commit();
-          TRACE(11, n);
-        }
-        continue;
-      }
       // Two independent 64-row halves (warps 8-9: query rows 0-63, warps 10-11: rows 64-127), each with its own half
       // of the staging, named barrier and issuing thread: while one half waits for its previous reduce-add to finish
       // reading its staging, the TMA engine works on the other half's.  Staging per half: D/32 column chunks
@@ -566,7 +434,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       const int hrow = r >> 6, rr = r & 63;
       const bool hlead = rr == 0;
       constexpr uint32_t HB = 64 * D * 4;
-      if (FPDT_BWD_EXP != 5 && hlead) bulk_wait_read0();
+      if (hlead) bulk_wait_read0();
       named_bar(2 + hrow, 64);
       const float2 sc = make_float2(a.scale, a.scale);
       uint8_t* stg = smem + C::oDQ + hrow * HB;
@@ -581,7 +449,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       }
       fence_async_shared();
       named_bar(2 + hrow, 64);
-      if (FPDT_BWD_EXP != 1 && !(FPDT_BWD_EXP == 6 && (n & 1)) && !(FPDT_BWD_EXP == 8 && (kt & 1)) && hlead) {
+      if (hlead) {
         const uint32_t sb = sDQ + hrow * HB;
         const int row0 = qt * 128 + 64 * hrow;
 #pragma unroll
@@ -594,10 +462,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
     if ((r & 63) == 0) bulk_wait0();
   }
   tc_fence_before();
-  if constexpr (kPair)
-    cluster_sync();  // no CTA leaves while its partner may still write into its shared memory
-  else
-    __syncthreads();
+  __syncthreads();
   if (warp == 13) tmem_dealloc<512>(tmem);
 #undef TRACE
 }
@@ -605,57 +470,37 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
 template <int D>
 int launch_pipe(const BwdArgs& a, cudaStream_t s) {
   using C = PipeCfg<D>;
-  // FPDT_BWD_PAIR=1: cluster pairs split the dQ reduce-add (see kernel).  Off by default: measured 579 TFLOP/s vs 867
-  // (the two CTAs' dQ warps run in lockstep through the DSMEM exchange, and that chain is longer than the reduce)
-  static const bool pair = [] {
-    const char* e = getenv("FPDT_BWD_PAIR");
-    return e && strcmp(e, "1") == 0;
-  }();
   TmapSet tm;
   bool ok = make_tile_tmap<D>(&tm.q, a.q.base, a.q.rows, a.q.heads);
   ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
   ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
   ok &= make_tile_tmap<D>(&tm.o, a.dout.base, a.dout.rows, a.dout.heads);
-  for (int rows = 128; rows >= 64; rows -= 64) {
-    ok &= make_tmap_f32_head_major(rows == 128 ? &tm.dq32 : &tm.dq32h, a.dq_acc, a.n_q_rows, a.hq, D,
-                                   a.dq_head_stride, 32, rows, CU_TENSOR_MAP_SWIZZLE_128B);
-    ok &= make_tmap_f32_head_major(rows == 128 ? &tm.dq16 : &tm.dq16h, a.dq_acc, a.n_q_rows, a.hq, D,
-                                   a.dq_head_stride, 16, rows, CU_TENSOR_MAP_SWIZZLE_64B);
-  }
+  ok &= make_tmap_f32_head_major(&tm.dq32h, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 32, 64,
+                                 CU_TENSOR_MAP_SWIZZLE_128B);
+  ok &= make_tmap_f32_head_major(&tm.dq16h, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 16, 64,
+                                 CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return -1;
-  const int n_kv_tiles = a.n_kv_rows / 128;
-  const bool use_pair = pair && (n_kv_tiles % 2 == 0);
-  auto kern = use_pair ? attn_bwd_pipe_kernel<D, true> : attn_bwd_pipe_kernel<D, false>;
-  static bool attr_set[2] = {false, false};
-  if (!attr_set[use_pair]) {
-    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    attr_set[use_pair] = true;
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(n_kv_tiles, a.hq / a.G);
-  cfg.blockDim = dim3(kThreads);
-  cfg.dynamicSmemBytes = C::kSmem;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = use_pair ? 2 : 1;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return (int)cudaLaunchKernelEx(&cfg, kern, tm, a);
+  if (int e = set_max_dynamic_smem((const void*)attn_bwd_pipe_kernel<D>, C::kSmem)) return e;
+  attn_bwd_pipe_kernel<D><<<dim3(a.n_kv_rows / 128, a.hq / a.G), kThreads, C::kSmem, s>>>(tm, a);
+  return (int)cudaGetLastError();
 }
 
 }  // namespace
 
-// head_dim 64 / 80 (the pipelined kernel); head_dim 128 stays on attn_bwd_sm100.cu (its TMEM/smem budget has no
-// room for the extra Q stage and the separate dQ columns)
+// head_dim 64 / 80: this kernel; head_dim 128 runs attn_bwd_q64_sm100.cu (no TMEM room here for a 128-column dQ
+// next to S^T, dP^T, dK and dV, nor shared memory for its staging)
 int launch_attn_bwd_pipe_bf16(const BwdArgs& a, int head_dim, cudaStream_t s) {
   switch (head_dim) {
     case 64: return launch_pipe<64>(a, s);
     case 80: return launch_pipe<80>(a, s);
   }
   return -2;
+}
+
+// The bf16 backward pair kernel for each head_dim.
+int launch_attn_bwd_bf16(const BwdArgs& a, int head_dim, cudaStream_t s) {
+  if (head_dim == 128) return launch_attn_bwd_q64_bf16(a, head_dim, s);
+  return launch_attn_bwd_pipe_bf16(a, head_dim, s);
 }
 
 }  // namespace fpdt

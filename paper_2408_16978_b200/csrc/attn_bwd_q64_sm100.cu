@@ -41,11 +41,8 @@ constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 128
 #endif
 constexpr int kRegsSoftmax = FPDT_Q64_REGS_SOFTMAX, kRegsDQ = FPDT_Q64_REGS_DQ, kRegsCtl = FPDT_Q64_REGS_CTL;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
-#ifndef FPDT_BWD_POLY_EVERY
-// all exponentials on MUFU (0): standalone d = 128 pair flat (4 -> 1002-1005, 0 -> 1004), c5 per-rank step on one
-// box 7.889 s -> 7.823 s (tools/gpu_ab_d128.sh)
-#define FPDT_BWD_POLY_EVERY 0
-#endif
+// All exponentials run on MUFU: one pair in 4 on the FMA-pipe polynomial was flat on the standalone d = 128 pair
+// (1002-1005 vs 1004 TFLOP/s) and 0.8% slower on the c5 per-rank step (7.889 vs 7.823 s on one box).
 
 constexpr int BQ = 64;
 
@@ -108,20 +105,6 @@ __device__ __forceinline__ float ex2(float x) {
   float y;
   asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
   return y;
-}
-// 2^x for a pair on the FMA pipe (degree-3 minimax on the fraction, exponent added as an integer; max rel. error
-// 7.5e-5); x clamped to >= -127
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
-  const float2 kRnd = make_float2(12582912.f, 12582912.f);
-  const float2 j = __fadd2_rn(x, kRnd);
-  const float2 f = __fadd2_rn(x, __fadd2_rn(kRnd, make_float2(-j.x, -j.y)));
-  float2 p = __ffma2_rn(f, make_float2(0.055169348f, 0.055169348f), make_float2(0.24260798f, 0.24260798f));
-  p = __ffma2_rn(p, f, make_float2(0.69326115f, 0.69326115f));
-  p = __ffma2_rn(p, f, make_float2(0.9999283f, 0.9999283f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
 }
 __device__ __forceinline__ void tma_reduce_add_3d(const CUtensorMap* m, uint32_t src, int c0, int c1, int c2) {
   asm volatile("cp.reduce.async.bulk.tensor.3d.global.shared::cta.add.tile.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(
@@ -357,14 +340,8 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
               __ffma2_rn(make_float2(p[i + 2], p[i + 3]), make_float2(sl2, sl2), make_float2(-l.z, -l.w));
           p[i] = ex2(x0.x);
           p[i + 1] = ex2(x0.y);
-          if (FPDT_BWD_POLY_EVERY >= 2 && (i / 4) % (FPDT_BWD_POLY_EVERY / 2 > 0 ? FPDT_BWD_POLY_EVERY / 2 : 1) == (FPDT_BWD_POLY_EVERY / 2) - 1) {
-            const float2 e = ex2_poly2(x1);
-            p[i + 2] = e.x;
-            p[i + 3] = e.y;
-          } else {
-            p[i + 2] = ex2(x1.x);
-            p[i + 3] = ex2(x1.y);
-          }
+          p[i + 2] = ex2(x1.x);
+          p[i + 3] = ex2(x1.y);
         }
       }
       // dP^T_n -> registers (then dP^T_{n+1} may be issued); P^T_n and dS^T_n (bf16) go to their own columns
@@ -531,11 +508,7 @@ int launch_q64(const BwdArgs& a, cudaStream_t s) {
   ok &= make_tmap_f32_head_major(&tm.dq16, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 16, BQ,
                                  CU_TENSOR_MAP_SWIZZLE_NONE);
   if (!ok) return -1;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(attn_bwd_q64_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    attr_set = true;
-  }
+  if (int e = set_max_dynamic_smem((const void*)attn_bwd_q64_kernel<D>, C::kSmem)) return e;
   attn_bwd_q64_kernel<D><<<dim3(a.n_kv_rows / 128, a.hq / a.G), kThreads, C::kSmem, s>>>(tm, a);
   return (int)cudaGetLastError();
 }

@@ -48,9 +48,6 @@ constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 168
 constexpr int kRegsSoftmax = FPDT_FWD_REGS_SOFTMAX, kRegsOther = FPDT_FWD_REGS_OTHER;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (kLaunchRegs - kRegsOther), "register pool");
 constexpr float kRescaleThreshold = 8.0f;
-#ifndef FPDT_FWD_EX2_F16
-#define FPDT_FWD_EX2_F16 0  // 1: MUFU exponentials as ex2.approx.f16x2 (2x MUFU rate, more instructions: measured 924 vs 956 TF)
-#endif
 // One exponential pair in N on the FMA pipe, the rest on MUFU (0 = all MUFU), per head_dim.  Measured on the
 // C = 64K, 32-head diagonal pair (tools/gpu_poly_sweep_fwd.sh, two sessions; run-to-run noise about 2%):
 //   d = 80:  0, 1, 2, 3 -> 800, 669, 811, 865; 4 -> 940-948 / 966-985; 5 -> 954-955 / 957-987; 6 -> 915-935; 8 -> 902-941
@@ -106,10 +103,11 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
 
 // 2^x for a pair on the FMA pipe (FA4-style MUFU offload): x = j + f, j = rint(x), f in [-1/2, 1/2];
 // degree-3 minimax for 2^f (max rel. error 7.5e-5 << bf16's 2^-9); the exponent is added as an integer.
-// x is clamped to >= -127 (callers use it only where x is finite).
+// x is clamped to >= -126 (callers use it only where x is finite; at -127 the exponent addition would wrap into
+// the sign bit and give a NaN, so keys far below the running max must still give ~0).
 __device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -127.f);
-  x.y = fmaxf(x.y, -127.f);
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
   const float2 kRnd = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
   const float2 j = __fadd2_rn(x, kRnd);
   const float2 f = __fadd2_rn(x, __fadd2_rn(kRnd, make_float2(-j.x, -j.y)));
@@ -120,16 +118,8 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
 }
 
-// 2^x for a pair on MUFU at twice the fp32 rate: the fp32 arguments rounded to f16 (relative 2^-11: absolute
-// <= 2^-8 in the exponent for the |x| <= 8 the lazy rescale allows, i.e. <= 0.27% on a P that is then rounded to
-// bf16 anyway, and <= 0.03% where |x| <= 1, the weights that dominate), ex2.approx.f16x2, back to fp32.
-__device__ __forceinline__ float2 ex2_f16x2(float2 x) {
-  uint32_t h;
-  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(h) : "f"(x.y), "f"(x.x));
-  asm("ex2.approx.f16x2 %0, %0;" : "+r"(h));
-  __half2 hv = *reinterpret_cast<__half2*>(&h);
-  return __half22float2(hv);
-}
+// (Measured and not kept: the MUFU exponentials as ex2.approx.f16x2 on f16-rounded arguments, twice the MUFU rate
+// but more instructions: 924 vs 956 TFLOP/s on the d = 80 pair.)
 
 // P = exp2(x*sl2 - mb) for the 128 columns of a row, packed to bf16 and stored to TMEM columns [tS, tS+64); returns
 // the sum of the fp32 values when kSum (else 0).  kEvery > 0: every kEvery-th pair on the FMA pipe.
@@ -148,8 +138,6 @@ __device__ __forceinline__ float exp_pack_store(const float* x, float sl2, float
       float2 pr;
       if (kEvery > 0 && (i / 2) % (kEvery > 0 ? kEvery : 1) == kEvery - 1) {
         pr = ex2_poly2(e);
-      } else if (FPDT_FWD_EX2_F16) {
-        pr = ex2_f16x2(e);
       } else {
         pr = make_float2(ex2(e.x), ex2(e.y));
       }
@@ -536,11 +524,7 @@ int launch_fwd(const FwdArgs& a, cudaStream_t s) {
   ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
   ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
   if (!ok) return -1;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaFuncSetAttribute(attn_fwd_kernel<D>, cudaFuncAttributeMaxDynamicSharedMemorySize, C::kSmem);
-    attr_set = true;
-  }
+  if (int e = set_max_dynamic_smem((const void*)attn_fwd_kernel<D>, C::kSmem)) return e;
   dim3 grid(a.n_q_rows / 256, a.hq);
   attn_fwd_kernel<D><<<grid, kThreads, C::kSmem, s>>>(tm, a);
   return (int)cudaGetLastError();

@@ -4,6 +4,7 @@
 #include <cmath>
 
 #include "fpdt.h"
+#include "fpdt_diag.h"
 #include "kernels.h"
 
 using namespace fpdt;
@@ -63,7 +64,7 @@ extern "C" int fpdt_debug_pair(int which, int head_dim, int causal, const void* 
   return launch_attn_bwd_bf16(a, head_dim, s) == 0 ? FPDT_OK : FPDT_ERR_CUDA;
 }
 
-// Diagnostic: one all-to-all layout kernel (F3/F10/B2/B7) on caller device buffers (include/fpdt.h).
+// Diagnostic: one all-to-all layout kernel (F3/F10/B2/B7) on caller device buffers (include/fpdt_diag.h).
 extern "C" int fpdt_debug_relayout(int which, const void* src, void* dst, int64_t c, int H, int head_dim, int p,
                                    int elem_bytes, int64_t hs_peer_stride, int64_t hs_row_ld, int hs_head0,
                                    int64_t seq_row_ld, void* stream) {

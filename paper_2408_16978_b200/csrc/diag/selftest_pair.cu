@@ -5,6 +5,7 @@
 // rank 0) issues every MMA; the commit arrives on the mbarrier of both CTAs (multicast).
 #include "attn_tile.cuh"
 #include "fpdt.h"
+#include "fpdt_diag.h"
 
 namespace fpdt {
 namespace {

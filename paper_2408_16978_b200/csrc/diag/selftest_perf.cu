@@ -5,6 +5,7 @@
 
 #include "attn_tile.cuh"
 #include "fpdt.h"
+#include "fpdt_diag.h"
 
 namespace fpdt {
 namespace {

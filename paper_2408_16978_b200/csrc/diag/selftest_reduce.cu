@@ -2,6 +2,7 @@
 // hot path: one CTA per SM repeatedly reduces a 40 KB staging tile ([128 rows][80] fp32, the d = 80 dQ partial of
 // one 128 x 128 (key, query) tile) into global memory, and reports SM cycles per tile.
 #include "fpdt.h"
+#include "fpdt_diag.h"
 #include "sm100_ptx.cuh"
 #include "tma_host.h"
 

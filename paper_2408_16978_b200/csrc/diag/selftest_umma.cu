@@ -11,6 +11,7 @@
 #include "tma_host.h"
 #include "smem_layout.cuh"
 #include "fpdt.h"
+#include "fpdt_diag.h"
 
 namespace fpdt {
 namespace {

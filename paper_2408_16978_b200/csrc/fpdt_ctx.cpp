@@ -15,7 +15,6 @@
 // Streams: compute (= the caller's stream), comm, h2d, d2h; every cross-stream dependency is an event.
 #include <cuda_runtime.h>
 #include <nccl.h>
-#include <cublas_v2.h>
 
 #include <cmath>
 #include <condition_variable>
@@ -64,15 +63,6 @@ struct Fail {
     if (r_ != 0) {                                                                                  \
       g_last_error = std::string(#x) + " failed: " +                                                \
                      (r_ > 0 ? cudaGetErrorString((cudaError_t)r_) : "tensor map / argument error"); \
-      throw Fail{FPDT_ERR_CUDA};                                                                    \
-    }                                                                                               \
-  } while (0)
-
-#define FPDT_CHECK_CUBLAS(x)                                                                        \
-  do {                                                                                              \
-    cublasStatus_t r_ = (x);                                                                        \
-    if (r_ != CUBLAS_STATUS_SUCCESS) {                                                              \
-      g_last_error = std::string(#x) + ": cublas status " + std::to_string((int)r_);                \
       throw Fail{FPDT_ERR_CUDA};                                                                    \
     }                                                                                               \
   } while (0)
@@ -158,7 +148,6 @@ struct fpdt_ctx {
   cudaStream_t s_comm = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   // Q-outer backward: second compute stream (pairs of one query chunk run two at a time) and its slot events
   cudaStream_t s_comp2 = nullptr;
-  cublasHandle_t blas = nullptr;  // fused QKV projection GEMMs (created by the first block call)
   int qo_streams = 2;  // FPDT_BWD_QO_STREAMS (1 or 2)
   // scheduler stress (debug, FPDT_STRESS_NS > 0): a random sleep kernel of up to stress_ns ns goes onto the stream of
   // every copy, all-to-all, GEMM and attention launch, before it (SURVEY §4 tier 5)
@@ -196,6 +185,17 @@ struct fpdt_ctx {
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_fwd, t_bwd;
   size_t n_fwd = 0, n_bwd = 0;
+  // every event created once in create_ctx (destroyed by fpdt_ctx_destroy; null handles are skipped)
+  std::vector<cudaEvent_t> fixed_events() const {
+    std::vector<cudaEvent_t> v = {ev_enter, ev_o_ready, ev_comm_done, ev_d2h_done, ev_h2d_done, ev_tmp, ev_fork, ev_join};
+    for (int b = 0; b < 2; ++b)
+      for (cudaEvent_t e : {ev_slot_free[b], ev_slot_filled[b], ev_q_free[b], ev_q_filled[b], ev_dq_ready[b],
+                            ev_kv_free[b], ev_kv_filled[b], ev_recv_used_c[b], ev_recv_used_d[b]})
+        v.push_back(e);
+    for (int b = 0; b < 4; ++b) v.insert(v.end(), {ev_qo_free[b], ev_qo_filled[b], ev_qo_done[b]});
+    for (int b = 0; b < 3; ++b) v.push_back(ev_qo_send[b]);
+    return v;
+  }
 };
 
 namespace {
@@ -464,47 +464,27 @@ void launch_bwd(fpdt_ctx* ctx, const Config& c, const BwdArgs& a, cudaStream_t s
 }
 
 // ------------------------------------------------------------------------------------------ projection GEMMs
-// Plain library GEMMs (cuBLAS, fp32 accumulation; the fp32 mode uses pedantic FP32, no TF32) on row-major
-// operands, expressed as column-major products of the transposes.
-cublasHandle_t blas_on(fpdt_ctx* ctx, cudaStream_t s) {
-  stress(ctx, s);
-  if (!ctx->blas) FPDT_CHECK_CUBLAS(cublasCreate(&ctx->blas));
-  FPDT_CHECK_CUBLAS(cublasSetStream(ctx->blas, s));
-  return ctx->blas;
-}
-cudaDataType_t blas_type(int dtype) { return dtype == FPDT_BF16 ? CUDA_R_16BF : CUDA_R_32F; }
-cublasComputeType_t blas_compute(int dtype) {
-  return dtype == FPDT_BF16 ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC;
-}
-// Y[rows][n] (row stride ldy) = X[rows][k] (ldx) W[k][n] (ldw)       (forward projection)
+// Hand-written GEMMs (gemm_sm100.cu): tcgen05 with fp32 accumulation in bf16 mode, true-FP32 SIMT in fp32 mode.
+// Y[rows][n] (row stride ldy) = X[rows][k] (ldx) W[k][n] (ldw)       (forward projection); with `sc` the
+// output is scattered straight into the all-to-all send layout instead (the F3 pack fused into the GEMM)
 void gemm_xw(fpdt_ctx* ctx, int dtype, const void* X, int64_t ldx, const void* W, int64_t ldw, void* Y, int64_t ldy,
-             int64_t rows, int64_t k, int64_t n, cudaStream_t s) {
-  const float one = 1.f, zero = 0.f;
-  const cudaDataType_t t = blas_type(dtype);
-  FPDT_CHECK_CUBLAS(cublasGemmEx(blas_on(ctx, s), CUBLAS_OP_N, CUBLAS_OP_N, (int)n, (int)rows, (int)k, &one, W, t,
-                                 (int)ldw, X, t, (int)ldx, &zero, Y, t, (int)ldy, blas_compute(dtype),
-                                 CUBLAS_GEMM_DEFAULT));
+             int64_t rows, int64_t k, int64_t n, cudaStream_t s, const ScatterOut* sc = nullptr) {
+  stress(ctx, s);
+  FPDT_CHECK_LAUNCH(launch_gemm_xw(dtype == FPDT_FP32, X, ldx, W, ldw, Y, ldy, rows, k, n, sc, s));
   ctx->stats.kernel_launches++;
 }
 // dX[rows][k] (ldx) = dY[rows][n] (ldy) W^T                            (hidden-state gradient)
 void gemm_dx(fpdt_ctx* ctx, int dtype, const void* dY, int64_t ldy, const void* W, int64_t ldw, void* dX, int64_t ldx,
              int64_t rows, int64_t k, int64_t n, cudaStream_t s) {
-  const float one = 1.f, zero = 0.f;
-  const cudaDataType_t t = blas_type(dtype);
-  FPDT_CHECK_CUBLAS(cublasGemmEx(blas_on(ctx, s), CUBLAS_OP_T, CUBLAS_OP_N, (int)k, (int)rows, (int)n, &one, W, t,
-                                 (int)ldw, dY, t, (int)ldy, &zero, dX, t, (int)ldx, blas_compute(dtype),
-                                 CUBLAS_GEMM_DEFAULT));
+  stress(ctx, s);
+  FPDT_CHECK_LAUNCH(launch_gemm_dx(dtype == FPDT_FP32, dY, ldy, W, ldw, dX, ldx, rows, k, n, s));
   ctx->stats.kernel_launches++;
 }
 // dW[k][n] fp32 (= or +=) X[rows][k]^T dY[rows][n]                       (weight gradient, summed over chunks)
 void gemm_dw(fpdt_ctx* ctx, int dtype, const void* X, int64_t ldx, const void* dY, int64_t ldy, float* dW, int64_t rows,
              int64_t k, int64_t n, bool accumulate, cudaStream_t s) {
-  const float one = 1.f, beta = accumulate ? 1.f : 0.f;
-  const cudaDataType_t t = blas_type(dtype);
-  FPDT_CHECK_CUBLAS(cublasGemmEx(blas_on(ctx, s), CUBLAS_OP_N, CUBLAS_OP_T, (int)n, (int)k, (int)rows, &one, dY, t,
-                                 (int)ldy, X, t, (int)ldx, &beta, dW, CUDA_R_32F, (int)n,
-                                 dtype == FPDT_BF16 ? CUBLAS_COMPUTE_32F : CUBLAS_COMPUTE_32F_PEDANTIC,
-                                 CUBLAS_GEMM_DEFAULT));
+  stress(ctx, s);
+  FPDT_CHECK_LAUNCH(launch_gemm_dw(dtype == FPDT_FP32, X, ldx, dY, ldy, dW, rows, k, n, accumulate, s));
   ctx->stats.kernel_launches++;
 }
 
@@ -546,14 +526,15 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     }
   }
   // fused projection (fpdt_block_fwd): chunk m of the hidden state is projected on the comm stream just before
-  // its all-to-all; at p = 1 the GEMM writes the combined head layout [C][Hq + 2Hkv][d] directly, at p > 1
-  // it writes the chunk's sequence rows [c][Hq + 2Hkv][d], which the pack kernels read with that row stride.
+  // its all-to-all; the GEMM's epilogue writes the all-to-all send layout [p][c][hq + 2hkv][d] directly
+  // (the pack fused into the GEMM); at p = 1 that layout is the combined head layout [C][Hq + 2Hkv][d] itself.
   const bool proj = pj != nullptr, headbuf = p > 1 || proj;
   const int64_t ntot = (int64_t)(c.Hq + 2 * c.Hkv) * d;
-  uint8_t* pbuf = nullptr;
+  ScatterOut scat;
+  scat.d = d; scat.Hq = c.Hq; scat.Hkv = c.Hkv; scat.hq = hq; scat.hkv = hkv;
+  scat.peer_stride = c.c * hcomb * d;
   if (proj && p == 1)
     for (int b = 0; b < 2; ++b) a2a_recv[b] = (uint8_t*)dev(ctx, B_A2A_RECV0 + b, (size_t)C * hcomb * d * eb);
-  if (proj && p > 1) pbuf = (uint8_t*)dev(ctx, B_PROJ0, (size_t)c.c * ntot * eb);
   const Residency R = make_residency(u, c.offload ? ctx->saved_res_kv : 0, c.offload ? ctx->saved_res_q : 0);
   uint8_t* resstore = (p > 1 && R.n > 0) ? (uint8_t*)dev(ctx, B_RESSTORE, (size_t)R.n * C * hcomb * d * eb) : nullptr;
   auto res_chunk = [&](int64_t m) { return resstore + (size_t)R.slot[(size_t)m] * C * hcomb * d * eb; };
@@ -608,26 +589,20 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       const uint8_t *qm = (const uint8_t*)q + (size_t)m * c.c * c.Hq * d * eb,
                     *km = (const uint8_t*)k + (size_t)m * c.c * c.Hkv * d * eb,
                     *vm = (const uint8_t*)v + (size_t)m * c.c * c.Hkv * d * eb;
-      int64_t src_ld = 0;  // dense caller rows
       if (proj) {
         const uint8_t* xm = (const uint8_t*)pj->x + (size_t)m * c.c * pj->hidden * eb;
-        gemm_xw(ctx, c.dtype, xm, pj->hidden, pj->w, ntot, p == 1 ? recv : pbuf, ntot, c.c, pj->hidden, ntot,
-                ctx->s_comm);
-        qm = pbuf;
-        km = pbuf + (size_t)c.Hq * d * eb;
-        vm = pbuf + (size_t)(c.Hq + c.Hkv) * d * eb;
-        src_ld = ntot;
-      }
-      if (p > 1) {
+        gemm_xw(ctx, c.dtype, xm, pj->hidden, pj->w, ntot, p == 1 ? recv : a2a_send[b], ntot, c.c, pj->hidden, ntot,
+                ctx->s_comm, &scat);
+      } else if (p > 1) {
         FPDT_CHECK_LAUNCH(launch_pack_seq2head(qm, c.c, c.Hq, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d, 0,
-                                               ctx->s_comm, src_ld));
+                                               ctx->s_comm));
         FPDT_CHECK_LAUNCH(launch_pack_seq2head(km, c.c, c.Hkv, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d, hq,
-                                               ctx->s_comm, src_ld));
+                                               ctx->s_comm));
         FPDT_CHECK_LAUNCH(launch_pack_seq2head(vm, c.c, c.Hkv, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d,
-                                               hq + hkv, ctx->s_comm, src_ld));
+                                               hq + hkv, ctx->s_comm));
         ctx->stats.kernel_launches += 3;
-        alltoall(ctx, a2a_send[b], recv, per_peer, c.dtype);
       }
+      if (p > 1) alltoall(ctx, a2a_send[b], recv, per_peer, c.dtype);
       rec(ctx->ev_a2a[m], ctx->s_comm);
       if (c.offload) {
         // F5: offload q_m, kv_m from the receive buffer
@@ -690,7 +665,6 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       a.has_prev = 0;
       a.is_final = (last_kept < 0);
       launch_fwd(ctx, c, a, cs);
-      if (headbuf) rec(ctx->ev_recv_used_c[m & 1], cs);
       // F7/F8: earlier chunks fetched from the host store, double-buffered
       for (int64_t i = 0; i < m; ++i) {
         if (!keep(m, i)) continue;
@@ -728,6 +702,8 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
         ++fetch;
       }
     }
+    // chunk m's receive buffer (its q rows) is read by every pair (m, i) above: free it only after the last one
+    if (headbuf) rec(ctx->ev_recv_used_c[m & 1], cs);
     // output projection of chunk m (fpdt_block_fwd with w_o): y_m = o_m w_o once O_m is final in the sequence layout
     const int64_t od = (int64_t)c.Hq * d;
     if (proj && pj->w_o && p == 1)
@@ -1491,13 +1467,14 @@ int fpdt_ctx_destroy(fpdt_ctx* ctx) {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
     if (ctx->comm) ncclCommDestroy(ctx->comm);
-    if (ctx->blas) cublasDestroy(ctx->blas);
     for (auto& b : ctx->bufs)
       if (b.ptr) cudaFree(b.ptr);
     if (ctx->host) cudaFreeHost(ctx->host);
     if (ctx->host_dkv) cudaFreeHost(ctx->host_dkv);
     for (auto v : {&ctx->ev_off, &ctx->ev_doff, &ctx->ev_dqoff, &ctx->ev_dkvoff, &ctx->ev_a2a})
       for (auto e : *v) cudaEventDestroy(e);
+    for (cudaEvent_t e : ctx->fixed_events())
+      if (e) cudaEventDestroy(e);
     for (auto& pr : ctx->t_fwd) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
     for (auto& pr : ctx->t_bwd) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
     cudaStreamDestroy(ctx->s_comm);

@@ -5,7 +5,28 @@
 #include <cuda_bf16.h>
 #include <stdint.h>
 
+#include <mutex>
+#include <set>
+#include <utility>
+
 namespace fpdt {
+
+// Opt kernel `kern` in to `bytes` of dynamic shared memory on the CURRENT device (cudaFuncSetAttribute acts per
+// device), once per (kernel, device); thread-safe (the in-process group's rank threads launch concurrently).
+// Returns the cudaError_t of the attribute call (0 on success).
+inline int set_max_dynamic_smem(const void* kern, int bytes) {
+  static std::mutex mu;
+  static std::set<std::pair<const void*, int>> done;
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return (int)e;
+  std::lock_guard<std::mutex> lk(mu);
+  if (done.count({kern, dev})) return 0;
+  e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (e != cudaSuccess) return (int)e;
+  done.insert({kern, dev});
+  return 0;
+}
 
 // One tensor view for the attention kernels: a bf16 (or fp32) buffer laid out [rows][heads][head_dim].
 struct HeadView {
@@ -101,6 +122,25 @@ int launch_pack_seq2head(const void* src, int64_t c, int H, int head_dim, int p,
 int launch_unpack_head2seq(const void* src, int64_t src_peer_stride_elems, int64_t src_row_ld, int src_head0,
                            int64_t c, int H, int head_dim, int p, int elem_bytes, void* dst, cudaStream_t s,
                            int64_t dst_row_ld = 0);
+// Projection GEMMs (gemm_sm100.cu; fpdt_block_fwd/bwd).  Row-major operands with row strides in elements; bf16 mode
+// (dtype_fp32 = 0) on tcgen05 with fp32 accumulation, fp32 mode on true-FP32 SIMT.  Returns 0, a cudaError_t, or -1
+// (tensor map encoding failed).
+// Optional scatter of the forward projection's output into the all-to-all send layout: column j of the projected
+// rows (head j / d of the q | k | v heads) goes to send[peer][row][slot][e] (peer_stride elements per peer).
+struct ScatterOut {
+  int d = 0, Hq = 0, Hkv = 0, hq = 0, hkv = 0;
+  int64_t peer_stride = 0;
+};
+// Y[rows][n] (ldy) = X[rows][k] (ldx) W[k][n] (ldw); scatter != nullptr: Y is the send buffer (ldy unused)
+int launch_gemm_xw(int dtype_fp32, const void* X, int64_t ldx, const void* W, int64_t ldw, void* Y, int64_t ldy,
+                   int64_t rows, int64_t k, int64_t n, const ScatterOut* scatter, cudaStream_t s);
+// dX[rows][k] (ldx) = dY[rows][n] (ldy) W^T, W[k][n] (ldw)
+int launch_gemm_dx(int dtype_fp32, const void* dY, int64_t ldy, const void* W, int64_t ldw, void* dX, int64_t ldx,
+                   int64_t rows, int64_t k, int64_t n, cudaStream_t s);
+// dW[k][n] fp32 (= or +=) X[rows][k]^T dY[rows][n]
+int launch_gemm_dw(int dtype_fp32, const void* X, int64_t ldx, const void* dY, int64_t ldy, float* dW, int64_t rows,
+                   int64_t k, int64_t n, bool accumulate, cudaStream_t s);
+
 // debug: one thread sleeps about ns nanoseconds on stream s (scheduler stress, FPDT_STRESS_NS)
 int launch_stress_sleep(uint32_t ns, cudaStream_t s);
 // lse transpose: src[h*ld + t] (log2-domain) -> dst[t*dst_ld + dst_head0 + h] (natural log)

@@ -22,10 +22,11 @@ STATUS_NAMES = {0: "FPDT_OK", 1: "FPDT_ERR_ARG", 2: "FPDT_ERR_DIVISIBILITY", 3: 
 # names of every symbol include/fpdt.h declares (checked by the CPU tests against the built library)
 EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_attn_fwd", "fpdt_attn_bwd",
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
-            "fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_debug_pair", "fpdt_group_create",
-            "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity", "fpdt_set_residency",
-            "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes", "fpdt_selftest_pair", "fpdt_debug_relayout",
-            "fpdt_selftest_softmax", "fpdt_selftest_reduce")
+            "fpdt_group_create", "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity",
+            "fpdt_set_residency", "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes")
+# include/fpdt_diag.h (libfpdt_diag.so: micro-benchmarks and direct kernel launches, not on the FPDT path)
+DIAG_EXPORTED = ("fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_selftest_softmax", "fpdt_selftest_reduce",
+                 "fpdt_selftest_pair", "fpdt_debug_relayout", "fpdt_debug_pair")
 
 
 class FpdtError(RuntimeError):
@@ -90,6 +91,10 @@ def _declare(lib):
     lib.fpdt_kernel_time.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int64),
                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int64), c_int]
     lib.fpdt_kernel_time.restype = c_int
+
+
+def _declare_diag(lib):
+    P = c_void_p
     lib.fpdt_selftest_umma.argtypes = [c_int, c_int, P, P, c_int, c_int, P, P]
     lib.fpdt_selftest_umma.restype = c_int
     lib.fpdt_selftest_reduce.argtypes = [c_int, c_int, c_int, c_int, P, P, P]
@@ -105,6 +110,11 @@ def _declare(lib):
     lib.fpdt_selftest_perf.restype = c_int
     lib.fpdt_debug_pair.argtypes = [c_int, c_int, c_int, P, P, P, P, P, P, P, P, P, c_int64, c_int, c_int, P, c_int, P]
     lib.fpdt_debug_pair.restype = c_int
+
+
+def diag():
+    """libfpdt_diag.so (include/fpdt_diag.h)."""
+    return _lib.load_diag()
 
 
 def lib():

@@ -9,8 +9,8 @@ import pytest
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-def _declared():
-    with open(os.path.join(ROOT, "include", "fpdt.h")) as f:
+def _declared(header="fpdt.h"):
+    with open(os.path.join(ROOT, "include", header)) as f:
         src = f.read()
     return sorted(set(re.findall(r"\b(fpdt_[a-z_0-9]+)\s*\(", src)))
 
@@ -38,6 +38,21 @@ def test_library_exports_every_declared_symbol(lib):
 def test_binding_lists_every_symbol():
     from paper_2408_16978_b200 import fpdt
     assert sorted(fpdt.EXPORTED) == _declared()
+
+
+def test_diag_library_is_separate(lib):
+    """Diagnostics (micro-benchmarks, direct kernel launches) live in libfpdt_diag.so, not in the product library;
+    the product library has no cuBLAS dependency (the projection GEMMs are the library's own kernels)."""
+    from paper_2408_16978_b200 import _lib, fpdt
+    diag = _lib.load_diag()
+    assert sorted(fpdt.DIAG_EXPORTED) == _declared("fpdt_diag.h")
+    assert not [n for n in fpdt.DIAG_EXPORTED if not hasattr(diag, n)]
+    import subprocess
+    so = os.path.join(ROOT, "paper_2408_16978_b200", "libfpdt.so")
+    syms = subprocess.run(["nm", "-D", so], capture_output=True, text=True, check=True).stdout
+    assert "fpdt_selftest" not in syms and "fpdt_debug" not in syms
+    deps = subprocess.run(["readelf", "-d", so], capture_output=True, text=True, check=True).stdout
+    assert "cublas" not in deps.lower() and "cublas" not in syms.lower()
 
 
 def test_global_token_matches_layout_contract(lib):

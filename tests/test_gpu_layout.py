@@ -16,7 +16,7 @@ pytestmark = pytest.mark.gpu
 
 def _relayout(which, src, dst, c, H, d, p, eb, peer_stride, row_ld, head0, seq_ld):
     from paper_2408_16978_b200 import fpdt
-    rc = fpdt.lib().fpdt_debug_relayout(which, ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()), c, H,
+    rc = fpdt.diag().fpdt_debug_relayout(which, ctypes.c_void_p(src.data_ptr()), ctypes.c_void_p(dst.data_ptr()), c, H,
                                         d, p, eb, peer_stride, row_ld, head0, seq_ld, None)
     assert rc == 0, rc
     torch.cuda.synchronize()
@@ -77,7 +77,7 @@ def test_relayout_argument_errors():
     from paper_2408_16978_b200 import fpdt
     x = torch.zeros(1024, device="cuda")
     P = ctypes.c_void_p(x.data_ptr())
-    lib = fpdt.lib()
+    lib = fpdt.diag()
     assert lib.fpdt_debug_relayout(2, P, P, 4, 4, 64, 1, 4, 1, 1, 0, 0, None) == fpdt.FPDT_ERR_ARG   # which
     assert lib.fpdt_debug_relayout(0, P, P, 4, 6, 64, 4, 4, 1, 1, 0, 0, None) == fpdt.FPDT_ERR_ARG   # H % p
     assert lib.fpdt_debug_relayout(0, P, P, 4, 4, 60, 1, 2, 1, 1, 0, 0, None) == fpdt.FPDT_ERR_ARG   # 16 B vectors

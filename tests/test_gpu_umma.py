@@ -14,7 +14,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(scope="module")
 def lib():
     from paper_2408_16978_b200 import _lib
-    return _lib.load()
+    return _lib.load_diag()
 
 
 @pytest.fixture(scope="module")

@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2408_16978_b200 import _lib
 
-lib = _lib.load()
+lib = _lib.load_diag()
 out = torch.zeros(4, device="cuda")
 def run(what, n, iters):
     rc = lib.fpdt_selftest_perf(what, n, iters, ctypes.c_void_p(out.data_ptr()), None)

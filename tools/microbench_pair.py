@@ -1,4 +1,4 @@
-"""CTA-pair MMA micro-benchmark (include/fpdt.h fpdt_selftest_pair): SM cycles per SS MMA for the single-CTA
+"""CTA-pair MMA micro-benchmark (include/fpdt_diag.h fpdt_selftest_pair): SM cycles per SS MMA for the single-CTA
 M = 128 form and the CTA-pair M = 256 form (cta_group::2) at several N, all 148 SMs busy.  The pair form does twice
 the work of one M = 128 MMA per issue; per SM it reads its own 128 x 16 A slice and half of B."""
 import json
@@ -11,7 +11,7 @@ import torch  # noqa: E402
 from paper_2408_16978_b200 import fpdt  # noqa: E402
 
 out = torch.zeros(1, device="cuda")
-lib = fpdt.lib()
+lib = fpdt.diag()
 res = []
 for mode in (0, 1, 2):
     for n in (64, 80, 96, 128, 160, 192, 256):

@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2408_16978_b200 import _lib
 
-lib = _lib.load()
+lib = _lib.load_diag()
 g = torch.zeros(2 * 148 * 10240 + 1024, device="cuda")
 out = torch.zeros(4, device="cuda")
 names = {0: "3 swizzled boxes", 1: "1-D bulk 40KB", 2: "10 x 4KB bulk", 3: "1 box [128x80]", 4: "bulk STORE 40KB",

@@ -6,7 +6,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import torch
 from paper_2408_16978_b200 import _lib
 
-lib = _lib.load()
+lib = _lib.load_diag()
 out = torch.zeros(4, device="cuda")
 for what, cols, thr_list in ((0, 128, (128, 256)), (1, 64, (128, 256, 512))):
     for every, name in ((4, "25% poly"), (0, "all MUFU"), (2, "50% poly"), (8, "12% poly")):

@@ -49,7 +49,7 @@ def main():
     args = ap.parse_args()
     H, d = args.heads, args.d
     Hkv = args.kv_heads or H
-    lib = _lib.load()
+    lib = _lib.load_diag()
     P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None  # noqa: E731
     bf = torch.bfloat16
     torch.manual_seed(0)

@@ -15,7 +15,7 @@ C = int(sys.argv[2]) if len(sys.argv) > 2 else 65536
 H = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 d = int(sys.argv[4]) if len(sys.argv) > 4 else 80
 cta = int(sys.argv[5]) if len(sys.argv) > 5 else 0
-lib = _lib.load()
+lib = _lib.load_diag()
 torch.manual_seed(0)
 bf = torch.bfloat16
 q, k, v, do = (torch.randn(C, H, d, device="cuda").to(bf) for _ in range(4))
