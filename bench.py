@@ -96,6 +96,27 @@ class ClockSampler:
                 "reasons": reasons, "samples": len(self.samples)}
 
 
+def max_seq_record():
+    """The longest sequence one B200 sustained through the C-ABI (fwd + bwd, offload on), from the committed
+    tools/max_seq.py runs (a separate multi-minute job, not repeated inside this bench)."""
+    best = None
+    for name in ("r02_max_seq.jsonl", "r01_max_seq.jsonl", "r01_max_seq_8b_v2.jsonl"):
+        path = os.path.join(ROOT, "profiles", name)
+        if not os.path.exists(path):
+            continue
+        with open(path) as f:
+            for line in f:
+                try:
+                    r = json.loads(line)
+                except ValueError:
+                    continue
+                S = r.get("S") or r.get("seq")
+                if S and (best is None or S > best["tokens"]):
+                    best = {"tokens": S, "shape": {k: r.get(k) for k in ("heads_q", "heads_kv", "head_dim", "chunk")
+                                                   if k in r}, "step_s": r.get("step_s"), "source": f"profiles/{name}"}
+    return best
+
+
 def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
@@ -240,6 +261,7 @@ def run_ours(args):
     wall = time.perf_counter() - wall0
     clocks = sampler.stop()
     st1 = ctx.stats()
+    gap_ms, n_gaps = ctx.kernel_gaps()
     fwd_ms, n_fwd, bwd_ms, n_bwd = ctx.kernel_time(reset=True)
     ctx.set_kernel_timing(False)
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
@@ -373,6 +395,13 @@ def run_ours(args):
         "host_link": {"h2d_GBps": h2d_lib / (ms / 1e3) / 1e9, "d2h_GBps": d2h_lib / (ms / 1e3) / 1e9,
                       "measured_peak_GBps": {"h2d": 55.6, "d2h": 57.3}},
         "a2a_bytes_per_step": (st1["bytes_a2a"] - st0["bytes_a2a"]) // args.steps,
+        # compute-stream accounting from the library's per-launch CUDA events: time the compute stream spent between
+        # consecutive pair kernels of one call (waiting for an exchange, a fetch or a support kernel), and the step
+        # time not covered by pair kernels at all (that plus the fwd/bwd preambles, D preprocess and converts)
+        "compute_stream": {"pair_kernel_ms_per_step": (fwd_ms + bwd_ms) / args.steps,
+                           "gap_ms_per_step": gap_ms / args.steps, "gaps_per_step": n_gaps // args.steps,
+                           "exposed_ms_per_step": ms - (fwd_ms + bwd_ms) / args.steps},
+        "max_seq_per_gpu": max_seq_record(),
         "device_bytes_library": st1["device_bytes"],
         "wall_s_timed": wall,
         "cpu_baseline": cpu,

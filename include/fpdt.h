@@ -226,6 +226,14 @@ int fpdt_set_kernel_timing(fpdt_ctx* ctx, int enable);
 int fpdt_kernel_time(fpdt_ctx* ctx, double* fwd_ms, int64_t* fwd_launches, double* bwd_ms, int64_t* bwd_launches,
                      int reset);
 
+/* Compute-stream stall accounting (SURVEY §8(a) stream/event skeleton): over the attention launches recorded since the
+ * last reset of fpdt_kernel_time, the summed time between the end of one launch and the start of the next launch of
+ * the same fpdt call on the same stream (*gap_ms), and the number of such gaps (*n_gaps).  A gap is time the
+ * compute stream spent waiting for a chunk exchange, a host fetch or a small support kernel instead of running pair
+ * kernels.  Synchronises on the recorded events; call it before fpdt_kernel_time(..., reset = 1).
+ * Returns FPDT_OK, FPDT_ERR_ARG or FPDT_ERR_CUDA. */
+int fpdt_kernel_gaps(fpdt_ctx* ctx, double* gap_ms, int64_t* n_gaps);
+
 #ifdef __cplusplus
 }
 #endif

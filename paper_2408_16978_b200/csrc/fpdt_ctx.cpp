@@ -112,7 +112,7 @@ enum BufId {
   B_STORE, B_D, B_DQDEV, B_QSLOT0, B_QSLOT1, B_DOSLOT0, B_DOSLOT1, B_DQSLOT0, B_DQSLOT1, B_DKACC, B_DVACC,
   B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_RESSTORE, B_DORES, B_DQRES, B_DKVSLOT0,
   B_DKVSLOT1, B_DKVRES, B_KVSLOT2, B_KVSLOT3, B_DKVSLOT2, B_DKVSLOT3, B_QOSEND, B_QORECV, B_PROJ0, B_PROJ1,
-  B_PROJ2, B_DOUT, B_NUM
+  B_PROJ2, B_DOUT, B_OHAT1, B_BWD_SEND1, B_BWD_RECV1, B_NUM
 };
 
 }  // namespace
@@ -164,7 +164,7 @@ struct fpdt_ctx {
   std::vector<cudaEvent_t> ev_off, ev_doff, ev_dqoff, ev_dkvoff, ev_a2a;
   cudaEvent_t ev_enter = nullptr, ev_slot_free[2] = {}, ev_slot_filled[2] = {}, ev_q_free[2] = {}, ev_q_filled[2] = {},
               ev_dq_ready[2] = {}, ev_kv_free[2] = {}, ev_kv_filled[2] = {}, ev_recv_used_c[2] = {},
-              ev_recv_used_d[2] = {}, ev_o_ready = nullptr, ev_comm_done = nullptr, ev_d2h_done = nullptr,
+              ev_recv_used_d[2] = {}, ev_ohat_free[2] = {}, ev_bsend_free[2] = {}, ev_o_ready = nullptr, ev_comm_done = nullptr, ev_d2h_done = nullptr,
               ev_h2d_done = nullptr, ev_tmp = nullptr;
   // saved state
   bool fwd_done = false;
@@ -184,13 +184,16 @@ struct fpdt_ctx {
   // kernel timing
   bool timing = false;
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_fwd, t_bwd;
+  std::vector<std::pair<cudaStream_t, int64_t>> t_fwd_src, t_bwd_src;  // launch stream and call number per launch
   size_t n_fwd = 0, n_bwd = 0;
+  int64_t call_seq = 0;  // fpdt_attn_* / fpdt_block_* calls so far (kernel-gap accounting)
   // every event created once in create_ctx (destroyed by fpdt_ctx_destroy; null handles are skipped)
   std::vector<cudaEvent_t> fixed_events() const {
     std::vector<cudaEvent_t> v = {ev_enter, ev_o_ready, ev_comm_done, ev_d2h_done, ev_h2d_done, ev_tmp, ev_fork, ev_join};
     for (int b = 0; b < 2; ++b)
       for (cudaEvent_t e : {ev_slot_free[b], ev_slot_filled[b], ev_q_free[b], ev_q_filled[b], ev_dq_ready[b],
-                            ev_kv_free[b], ev_kv_filled[b], ev_recv_used_c[b], ev_recv_used_d[b]})
+                            ev_kv_free[b], ev_kv_filled[b], ev_recv_used_c[b], ev_recv_used_d[b], ev_ohat_free[b],
+                            ev_bsend_free[b]})
         v.push_back(e);
     for (int b = 0; b < 4; ++b) v.insert(v.end(), {ev_qo_free[b], ev_qo_filled[b], ev_qo_done[b]});
     for (int b = 0; b < 3; ++b) v.push_back(ev_qo_send[b]);
@@ -427,13 +430,16 @@ struct TimedScope {
   TimedScope(fpdt_ctx* c, bool f, cudaStream_t st) : ctx(c), fwd(f), s(st) {
     if (!ctx->timing) return;
     auto& v = fwd ? ctx->t_fwd : ctx->t_bwd;
+    auto& src = fwd ? ctx->t_fwd_src : ctx->t_bwd_src;
     size_t& n = fwd ? ctx->n_fwd : ctx->n_bwd;
     if (v.size() <= n) {
       cudaEvent_t a, b;
       FPDT_CHECK_CUDA(cudaEventCreate(&a));
       FPDT_CHECK_CUDA(cudaEventCreate(&b));
       v.push_back({a, b});
+      src.push_back({nullptr, 0});
     }
+    src[n] = {s, ctx->call_seq};
     ev = &v[n++];
     rec(ev->first, s);
   }
@@ -504,6 +510,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     o_acc = (float*)dev(ctx, B_OACC, (size_t)C * hq * d * 4);
     lse_acc = (float*)dev(ctx, B_LSEACC, (size_t)hq * C * 4);
   }
+  ++ctx->call_seq;
   ensure_events(ctx->ev_off, u);
   ensure_events(ctx->ev_a2a, u);
   rec(ctx->ev_enter, cs);
@@ -516,7 +523,11 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   // device store for resident mode with p > 1: gathered [S][hcomb][d]
   uint8_t* store = nullptr;
   if (!c.offload && p > 1) store = (uint8_t*)dev(ctx, B_STORE, (size_t)c.S * hcomb * d * eb);
-  uint8_t* o_hat = p > 1 ? (uint8_t*)dev(ctx, B_OHAT, (size_t)C * hq * d * eb) : nullptr;
+  // head-layout output of a chunk before its return all-to-all (p > 1), double-buffered so that chunk m+1's pairs
+  // run while chunk m's output is exchanged
+  uint8_t* o_hat[2] = {nullptr, nullptr};
+  if (p > 1)
+    for (int b = 0; b < 2; ++b) o_hat[b] = (uint8_t*)dev(ctx, b ? B_OHAT1 : B_OHAT, (size_t)C * hq * d * eb);
   uint8_t* a2a_send[2] = {nullptr, nullptr};
   uint8_t* a2a_recv[2] = {nullptr, nullptr};
   if (p > 1) {
@@ -547,6 +558,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   for (int b = 0; b < 2; ++b) {
     rec(ctx->ev_recv_used_c[b], cs);
     rec(ctx->ev_recv_used_d[b], cs);
+    rec(ctx->ev_ohat_free[b], cs);
   }
   // p == 1 with offload: the head-layout chunk IS the caller's rows; offload all chunks up front
   if (p == 1 && c.offload && !proj) {
@@ -560,12 +572,56 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       rec(ctx->ev_off[m], ctx->s_d2h);
     }
   }
+  // receive buffer of chunk m in the head layout (headbuf)
+  auto recv_of = [&](int64_t m) -> uint8_t* {
+    return !c.offload ? store + (size_t)m * C * hcomb * d * eb : R.slot[(size_t)m] >= 0 ? res_chunk(m)
+                                                                                      : a2a_recv[m & 1];
+  };
+  // F3/F4/F5 for chunk m on the comm (and d2h) stream: projection or pack, all-to-all seq -> head, offload of q_m
+  // and kv_m from the receive buffer.  Enqueued one chunk AHEAD of the compute (software pipeline): the exchange of
+  // chunk m+1 is on the comm stream before the output exchange of chunk m, so it runs during chunk m's pairs and only
+  // the first chunk's exchange (and the last chunk's output return) is exposed.
+  auto exchange = [&](int64_t m) {
+    const int b = (int)(m & 1);
+    uint8_t* recv = recv_of(m);
+    wait(ctx->s_comm, ctx->ev_recv_used_c[b]);
+    wait(ctx->s_comm, ctx->ev_recv_used_d[b]);
+    const size_t per_peer = (size_t)c.c * hcomb * d;
+    if (proj) {
+      const uint8_t* xm = (const uint8_t*)pj->x + (size_t)m * c.c * pj->hidden * eb;
+      gemm_xw(ctx, c.dtype, xm, pj->hidden, pj->w, ntot, p == 1 ? recv : a2a_send[b], ntot, c.c, pj->hidden, ntot,
+              ctx->s_comm, &scat);
+    } else {
+      const uint8_t *qm = (const uint8_t*)q + (size_t)m * c.c * c.Hq * d * eb,
+                    *km = (const uint8_t*)k + (size_t)m * c.c * c.Hkv * d * eb,
+                    *vm = (const uint8_t*)v + (size_t)m * c.c * c.Hkv * d * eb;
+      FPDT_CHECK_LAUNCH(launch_pack_seq2head(qm, c.c, c.Hq, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d, 0,
+                                             ctx->s_comm));
+      FPDT_CHECK_LAUNCH(launch_pack_seq2head(km, c.c, c.Hkv, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d, hq,
+                                             ctx->s_comm));
+      FPDT_CHECK_LAUNCH(launch_pack_seq2head(vm, c.c, c.Hkv, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d,
+                                             hq + hkv, ctx->s_comm));
+      ctx->stats.kernel_launches += 3;
+    }
+    if (p > 1) alltoall(ctx, a2a_send[b], recv, per_peer, c.dtype);
+    rec(ctx->ev_a2a[m], ctx->s_comm);
+    if (c.offload) {
+      wait(ctx->s_d2h, ctx->ev_a2a[m]);
+      const size_t pitch = (size_t)hcomb * d * eb;
+      if (!R.q(m)) d2h_2d(ctx, ctx->host + hl.q(m), row_q, recv, pitch, row_q, C);
+      if (!R.kv(m)) d2h_2d(ctx, ctx->host + hl.kv(m, u), row_kv2, recv + row_q, pitch, row_kv2, C);
+      rec(ctx->ev_off[m], ctx->s_d2h);
+      rec(ctx->ev_recv_used_d[b], ctx->s_d2h);
+    }
+  };
   int fetch = 0;
   int64_t high = 0;
   // block sparsity (§5.6): skipped key chunks are neither fetched nor computed
   const std::vector<uint8_t>& plan = ctx->saved_plan;
   auto keep = [&](int64_t m, int64_t i) { return plan.empty() || plan[(size_t)(m * u + i)] != 0; };
+  if (headbuf) exchange(0);
   for (int64_t m = 0; m < u; ++m) {
+    if (headbuf && m + 1 < u) exchange(m + 1);
     int64_t last_kept = -1;  // the last earlier key chunk chunk m attends
     for (int64_t i = 0; i < m; ++i)
       if (keep(m, i)) last_kept = i;
@@ -579,42 +635,8 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       q_row0 = m * C;
       kv_row0_cur = m * C;
     } else {
-      // F3/F4: pack q,k,v rows of slot m and all-to-all (seq -> head)
-      const int b = (int)(m & 1);
-      uint8_t* recv = !c.offload ? store + (size_t)m * C * hcomb * d * eb : R.slot[(size_t)m] >= 0 ? res_chunk(m)
-                                                                                               : a2a_recv[b];
-      wait(ctx->s_comm, ctx->ev_recv_used_c[b]);
-      wait(ctx->s_comm, ctx->ev_recv_used_d[b]);
-      const size_t per_peer = (size_t)c.c * hcomb * d;
-      const uint8_t *qm = (const uint8_t*)q + (size_t)m * c.c * c.Hq * d * eb,
-                    *km = (const uint8_t*)k + (size_t)m * c.c * c.Hkv * d * eb,
-                    *vm = (const uint8_t*)v + (size_t)m * c.c * c.Hkv * d * eb;
-      if (proj) {
-        const uint8_t* xm = (const uint8_t*)pj->x + (size_t)m * c.c * pj->hidden * eb;
-        gemm_xw(ctx, c.dtype, xm, pj->hidden, pj->w, ntot, p == 1 ? recv : a2a_send[b], ntot, c.c, pj->hidden, ntot,
-                ctx->s_comm, &scat);
-      } else if (p > 1) {
-        FPDT_CHECK_LAUNCH(launch_pack_seq2head(qm, c.c, c.Hq, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d, 0,
-                                               ctx->s_comm));
-        FPDT_CHECK_LAUNCH(launch_pack_seq2head(km, c.c, c.Hkv, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d, hq,
-                                               ctx->s_comm));
-        FPDT_CHECK_LAUNCH(launch_pack_seq2head(vm, c.c, c.Hkv, d, p, eb, a2a_send[b], per_peer, (int64_t)hcomb * d,
-                                               hq + hkv, ctx->s_comm));
-        ctx->stats.kernel_launches += 3;
-      }
-      if (p > 1) alltoall(ctx, a2a_send[b], recv, per_peer, c.dtype);
-      rec(ctx->ev_a2a[m], ctx->s_comm);
-      if (c.offload) {
-        // F5: offload q_m, kv_m from the receive buffer
-        wait(ctx->s_d2h, ctx->ev_a2a[m]);
-        const size_t pitch = (size_t)hcomb * d * eb;
-        if (!R.q(m)) d2h_2d(ctx, ctx->host + hl.q(m), row_q, recv, pitch, row_q, C);
-        if (!R.kv(m)) d2h_2d(ctx, ctx->host + hl.kv(m, u), row_kv2, recv + row_q, pitch, row_kv2, C);
-        rec(ctx->ev_off[m], ctx->s_d2h);
-        rec(ctx->ev_recv_used_d[b], ctx->s_d2h);
-      }
       wait(cs, ctx->ev_a2a[m]);
-      const uint8_t* base = c.offload ? recv : store;
+      const uint8_t* base = c.offload ? recv_of(m) : store;
       qv = {base, c.offload ? C : c.S, hcomb, 0};
       kv = {base, c.offload ? C : c.S, hcomb, hq};
       vv = {base, c.offload ? C : c.S, hcomb, hq + hkv};
@@ -638,7 +660,8 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       a.lse_user = lse ? lse + (size_t)m * C * c.Hq : nullptr;
       a.lse_user_ld = c.Hq;
     } else {
-      a.o_out = o_hat;
+      wait(cs, ctx->ev_ohat_free[m & 1]);  // chunk m-2's output has left this buffer
+      a.o_out = o_hat[m & 1];
       a.o_ld = (int64_t)hq * d;
     }
     a.lse_save = lse_save + m * C;
@@ -710,11 +733,13 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       gemm_xw(ctx, c.dtype, (const uint8_t*)o + (size_t)m * C * od * eb, od, pj->w_o, pj->hidden,
               (uint8_t*)pj->y + (size_t)m * C * pj->hidden * eb, pj->hidden, C, od, pj->hidden, cs);
     if (p > 1) {
-      // F10: all-to-all of O_m back to the sequence layout, then unpack into the caller's rows of slot m
+      // F10: all-to-all of O_m back to the sequence layout, then unpack into the caller's rows of slot m (on the comm
+      // stream behind chunk m+1's exchange, so it overlaps chunk m+1's pairs)
       rec(ctx->ev_o_ready, cs);
       wait(ctx->s_comm, ctx->ev_o_ready);
       uint8_t* back = (uint8_t*)dev(ctx, B_BWD_RECV, (size_t)C * hq * d * eb);
-      alltoall(ctx, o_hat, back, (size_t)c.c * hq * d, c.dtype);
+      alltoall(ctx, o_hat[m & 1], back, (size_t)c.c * hq * d, c.dtype);
+      rec(ctx->ev_ohat_free[m & 1], ctx->s_comm);
       FPDT_CHECK_LAUNCH(launch_unpack_head2seq(back, (int64_t)c.c * hq * d, (int64_t)hq * d, 0, c.c, c.Hq, d, p, eb,
                                                (uint8_t*)o + (size_t)m * c.c * c.Hq * d * eb, ctx->s_comm));
       ctx->stats.kernel_launches++;
@@ -727,15 +752,13 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
         float* lr = (float*)dev(ctx, B_LSE_RECV, (size_t)C * hq * 4);
         FPDT_CHECK_LAUNCH(launch_lse_to_user(lse_save + m * C, c.S, C, hq, lt, hq, 0, ctx->s_comm));
         alltoall(ctx, lt, lr, (size_t)c.c * hq, FPDT_FP32);
-        // unpack [p][c][hq] -> [c][Hq]: treat each row of hq floats as one head of hq*4 bytes... use 1-float heads
+        // unpack [p][c][hq] -> [c][Hq]: rank r's block holds heads [r hq, (r+1) hq) of every row
         for (int r = 0; r < p; ++r)
           FPDT_CHECK_CUDA(cudaMemcpy2DAsync(lse + (size_t)m * c.c * c.Hq + (size_t)r * hq, (size_t)c.Hq * 4,
                                             lr + (size_t)r * c.c * hq, (size_t)hq * 4, (size_t)hq * 4, c.c,
                                             cudaMemcpyDeviceToDevice, ctx->s_comm));
         ctx->stats.kernel_launches++;
       }
-      rec(ctx->ev_comm_done, ctx->s_comm);
-      wait(cs, ctx->ev_comm_done);  // o_hat reuse by the next chunk waits for the send
     }
   }
   ctx->stats.fetch_slots_highwater = std::max(ctx->stats.fetch_slots_highwater, high);
@@ -895,6 +918,7 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
       } else {
         qi = {res_chunk(i), C, hcomb, 0};
         doi = {dores + (size_t)R.qslot[(size_t)i] * C * 2 * hq * d * eb, C, 2 * hq, hq};
+        wait(cs, ctx->ev_a2a[i]);  // its (O, dO) exchange and D_i
       }
     } else {
       // B4 (once per outer iteration): fetch q_i, dO_i
@@ -1018,6 +1042,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
     gemm_dw(ctx, c.dtype, o, od, dout, pj->hidden, pj->dw_o, c.s_local, od, pj->hidden, false, cs);
     dout = dO;
   }
+  ++ctx->call_seq;
   ensure_events(ctx->ev_doff, u);
   ensure_events(ctx->ev_dqoff, u);
   ensure_events(ctx->ev_a2a, u);
@@ -1076,8 +1101,13 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
         rec(ctx->ev_doff[m], ctx->s_d2h);
       }
     }
-    rec(ctx->ev_comm_done, ctx->s_comm);
-    wait(cs, ctx->ev_comm_done);
+    // The chunk loop below waits for chunk i's exchange only where it reads chunk i (offloaded chunks through the
+    // dO_i offload -> fetch chain, resident ones by ev_a2a[i]), so chunk 0's pairs start while the later (O, dO)
+    // exchanges still run on the comm stream.  The resident-mode launches span many chunks: they wait for all.
+    if (!c.offload) {
+      rec(ctx->ev_comm_done, ctx->s_comm);
+      wait(cs, ctx->ev_comm_done);
+    }
     do_h = gathered;
     do_rows = c.S;
     do_heads = 2 * hq;
@@ -1086,8 +1116,16 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
 
   float* dk_acc = (float*)dev(ctx, B_DKACC, (size_t)C * hkv * d * 4);
   float* dv_acc = (float*)dev(ctx, B_DVACC, (size_t)C * hkv * d * 4);
-  uint8_t* bsend = p > 1 ? (uint8_t*)dev(ctx, B_BWD_SEND, (size_t)C * hcomb * d * eb) : nullptr;
-  uint8_t* brecv = p > 1 ? (uint8_t*)dev(ctx, B_BWD_RECV, (size_t)C * hcomb * d * eb) : nullptr;
+  // B7 buffers (p > 1), double-buffered by the outer index j: outer iteration j+1 fills one while chunk j's final
+  // dq, dk, dv leave through the other
+  uint8_t *bsend2[2] = {nullptr, nullptr}, *brecv2[2] = {nullptr, nullptr};
+  if (p > 1)
+    for (int b = 0; b < 2; ++b) {
+      bsend2[b] = (uint8_t*)dev(ctx, b ? B_BWD_SEND1 : B_BWD_SEND, (size_t)C * hcomb * d * eb);
+      brecv2[b] = (uint8_t*)dev(ctx, b ? B_BWD_RECV1 : B_BWD_RECV, (size_t)C * hcomb * d * eb);
+      rec(ctx->ev_bsend_free[b], cs);
+    }
+  uint8_t* bsend = nullptr;  // the send buffer of the current outer iteration
 
   // fused projection (fpdt_block_bwd): chunk j's final dq, dk, dv land in a chunk buffer of sequence rows
   // [c][Hq + 2Hkv][d] (double-buffered by j), from which the projection backward forms dx_j and adds x_j^T dqkv_j
@@ -1130,6 +1168,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
     }
     rec(ctx->ev_o_ready, cs);
     wait(ctx->s_comm, ctx->ev_o_ready);
+    uint8_t* brecv = brecv2[j & 1];
     alltoall(ctx, bsend, brecv, (size_t)c.c * hcomb * d, c.dtype);
     const int64_t pst = (int64_t)c.c * hcomb * d, rld = (int64_t)hcomb * d;
     uint8_t *dqj = (uint8_t*)dq + (size_t)j * c.c * c.Hq * d * eb, *dkj = (uint8_t*)dk + (size_t)j * c.c * c.Hkv * d * eb,
@@ -1147,8 +1186,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
                                              dst_ld));
     ctx->stats.kernel_launches += 3;
     proj_bwd(j, ctx->s_comm);  // projection backward of chunk j overlaps the next outer iteration
-    rec(ctx->ev_comm_done, ctx->s_comm);
-    wait(cs, ctx->ev_comm_done);  // bsend / brecv reuse by the next outer iteration
+    rec(ctx->ev_bsend_free[j & 1], ctx->s_comm);  // bsend / brecv [j & 1] reusable by outer iteration j + 2
   };
   auto set_kv_out = [&](BwdArgs& a, int64_t j) {
     if (p == 1 && proj) {
@@ -1186,6 +1224,10 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       vv = {store, c.S, hcomb, hq + hkv};
     }
     for (int64_t j = 0; j < u; ++j) {
+      if (p > 1) {
+        bsend = bsend2[j & 1];
+        wait(cs, ctx->ev_bsend_free[j & 1]);
+      }
       BwdArgs a;
       a.q = qv; a.k = kv; a.v = vv;
       a.dout = {do_h, do_rows, do_heads, do_head0};
@@ -1239,6 +1281,10 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
     std::vector<char> dq_started((size_t)u, 0);  // chunk i's dq partial already holds contributions (host store)
     for (int64_t j = 0; j < u; ++j) {
       const int ks = (int)(j & 1);
+      if (p > 1) {
+        bsend = bsend2[j & 1];
+        wait(cs, ctx->ev_bsend_free[j & 1]);  // chunk j-2's final gradients have left this buffer
+      }
       int64_t last_i = j;  // the last query chunk that attends key chunk j
       for (int64_t i = j; i < u; ++i)
         if (keep(i, j)) last_i = i;
@@ -1280,6 +1326,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
             doi = {dores + (size_t)R.qslot[(size_t)i] * C * 2 * hq * d * eb, C, 2 * hq, hq};
           }
           dqi = dqres + (size_t)R.qslot[(size_t)i] * C * hq * d;
+          if (p > 1) wait(cs, ctx->ev_a2a[i]);  // its (O, dO) exchange and D_i (a no-op after the first pair)
           if (!dq_started[i]) FPDT_CHECK_CUDA(cudaMemsetAsync(dqi, 0, (size_t)C * hq * d * 4, cs));
         } else {
           // B4: fetch q_i, dO_i and (when it already holds contributions) the dq partial of chunk i
@@ -1328,6 +1375,8 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   wait(cs, ctx->ev_d2h_done);
   rec(ctx->ev_h2d_done, ctx->s_h2d);
   wait(cs, ctx->ev_h2d_done);
+  rec(ctx->ev_comm_done, ctx->s_comm);  // the last chunk's gradients are in the caller's tensors
+  wait(cs, ctx->ev_comm_done);
 }
 
 }  // namespace
@@ -1398,7 +1447,7 @@ fpdt_ctx* create_ctx(int world_size, int rank, const unsigned char* nccl_id, fpd
     for (int b = 0; b < 2; ++b) {
       cudaEvent_t* pe[] = {&ctx->ev_slot_free[b], &ctx->ev_slot_filled[b], &ctx->ev_q_free[b], &ctx->ev_q_filled[b],
                            &ctx->ev_dq_ready[b], &ctx->ev_kv_free[b], &ctx->ev_kv_filled[b], &ctx->ev_recv_used_c[b],
-                           &ctx->ev_recv_used_d[b]};
+                           &ctx->ev_recv_used_d[b], &ctx->ev_ohat_free[b], &ctx->ev_bsend_free[b]};
       for (auto e : pe) FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
     if (world_size > 1 && !group) {
@@ -1674,6 +1723,34 @@ int fpdt_kernel_time(fpdt_ctx* ctx, double* fwd_ms, int64_t* fwd_launches, doubl
     if (fwd_launches) *fwd_launches = (int64_t)ctx->n_fwd;
     if (bwd_launches) *bwd_launches = (int64_t)ctx->n_bwd;
     if (reset) ctx->n_fwd = ctx->n_bwd = 0;
+  });
+}
+
+int fpdt_kernel_gaps(fpdt_ctx* ctx, double* gap_ms, int64_t* n_gaps) {
+  return run([&] {
+    if (!ctx || !gap_ms || !n_gaps) fail(FPDT_ERR_ARG, "null argument");
+    double g = 0;
+    int64_t n = 0;
+    for (int fwd = 0; fwd < 2; ++fwd) {
+      const auto& v = fwd ? ctx->t_fwd : ctx->t_bwd;
+      const auto& src = fwd ? ctx->t_fwd_src : ctx->t_bwd_src;
+      const size_t cnt = fwd ? ctx->n_fwd : ctx->n_bwd;
+      for (size_t i = 0; i < cnt; ++i) {
+        // the previous launch of the same call on the same stream
+        for (size_t j = i; j-- > 0;) {
+          if (src[j].second != src[i].second) break;
+          if (src[j].first != src[i].first) continue;
+          float ms = 0;
+          FPDT_CHECK_CUDA(cudaEventSynchronize(v[i].first));
+          FPDT_CHECK_CUDA(cudaEventElapsedTime(&ms, v[j].second, v[i].first));
+          g += std::max(0.f, ms);
+          ++n;
+          break;
+        }
+      }
+    }
+    *gap_ms = g;
+    *n_gaps = n;
   });
 }
 

@@ -23,7 +23,8 @@ STATUS_NAMES = {0: "FPDT_OK", 1: "FPDT_ERR_ARG", 2: "FPDT_ERR_DIVISIBILITY", 3: 
 EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_attn_fwd", "fpdt_attn_bwd",
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_group_create", "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity",
-            "fpdt_set_residency", "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes")
+            "fpdt_set_residency", "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes",
+            "fpdt_kernel_gaps")
 # include/fpdt_diag.h (libfpdt_diag.so: micro-benchmarks and direct kernel launches, not on the FPDT path)
 DIAG_EXPORTED = ("fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_selftest_softmax", "fpdt_selftest_reduce",
                  "fpdt_selftest_pair", "fpdt_debug_relayout", "fpdt_debug_pair")
@@ -91,6 +92,8 @@ def _declare(lib):
     lib.fpdt_kernel_time.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int64),
                                      ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int64), c_int]
     lib.fpdt_kernel_time.restype = c_int
+    lib.fpdt_kernel_gaps.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int64)]
+    lib.fpdt_kernel_gaps.restype = c_int
 
 
 def _declare_diag(lib):
@@ -224,6 +227,13 @@ class FPDTContext:
         _check(lib().fpdt_kernel_time(self.handle, ctypes.byref(f), ctypes.byref(nf), ctypes.byref(b),
                                       ctypes.byref(nb), int(reset)))
         return f.value, nf.value, b.value, nb.value
+
+    def kernel_gaps(self):
+        """(gap_ms, n_gaps): compute-stream time between consecutive attention launches of one call since the last
+        kernel_time reset (include/fpdt.h fpdt_kernel_gaps)."""
+        g, n = ctypes.c_double(), c_int64()
+        _check(lib().fpdt_kernel_gaps(self.handle, ctypes.byref(g), ctypes.byref(n)))
+        return g.value, n.value
 
 
 def fpdt_attn_fwd(ctx: FPDTContext, q, k, v, o, lse, s_local: int, n_q_heads: int, n_kv_heads: int, head_dim: int,
