@@ -234,6 +234,14 @@ int fpdt_kernel_time(fpdt_ctx* ctx, double* fwd_ms, int64_t* fwd_launches, doubl
  * Returns FPDT_OK, FPDT_ERR_ARG or FPDT_ERR_CUDA. */
 int fpdt_kernel_gaps(fpdt_ctx* ctx, double* gap_ms, int64_t* n_gaps);
 
+/* All-to-all timing (p > 1, with fpdt_set_kernel_timing on): CUDA events around every exchange on the comm stream
+ * since the last reset of fpdt_kernel_time.  *total_ms = summed exchange time, *n = exchanges, *bytes = bytes sent to
+ * other ranks by them (for bus GB/s = bytes / time), *first_ms / *last_ms (nullable) = the first and the last exchange
+ * (the pipeline fill and drain).  Synchronises on the events; call before fpdt_kernel_time(reset=1).
+ * Returns FPDT_OK, FPDT_ERR_ARG or FPDT_ERR_CUDA. */
+int fpdt_exchange_time(fpdt_ctx* ctx, double* total_ms, int64_t* n, int64_t* bytes, double* first_ms,
+                       double* last_ms);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,4 +1,5 @@
-// Backward chunk-pair attention for sm_100a, head_dim 64 / 80: software-pipelined across query tiles.
+// Backward chunk-pair attention for sm_100a, head_dim 64 / 80: software-pipelined across query tiles; the dQ product in
+// fp16 (see PipeCfg).
 //
 // Same operation as attn_bwd_sm100.cu (one (key/value chunk j, query chunk i) step of FPDT's nested backward
 // loop, fig:bw_db; KV-stationary CTA = one 128-row key/value tile of one KV head walking the
@@ -23,7 +24,7 @@
 //   WG1 (4-7)   softmax-gradient, query columns [64,128)                                ; final dV    168 regs
 //   WG2 (8-11)  dQ read-out (thread = query row) -> smem staging -> TMA bulk reduce-add              104 regs
 //   WG3 (12)    TMA producer; (13) TMEM allocator + single-thread MMA issuer; (14, 15) idle          72 regs
-// Shared memory (d = 80: 215 KB): K, V | 3 Q stages (+ lse2/D rows) | 2 dO stages | dS | dQ staging.
+// Shared memory (d = 80: 215 KB): K, V | 2 Q stages (+ lse2/D rows) | 2 dO stages | fp16 K | dS (fp16) | dQ staging.
 // TMEM: S^T [0,128) | dP^T [128,256), then per query half h: P^T [128+64h, +32), dS^T [160+64h, +32) (bf16) |
 //       dQ [256,256+D) | dK | dV  (496 columns at d = 80).
 #include "attn_tile.cuh"
@@ -48,16 +49,22 @@ constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 128
 #endif
 constexpr int kRegsSoftmax = FPDT_BWD_REGS_SOFTMAX, kRegsDQ = FPDT_BWD_REGS_DQ, kRegsCtl = FPDT_BWD_REGS_CTL;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
+// The dQ product runs in fp16 (dS and a copy of K rounded to fp16, fp32 accumulation): its sum cancels
+// (sum_j dS_ij = 0), so a common offset of the keys multiplies the rounding error of dS -- a key drift of 32 in one
+// dimension (fpdt_inputs "drift") costs ~1.2e-2 normwise in dQ with bf16 dS, ~1.5e-3 with fp16 (measured: bf16
+// 0.012-0.026 on the GPU drift cases).  The fp16 copy of K takes the shared memory of a third Q stage (2 stages:
+// 858 vs 871 TFLOP/s for the bf16 product with 3 stages, C = 64K, 32 x 80 diagonal pair).
 template <int D>
 struct PipeCfg {
   using T = Tile<D>;
-  static constexpr int QS = 3, OS = 2;
+  static constexpr int QS = 2, OS = 2;
   static constexpr int TB = T::kBytes;
-  static constexpr int kDS = 128 * 128 * 2;  // dS (bf16)
+  static constexpr int kDS = 128 * 128 * 2;  // dS (fp16)
   static constexpr int kDQ = 128 * D * 4;
   static constexpr int kStats = 1024;  // lse2[128] + D[128] fp32
   static constexpr int oK = 0, oV = TB, oQ = 2 * TB, oO = oQ + QS * TB;
-  static constexpr int oDS = ((oO + OS * TB + 1023) / 1024) * 1024;
+  static constexpr int oKH = ((oO + OS * TB + 1023) / 1024) * 1024;  // fp16 copy of K (B of dQ)
+  static constexpr int oDS = oKH + ((TB + 1023) / 1024) * 1024;
   static constexpr int oDQ = oDS + kDS;
   static constexpr int oStats = oDQ + kDQ;
   static constexpr int oBars = oStats + QS * kStats;
@@ -95,6 +102,12 @@ __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ float4 lds4(const float* p) { return *reinterpret_cast<const float4*>(p); }
 
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
+
 template <int D>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdArgs a) {
@@ -110,7 +123,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
   constexpr int B_KV = 0, B_QF = 1, B_QE = B_QF + QS, B_OF = B_QE + QS, B_OE = B_OF + OS, B_S = B_OE + OS,
                 B_SFREE = B_S + 1, B_DP = B_SFREE + 1, B_P = B_DP + 1, B_DS = B_P + 1,
                 B_DSFREE = B_DS + 1, B_DQF = B_DSFREE + 1, B_DQE = B_DQF + 1, B_KVDONE = B_DQE + 1,
-                B_NUM = B_KVDONE + 1;
+                B_KH = B_KVDONE + 1, B_NUM = B_KH + 1;
   static_assert(B_NUM <= 30, "barrier area");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::oBars + 30 * 8);
 
@@ -153,6 +166,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
     mbar_init(bar(B_DQF), 1);
     mbar_init(bar(B_DQE), 128);
     mbar_init(bar(B_KVDONE), 1);
+    mbar_init(bar(B_KH), 4);
     fence_mbar_init();
   }
   tc_fence_before();
@@ -192,7 +206,9 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       if (elect_one() && n_iter > 0) {
         const uint32_t idS = idesc_bf16(128, 128, 0, 0);  // S^T, dP^T: A (K or V rows), B (Q or dO rows) K-major
         const uint32_t idG = idesc_bf16(128, D, 0, 1);    // dV, dK: A = P^T / dS^T K-major smem, B MN-major
-        const uint32_t idQ = idesc_bf16(128, D, 1, 1);    // dQ: A = dS MN-major smem, B = K MN-major
+        // dQ: A = dS MN-major smem, B = K MN-major, both fp16 (kind::f16 with fp16 inputs)
+        const uint32_t idQ = (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(D >> 3) << 17) | ((128u >> 4) << 24);
+        const uint32_t sKQ = base + C::oKH;  // the fp16 copy of K
         const uint32_t tS = tmem + C::tS, tdP = tmem + C::tdP, tdQ = tmem + C::tdQ, tdK = tmem + C::tdK,
                        tdV = tmem + C::tdV;
         auto sQ = [&](int n) { return base + C::oQ + (n % QS) * C::TB; };
@@ -250,9 +266,12 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
           if (n > 0) {
             mbar_wait(bar(B_DQE), (n - 1) & 1);
             tc_fence_after();
+          } else {
+            mbar_wait(bar(B_KH), 0);  // the fp16 copy of K is built
+            tc_fence_after();
           }
 #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) mma_ss(tdQ, desc_a_mn_sw128(sDS, kk), T::desc_mn(sK, kk), idQ, kk > 0);
+          for (int kk = 0; kk < 8; ++kk) mma_ss(tdQ, desc_a_mn_sw128(sDS, kk), T::desc_mn(sKQ, kk), idQ, kk > 0);
           mma_commit(bar(B_DQF));
           mma_commit(bar(B_DSFREE));
           TRACE(8, n);
@@ -337,20 +356,28 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       tc_fence_before();
       mbar_arrive(bar(B_P));
       if (warp == 0 && lane == 0) TRACE(1, n);
-      // dS = P o (dP - D) -> TMEM (dS^T, A of dK) and smem (MN-major dS tile, A of dQ)
+      // dS = P o (dP - D) -> TMEM (dS^T bf16, A of dK) and smem (MN-major dS tile fp16, A of dQ)
       uint32_t pk[32];
+      {
+        // dS in place of dP (fp32), bf16 to TMEM; the fp16 copy for the smem tile is packed below
 #pragma unroll
-      for (int i = 0; i < 64; i += 4) {
-        const float4 dd = lds4(st + 128 + i);
-        const float2 a0 = __fmul2_rn(make_float2(p[i], p[i + 1]),
-                                     __fadd2_rn(make_float2(dp[i], dp[i + 1]), make_float2(-dd.x, -dd.y)));
-        const float2 a1 = __fmul2_rn(make_float2(p[i + 2], p[i + 3]),
-                                     __fadd2_rn(make_float2(dp[i + 2], dp[i + 3]), make_float2(-dd.z, -dd.w)));
-        pk[i / 2] = pack_bf16x2(a0.x, a0.y);
-        pk[i / 2 + 1] = pack_bf16x2(a1.x, a1.y);
+        for (int i = 0; i < 64; i += 4) {
+          const float4 dd = lds4(st + 128 + i);
+          const float2 a0 = __fmul2_rn(make_float2(p[i], p[i + 1]),
+                                       __fadd2_rn(make_float2(dp[i], dp[i + 1]), make_float2(-dd.x, -dd.y)));
+          const float2 a1 = __fmul2_rn(make_float2(p[i + 2], p[i + 3]),
+                                       __fadd2_rn(make_float2(dp[i + 2], dp[i + 3]), make_float2(-dd.z, -dd.w)));
+          dp[i] = a0.x; dp[i + 1] = a0.y; dp[i + 2] = a1.x; dp[i + 3] = a1.y;
+        }
+#pragma unroll
+        for (int c = 0; c < 64; c += 32) {
+#pragma unroll
+          for (int i = 0; i < 32; i += 2) pk[i / 2] = pack_bf16x2(dp[c + i], dp[c + i + 1]);
+          tmem_st16(tdP + 32 + c / 2, pk);
+        }
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) pk[i / 2] = pack_f16x2(dp[i], dp[i + 1]);
       }
-      tmem_st16(tdP + 32, pk);
-      tmem_st16(tdP + 48, pk + 16);
       if (n > 0) mbar_wait(bar(B_DSFREE), (n - 1) & 1);
       if (warp == 0 && lane == 0) TRACE(10, n);
 #pragma unroll
@@ -413,6 +440,26 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
     setmaxnreg_dec<kRegsDQ>();
     // ------------------------------------------------------------------ dQ read-out (query rows)
     const int r = (warp - 8) * 32 + lane;
+    {
+      // fp16 copy of the K tile, same (swizzled) layout, elementwise
+      if (n_iter > 0) mbar_wait(bar(B_KV), 0);
+      const uint4* src = reinterpret_cast<const uint4*>(smem + C::oK);
+      uint4* dst = reinterpret_cast<uint4*>(smem + C::oKH);
+      for (int i = r; i < C::TB / 16; i += 128) {
+        const uint4 x = src[i];
+        const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+        uint32_t ws[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[q]));
+          ws[q] = pack_f16x2(f.x, f.y);
+        }
+        dst[i] = make_uint4(ws[0], ws[1], ws[2], ws[3]);
+      }
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(B_KH));
+    }
     uint32_t tdQ = tmem + C::tdQ + (((warp & 3) * 32) << 16);
     asm volatile("" : "+r"(tdQ));
     for (int n = 0; n < n_iter; ++n) {
@@ -497,7 +544,8 @@ int launch_attn_bwd_pipe_bf16(const BwdArgs& a, int head_dim, cudaStream_t s) {
   return -2;
 }
 
-// The bf16 backward pair kernel for each head_dim.
+// The bf16 backward pair kernel for each head_dim: this file's kernel at 64 / 80, the 64-row query-tile kernel at 128.
+// (A CTA-pair variant, tcgen05 cta_group::2, is in the diagnostics library: correct but slower.)
 int launch_attn_bwd_bf16(const BwdArgs& a, int head_dim, cudaStream_t s) {
   if (head_dim == 128) return launch_attn_bwd_q64_bf16(a, head_dim, s);
   return launch_attn_bwd_pipe_bf16(a, head_dim, s);

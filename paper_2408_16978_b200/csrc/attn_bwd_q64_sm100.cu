@@ -9,13 +9,18 @@
 //   dQ^T = K^T dS^T          (the partial dQ of the tile, TMA bulk reduce-added into the fp32 dq accumulator)
 //
 // Why 64-row query tiles. With 128-row tiles at d = 128, Sᵀ, dPᵀ, dK and dV fill all 512 TMEM columns, and K, V,
-// the Q/dO stages and dS fill shared memory. There is no room to stage the 64 KB dQ partial for a TMA reduce-add,
-// so attn_bwd_sm100.cu reduces it with vector atomics (≈ 630 TFLOP/s). With 64-row query tiles:
+// the Q/dO stages and dS fill shared memory: there is no room to stage the 64 KB dQ partial for a TMA reduce-add.
+// With 64-row query tiles:
 //   * every product keeps M = 128. dQ is computed transposed (M = 128 over head_dim, N = 64 query rows), with
-//     A = Kᵀ read MN-major from the resident K tile and B = dS read MN-major from the tile the softmax warps
-//     write. For d < 128 the M = 128 read runs past the K tile into V; those rows of dQᵀ are never read out;
+//     A = Kᵀ read MN-major from an fp16 copy of the resident K tile and B = dS (fp16) read MN-major from the tile the
+//     softmax warps write. For d < 128 the M = 128 read runs past the copied tile into zeroed rows of dQᵀ that are
+//     never read out;
+//   * numerics: the dQ product is fp16 x fp16 (fp32 accumulation), everything else bf16.  dQ_i = sigma sum_j dS_ij k_j
+//     cancels (sum_j dS_ij = 0), so a common offset of the keys multiplies the rounding error of dS: a key drift of 32
+//     in one dimension (fpdt_inputs "drift") costs ~1e-2 relative error with bf16 dS, ~1.5e-3 with fp16;
 //   * TMEM: Sᵀ 64 | dPᵀ 64 | Pᵀ, dSᵀ (bf16) 64 | dQᵀ 64 | dK d | dV d (512 columns at d = 128);
-//   * shared memory (d = 128): K, V 64 KB | 3 Q + 2 dO stages 80 KB | dS 16 KB | dQ staging 2 × 32 KB | stats.
+//   * shared memory (d = 128): K, V 64 KB | 3 Q + 2 dO stages 80 KB | dS 16 KB | fp16 K 32 KB | dQ staging 32 KB
+//     (one buffer per 64-column group: a group's next staging waits until its previous reduce-add has read it).
 // The dQ read-out thread owns one head_dim column (a TMEM lane) and 64 query rows. It stages column groups of
 // [64 rows][64 cols] fp32 (and a 16-column group at d = 80) without swizzle: a warp writes 128 contiguous bytes
 // per row. Each group leaves as one TMA reduce-add box.
@@ -79,12 +84,14 @@ struct Cfg {
   static constexpr int QS = 3, OS = 2;
   static constexpr int kDQW = (D + 31) / 32;       // dQ read-out warps (thread = one head_dim column)
   static constexpr int kDS = 128 * BQ * 2;         // dS, [128 keys][64 queries] bf16, MN-major (queries contiguous)
-  static constexpr int kDQB = BQ * D * 4;          // one dQ staging buffer: column groups [64 rows][<=64 cols] fp32
+  static constexpr int kDQB = BQ * D * 4;          // dQ staging: column groups [64 rows][<=64 cols] fp32
   static constexpr int kStats = 2 * BQ * 4;        // lse2[64] + D[64]
+  static constexpr int kKH = 128 * 128 * 2;        // fp16 copy of K read as the M = 128 A operand of dQ^T
   static constexpr int oK = 0, oV = TK::kBytes, oQ = 2 * TK::kBytes, oO = oQ + QS * TQ::kBytes;
   static constexpr int oDS = oO + OS * TQ::kBytes;
-  static constexpr int oDQ = oDS + kDS;
-  static constexpr int oStats = oDQ + 2 * kDQB;
+  static constexpr int oKH = oDS + kDS;
+  static constexpr int oDQ = oKH + kKH;
+  static constexpr int oStats = oDQ + kDQB;
   static constexpr int oBars = oStats + QS * kStats;
   static constexpr int kSmem = oBars + 256;
   static_assert(oDS % 1024 == 0, "swizzle atoms are 1 KB aligned");
@@ -92,6 +99,7 @@ struct Cfg {
   // dQ^T = K^T dS^T runs with M = 128 over the K tile read MN-major: for D < 128 its rows >= D read the bytes that
   // follow the K tile in shared memory (V) and are never read out
   static_assert(oK + 128 * 128 * 2 <= oDS, "M = 128 read of K^T stays inside the K/V/Q area");
+  static_assert(oKH % 1024 == 0, "fp16 K copy keeps the K tile's swizzle phase");
   // P^T / dS^T (bf16) get their own columns so that dP^T_{n+1} can be issued as soon as dP^T_n is in registers
   static constexpr uint32_t tS = 0, tdP = 64, tPS = 128, tdQ = 192, tdK = 256, tdV = 256 + D;
   static_assert(256 + 2 * D <= 512, "TMEM budget");
@@ -118,9 +126,14 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                : "memory");
 }
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
-__device__ __forceinline__ void bulk_wait_read1() { asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
 __device__ __forceinline__ void named_bar(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
+  uint32_t r;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(r) : "f"(hi), "f"(lo));
+  return r;
+}
 __device__ __forceinline__ void sts32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
@@ -140,7 +153,7 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
   constexpr int B_KV = 0, B_QF = 1, B_QE = B_QF + QS, B_OF = B_QE + QS, B_OE = B_OF + OS, B_S = B_OE + OS,
                 B_SFREE = B_S + 1, B_DP = B_SFREE + 1, B_DPFREE = B_DP + 1, B_P = B_DPFREE + 1,
                 B_PFREE = B_P + 1, B_DS = B_PFREE + 1, B_DSFREE = B_DS + 1, B_DQF = B_DSFREE + 1,
-                B_DQE = B_DQF + 1, B_KVDONE = B_DQE + 1, B_NUM = B_KVDONE + 1;
+                B_DQE = B_DQF + 1, B_KVDONE = B_DQE + 1, B_KH = B_KVDONE + 1, B_NUM = B_KH + 1;
   static_assert(B_NUM <= 30, "barrier area");
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(smem + C::oBars + 30 * 8);
 
@@ -185,12 +198,14 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
     mbar_init(bar(B_DQF), 1);
     mbar_init(bar(B_DQE), 32 * C::kDQW);
     mbar_init(bar(B_KVDONE), 1);
+    mbar_init(bar(B_KH), 4);
     fence_mbar_init();
   }
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  const uint32_t sKH = base + C::oKH;
 
   if (warp >= 12) {
     setmaxnreg_dec<kRegsCtl>();
@@ -224,7 +239,8 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
       if (elect_one() && n_iter > 0) {
         const uint32_t idS = idesc_bf16(128, BQ, 0, 0);  // S^T, dP^T: A = K / V rows, B = Q / dO rows, K-major
         const uint32_t idG = idesc_bf16(128, D, 0, 1);   // dV, dK: A = P^T / dS^T in TMEM, B = dO / Q MN-major
-        const uint32_t idQ = idesc_bf16(128, BQ, 1, 1);  // dQ^T: A = K^T (K tile MN-major), B = dS MN-major
+        // dQ^T: A = K^T (the fp16 copy of the K tile, MN-major), B = dS (fp16, MN-major); kind::f16 with fp16 inputs
+        const uint32_t idQ = (1u << 4) | (1u << 15) | (1u << 16) | ((uint32_t)(BQ >> 3) << 17) | ((128u >> 4) << 24);
         const uint32_t tS = tmem + C::tS, tdP = tmem + C::tdP, tdK = tmem + C::tdK, tdV = tmem + C::tdV;
         auto sQ = [&](int n) { return base + C::oQ + (n % QS) * TQ::kBytes; };
         auto sO = [&](int n) { return base + C::oO + (n % OS) * TQ::kBytes; };
@@ -276,14 +292,15 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
           for (int kk = 0; kk < BQ / 16; ++kk)
             mma_ts(tdK, tPS + 32 + 8 * kk, TQ::mn(sQ(n), kk), idG, (n > 0 || kk > 0));
           mma_commit(bar(B_QE + n % QS));
-          if (n > 0) {
+          if (n > 0)
             mbar_wait(bar(B_DQE), (n - 1) & 1);
-            tc_fence_after();
-          }
+          else
+            mbar_wait(bar(B_KH), 0);  // the fp16 copy of K is built
+          tc_fence_after();
           TRACE(7, n);
 #pragma unroll
           for (int kk = 0; kk < 128 / 16; ++kk)
-            mma_ss(tdQ, TK::mn(sK, kk), smem_desc(sDS + kk * 2048, 8192, 1024, kSw128), idQ, kk > 0);
+            mma_ss(tdQ, TK::mn(sKH, kk), smem_desc(sDS + kk * 2048, 8192, 1024, kSw128), idQ, kk > 0);
           mma_commit(bar(B_DQF));
           mma_commit(bar(B_DSFREE));
         }
@@ -369,7 +386,9 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
       tc_fence_before();
       mbar_arrive(bar(B_P));
       if (warp == 0 && lane == 0) TRACE(1, n);
-      uint32_t pk[16];
+      // dS^T in bf16 (TMEM, A of dK += dS^T Q) and dS in fp16 (smem, B of dQ^T = K^T dS^T): the dQ sum cancels
+      // (sum_j dS_ij = 0), so a common key offset amplifies the rounding of dS there; fp16 has 3 more mantissa bits
+      uint32_t pk[16], ph[16];
 #pragma unroll
       for (int i = 0; i < 32; i += 4) {
         const float4 dd = *reinterpret_cast<const float4*>(st + BQ + i);
@@ -379,6 +398,8 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
                                      __fadd2_rn(make_float2(dp[i + 2], dp[i + 3]), make_float2(-dd.z, -dd.w)));
         pk[i / 2] = pack_bf16x2(a0.x, a0.y);
         pk[i / 2 + 1] = pack_bf16x2(a1.x, a1.y);
+        ph[i / 2] = pack_f16x2(a0.x, a0.y);
+        ph[i / 2 + 1] = pack_f16x2(a1.x, a1.y);
       }
       if (n > 0) {
         mbar_wait(bar(B_DSFREE), (n - 1) & 1);  // dK_{n-1} and dQ^T_{n-1} have read dS^T_{n-1} / dS_{n-1}
@@ -388,7 +409,7 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
       tmem_st16(tPw + 32, pk);
 #pragma unroll
       for (int m = 0; m < 4; ++m) {
-        const uint32_t w[4] = {pk[m * 4], pk[m * 4 + 1], pk[m * 4 + 2], pk[m * 4 + 3]};
+        const uint32_t w[4] = {ph[m * 4], ph[m * 4 + 1], ph[m * 4 + 2], ph[m * 4 + 3]};
         st_shared_v4(sDSr + ((((uint32_t)(4 * half + m)) ^ xr) << 4), w);
       }
       tmem_wait_st();
@@ -448,6 +469,31 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
     // Column group cg = columns [64 cg, 64 cg + 64) (D = 80: the second group is 16 wide) has its own staging, named
     // barrier and issuing thread, so one group stages while the TMA engine reads the other's.
     const int e = (warp & 3) * 32 + lane;  // TMEM lane of dQ^T = head_dim index
+    {
+      // fp16 copy of the K tile in the same (swizzled) layout, elementwise; the M = 128 read of K^T at D < 128 runs
+      // past the tile into rows that are never read out, zeroed here
+      if (n_iter > 0) mbar_wait(bar(B_KV), 0);
+      const uint4* src = reinterpret_cast<const uint4*>(smem + C::oK);
+      uint4* dst = reinterpret_cast<uint4*>(smem + C::oKH);
+      for (int i = e; i < C::kKH / 16; i += 128) {
+        uint4 w = make_uint4(0u, 0u, 0u, 0u);
+        if (i < TK::kBytes / 16) {
+          const uint4 x = src[i];
+          const uint32_t xs[4] = {x.x, x.y, x.z, x.w};
+          uint32_t ws[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const float2 f = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&xs[q]));
+            ws[q] = pack_f16x2(f.x, f.y);
+          }
+          w = make_uint4(ws[0], ws[1], ws[2], ws[3]);
+        }
+        dst[i] = w;
+      }
+      fence_async_shared();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(bar(B_KH));
+    }
     if ((int)(warp & 3) < C::kDQW) {
       const int cg = e >> 6, el = e & 63;
       const int gw = (D - 64 * cg) < 64 ? (D - 64 * cg) : 64;  // width of this column group
@@ -458,7 +504,6 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
       const float sc = a.scale;
       for (int n = 0; n < n_iter; ++n) {
         const int qt = qt_first + n / G, h = g * G + n % G;
-        const int buf = n & 1;
         mbar_wait(bar(B_DQF), n & 1);
         if (e == 0) TRACE(9, n);
         tc_fence_after();
@@ -468,9 +513,9 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
         tmem_wait_ld();
         tc_fence_before();
         mbar_arrive(bar(B_DQE));
-        if (lead) bulk_wait_read1();  // the reduce-add of tile n-2 (same staging buffer) has read its source
+        if (lead) bulk_wait_read0();  // the previous tile's reduce-add of this column group has read its staging
         named_bar(2 + cg, gthreads);
-        const uint32_t gbase = sDQ + (uint32_t)buf * C::kDQB + (uint32_t)(cg * 64 * BQ * 4);
+        const uint32_t gbase = sDQ + (uint32_t)(cg * 64 * BQ * 4);
         if (valid) {
           const uint32_t stg = gbase + (uint32_t)el * 4;
 #pragma unroll

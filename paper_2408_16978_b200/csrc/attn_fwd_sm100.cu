@@ -386,15 +386,17 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         for (int i = 0; i < 128; ++i)
           if (i > lim) x[i] = -INFINITY;
       }
-      // row max: 8 independent three-input max chains
+      // row max: 8 independent three-input max chains over columns 8..119, then the last 8 columns
       float m8[8];
 #pragma unroll
       for (int k = 0; k < 8; ++k) m8[k] = x[k];
 #pragma unroll
-      for (int i = 8; i < 128; i += 16) {
+      for (int i = 8; i + 16 <= 128; i += 16) {
 #pragma unroll
         for (int k = 0; k < 8; ++k) m8[k] = max3(m8[k], x[i + k], x[i + 8 + k]);
       }
+#pragma unroll
+      for (int k = 0; k < 8; ++k) m8[k] = fmaxf(m8[k], x[120 + k]);
       float mx = max3(max3(m8[0], m8[1], m8[2]), max3(m8[3], m8[4], m8[5]), fmaxf(m8[6], m8[7]));
       mx *= sl2;
       if ((warp & 3) == 0 && lane == 0) TRACE(9 + 4 * t, j);

@@ -7,6 +7,11 @@
 #include "fpdt_diag.h"
 #include "kernels.h"
 
+namespace fpdt {
+// CTA-pair backward (diag/attn_bwd_2cta_sm100.cu, this library only)
+int launch_attn_bwd_2cta_bf16(const BwdArgs& a, int head_dim, cudaStream_t s);
+}  // namespace fpdt
+
 using namespace fpdt;
 
 extern "C" int fpdt_debug_pair(int which, int head_dim, int causal, const void* q, const void* k, const void* v,
@@ -61,7 +66,13 @@ extern "C" int fpdt_debug_pair(int which, int head_dim, int causal, const void* 
   a.kv_out_ld = (int64_t)n_kv_heads * head_dim;
   a.trace = trace;
   a.trace_cta = trace_cta;
-  return launch_attn_bwd_bf16(a, head_dim, s) == 0 ? FPDT_OK : FPDT_ERR_CUDA;
+  // which 1: the kernel the library dispatches; 2: the single-CTA pipelined kernel (d = 64 / 80); 3: the CTA-pair
+  // kernel (d = 64 / 80); 4: the 64-row query-tile kernel
+  const int rc = which == 2   ? launch_attn_bwd_pipe_bf16(a, head_dim, s)
+                 : which == 3 ? launch_attn_bwd_2cta_bf16(a, head_dim, s)
+                 : which == 4 ? launch_attn_bwd_q64_bf16(a, head_dim, s)
+                              : launch_attn_bwd_bf16(a, head_dim, s);
+  return rc == 0 ? FPDT_OK : FPDT_ERR_CUDA;
 }
 
 // Diagnostic: one all-to-all layout kernel (F3/F10/B2/B7) on caller device buffers (include/fpdt_diag.h).

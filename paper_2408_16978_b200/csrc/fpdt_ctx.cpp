@@ -186,6 +186,9 @@ struct fpdt_ctx {
   std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_fwd, t_bwd;
   std::vector<std::pair<cudaStream_t, int64_t>> t_fwd_src, t_bwd_src;  // launch stream and call number per launch
   size_t n_fwd = 0, n_bwd = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> t_a2a;  // all-to-all timing (p > 1), with the kernel timing
+  std::vector<int64_t> t_a2a_bytes;
+  size_t n_a2a = 0;
   int64_t call_seq = 0;  // fpdt_attn_* / fpdt_block_* calls so far (kernel-gap accounting)
   // every event created once in create_ctx (destroyed by fpdt_ctx_destroy; null handles are skipped)
   std::vector<cudaEvent_t> fixed_events() const {
@@ -396,6 +399,19 @@ void d2h_2d(fpdt_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spi
 void alltoall(fpdt_ctx* ctx, const void* send, void* recv, size_t count_per_peer, int dtype) {
   const size_t eb = dtype == FPDT_BF16 ? 2 : 4;
   stress(ctx, ctx->s_comm);
+  std::pair<cudaEvent_t, cudaEvent_t>* tev = nullptr;
+  if (ctx->timing) {
+    if (ctx->t_a2a.size() <= ctx->n_a2a) {
+      cudaEvent_t e0, e1;
+      FPDT_CHECK_CUDA(cudaEventCreate(&e0));
+      FPDT_CHECK_CUDA(cudaEventCreate(&e1));
+      ctx->t_a2a.push_back({e0, e1});
+      ctx->t_a2a_bytes.push_back(0);
+    }
+    ctx->t_a2a_bytes[ctx->n_a2a] = (int64_t)(count_per_peer * (ctx->p - 1) * eb);
+    tev = &ctx->t_a2a[ctx->n_a2a++];
+    rec(tev->first, ctx->s_comm);
+  }
   if (!ctx->group) {
     FPDT_CHECK_NCCL(ncclAlltoAll(send, recv, count_per_peer, dtype == FPDT_BF16 ? ncclBfloat16 : ncclFloat32,
                                  ctx->comm, ctx->s_comm));
@@ -419,6 +435,7 @@ void alltoall(fpdt_ctx* ctx, const void* send, void* recv, size_t count_per_peer
     for (int q = 0; q < p; ++q) FPDT_CHECK_CUDA(cudaStreamWaitEvent(ctx->s_comm, g->ev_read[q], 0));
     g->barrier();  // nobody re-records ev_sent / ev_read before every rank has enqueued its waits
   }
+  if (tev) rec(tev->second, ctx->s_comm);
   ctx->stats.bytes_a2a += (int64_t)(count_per_peer * (ctx->p - 1) * eb);
 }
 
@@ -1526,6 +1543,7 @@ int fpdt_ctx_destroy(fpdt_ctx* ctx) {
       if (e) cudaEventDestroy(e);
     for (auto& pr : ctx->t_fwd) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
     for (auto& pr : ctx->t_bwd) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
+    for (auto& pr : ctx->t_a2a) cudaEventDestroy(pr.first), cudaEventDestroy(pr.second);
     cudaStreamDestroy(ctx->s_comm);
     cudaStreamDestroy(ctx->s_h2d);
     cudaStreamDestroy(ctx->s_d2h);
@@ -1722,7 +1740,29 @@ int fpdt_kernel_time(fpdt_ctx* ctx, double* fwd_ms, int64_t* fwd_launches, doubl
     if (bwd_ms) *bwd_ms = b;
     if (fwd_launches) *fwd_launches = (int64_t)ctx->n_fwd;
     if (bwd_launches) *bwd_launches = (int64_t)ctx->n_bwd;
-    if (reset) ctx->n_fwd = ctx->n_bwd = 0;
+    if (reset) ctx->n_fwd = ctx->n_bwd = ctx->n_a2a = 0;
+  });
+}
+
+int fpdt_exchange_time(fpdt_ctx* ctx, double* total_ms, int64_t* n, int64_t* bytes, double* first_ms, double* last_ms) {
+  return run([&] {
+    if (!ctx || !total_ms || !n || !bytes) fail(FPDT_ERR_ARG, "null argument");
+    double t = 0, f = 0, l = 0;
+    int64_t b = 0;
+    for (size_t i = 0; i < ctx->n_a2a; ++i) {
+      float ms = 0;
+      FPDT_CHECK_CUDA(cudaEventSynchronize(ctx->t_a2a[i].second));
+      FPDT_CHECK_CUDA(cudaEventElapsedTime(&ms, ctx->t_a2a[i].first, ctx->t_a2a[i].second));
+      t += ms;
+      b += ctx->t_a2a_bytes[i];
+      if (i == 0) f = ms;
+      l = ms;
+    }
+    *total_ms = t;
+    *n = (int64_t)ctx->n_a2a;
+    *bytes = b;
+    if (first_ms) *first_ms = f;
+    if (last_ms) *last_ms = l;
   });
 }
 

@@ -24,7 +24,7 @@ EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_a
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_group_create", "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity",
             "fpdt_set_residency", "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes",
-            "fpdt_kernel_gaps")
+            "fpdt_kernel_gaps", "fpdt_exchange_time")
 # include/fpdt_diag.h (libfpdt_diag.so: micro-benchmarks and direct kernel launches, not on the FPDT path)
 DIAG_EXPORTED = ("fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_selftest_softmax", "fpdt_selftest_reduce",
                  "fpdt_selftest_pair", "fpdt_debug_relayout", "fpdt_debug_pair")
@@ -94,6 +94,9 @@ def _declare(lib):
     lib.fpdt_kernel_time.restype = c_int
     lib.fpdt_kernel_gaps.argtypes = [P, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(c_int64)]
     lib.fpdt_kernel_gaps.restype = c_int
+    D_ = ctypes.POINTER(ctypes.c_double)
+    lib.fpdt_exchange_time.argtypes = [P, D_, ctypes.POINTER(c_int64), ctypes.POINTER(c_int64), D_, D_]
+    lib.fpdt_exchange_time.restype = c_int
 
 
 def _declare_diag(lib):
@@ -227,6 +230,14 @@ class FPDTContext:
         _check(lib().fpdt_kernel_time(self.handle, ctypes.byref(f), ctypes.byref(nf), ctypes.byref(b),
                                       ctypes.byref(nb), int(reset)))
         return f.value, nf.value, b.value, nb.value
+
+    def exchange_time(self):
+        """dict(total_ms, n, bytes, first_ms, last_ms) of the all-to-alls since the last kernel_time reset."""
+        t, f, l = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        n, b = c_int64(), c_int64()
+        _check(lib().fpdt_exchange_time(self.handle, ctypes.byref(t), ctypes.byref(n), ctypes.byref(b), ctypes.byref(f),
+                                        ctypes.byref(l)))
+        return {"total_ms": t.value, "n": n.value, "bytes": b.value, "first_ms": f.value, "last_ms": l.value}
 
     def kernel_gaps(self):
         """(gap_ms, n_gaps): compute-stream time between consecutive attention launches of one call since the last

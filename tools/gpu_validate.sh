@@ -6,3 +6,4 @@ timeout 2400 python -m pytest ${1:-tests} -q -m gpu --durations=10 > gpurun_out/
 timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"; tail -1 gpurun_out/smoke.log
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench.log | cut -c1-400
 timeout 600 python tools/block_bench.py > gpurun_out/block_bench.log 2>&1; echo "block rc=$?"; tail -3 gpurun_out/block_bench.log
+timeout 900 python tools/overlap_probe.py > gpurun_out/overlap.jsonl 2> gpurun_out/overlap.err; echo "overlap rc=$?"; cut -c1-200 gpurun_out/overlap.jsonl; tail -3 gpurun_out/overlap.err

@@ -1,5 +1,6 @@
 """Time one chunk-pair kernel in isolation and print the warp-role timeline of one CTA
-(fpdt_debug_pair).  Usage: python tools/trace_pair.py [fwd|bwd] [C] [heads] [d] [cta]"""
+(fpdt_debug_pair).  Usage: python tools/trace_pair.py [fwd|bwd] [C] [heads] [d] [cta] [bwd kernel: 1 dispatch, 2 pipe,
+3 CTA pair, 4 q64]"""
 import ctypes
 import os
 import sys
@@ -15,6 +16,7 @@ C = int(sys.argv[2]) if len(sys.argv) > 2 else 65536
 H = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 d = int(sys.argv[4]) if len(sys.argv) > 4 else 80
 cta = int(sys.argv[5]) if len(sys.argv) > 5 else 0
+kern = int(sys.argv[6]) if len(sys.argv) > 6 else 1
 lib = _lib.load_diag()
 torch.manual_seed(0)
 bf = torch.bfloat16
@@ -33,7 +35,7 @@ def launch(tr):
     if which == "fwd":
         rc = lib.fpdt_debug_pair(0, d, 1, P(q), P(k), P(v), None, None, None, P(o), P(lse), None, C, H, H, tr, cta, None)
     else:
-        rc = lib.fpdt_debug_pair(1, d, 1, P(q), P(k), P(v), P(do), P(lse2), P(Dst), P(dq), P(dk), P(dv), C, H, H, tr,
+        rc = lib.fpdt_debug_pair(kern, d, 1, P(q), P(k), P(v), P(do), P(lse2), P(Dst), P(dq), P(dk), P(dv), C, H, H, tr,
                                  cta, None)
     assert rc == 0, rc
 
@@ -49,13 +51,15 @@ e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 3
 fl = (4 if which == "fwd" else 10) * d * H * C * (C + 1) / 2
-print(f"{which} pair C={C} H={H} d={d}: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s")
+print(f"{which} pair C={C} H={H} d={d} kernel={kern}: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s")
+if len(sys.argv) > 7 and sys.argv[7] == "x":
+    sys.exit(0)
 launch(ctypes.c_void_p(trace.data_ptr()))
 torch.cuda.synchronize()
 t = trace.cpu().numpy()
 names = {"bwd": ["sm:got_S", "sm:arr_P", "sm:got_dP", "sm:arr_dS", "mma:got_P", "mma:got_dS", "mma:iss_S+1",
-                 "mma:got_dqempty", "mma:iss_dP+1", "dq:got_full", "sm:got_dsfree", "dq:reduce", "prod:got_qempty",
-                 "sm:S_loaded", "sm:exp_done", "sm:dP_loaded"],
+                 "mma:got_dqempty", "mma:iss_dP+1", "dq:got_full", "sm:got_dsfree", "dq:reduce", "prod:got_qempty|sm:got_dsrx",
+                 "sm:S_loaded", "sm:exp_done", "sm:dP_loaded|sm:stored"],
          "fwd": ["sm0:got_S", "sm0:arr_P", "sm1:got_S", "sm1:arr_P", "mma:got_P0", "mma:got_P1", "mma:got_K+1",
                  "prod:got_kvempty", "sm0:S_loaded", "sm0:max_done", "sm0:exp_done", "sm0:st_done",
                  "sm1:S_loaded", "sm1:max_done", "sm1:exp_done", "sm1:st_done"]}[which]
