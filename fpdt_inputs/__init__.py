@@ -23,8 +23,11 @@ IEEE fp32 ops so the device twin matches bitwise):
 
     normal : x
     peaky  : q*4                                                    (sharp attention)
-    drift  : q[...,0] += 2 ;  k[t,...,0] += t*(32/S)                (running max rises every chunk: at d = 128
-             the ramp moves the logits of the last keys by ~2*32/sqrt(128) = 5.7 nats over the sequence)
+    drift  : q[...,0] += 2 ;  k[t,...,0] += t*(8/S)                 (running max rises every chunk: the ramp moves
+             the logits of the last keys by ~2*8/sqrt(d) = 1.4 nats (d = 128) over the sequence)
+    drift32: the same with k[t,...,0] += t*(32/S)                   (~5.7 nats; adversarial for dQ: the key offset
+             -- up to 32 in one dimension, ~3x the norm of the rest of a key -- multiplies the rounding error of any
+             bf16 attention's dQ, R28)
     sink   : q += 0.5 ;  k[0] = 2 (all dims)                         (attention sink on token 0)
     same   : k[t] = base(K, token 0)                                (identical keys: closed form)
     class  : k[t] = base(K, token c(t)), c(t) = mix32(t^0xC1A55) % 3 for t < S/2, % 4 for t >= S/2;
@@ -39,7 +42,7 @@ import numpy as np
 
 Q, K, V, DO, X, W, WO, DY = 0, 1, 2, 3, 4, 5, 6, 7
 TENSOR_IDS = {"q": Q, "k": K, "v": V, "do": DO, "x": X, "w": W, "wo": WO, "dy": DY}
-DISTRIBUTIONS = ("normal", "peaky", "drift", "sink", "same", "class", "extreme")
+DISTRIBUTIONS = ("normal", "peaky", "drift", "sink", "same", "class", "extreme", "drift32")
 DIST_IDS = {name: i for i, name in enumerate(DISTRIBUTIONS)}
 N_CLASSES = 4
 
@@ -114,11 +117,11 @@ def generate(name: str, dist: str, seed: int, tokens: np.ndarray, n_heads: int, 
         x = x * np.float32(4.0)
     elif dist == "extreme" and name == "q":
         x = x * np.float32(30.0)
-    elif dist == "drift":
+    elif dist in ("drift", "drift32"):
         if name == "q":
             x[..., 0] = x[..., 0] + np.float32(2.0)
         elif name == "k":
-            step = np.float32(32.0 / seq_len)
+            step = np.float32((8.0 if dist == "drift" else 32.0) / seq_len)
             x[..., 0] = x[..., 0] + (tokens.astype(np.float32) * step).reshape(-1, 1)
     elif dist == "sink":
         if name == "q":

@@ -25,12 +25,12 @@ __device__ __forceinline__ float base_value(uint32_t a, uint64_t idx) {
 }
 
 // dist ids follow fpdt_inputs.DISTRIBUTIONS
-enum { D_NORMAL = 0, D_PEAKY, D_DRIFT, D_SINK, D_SAME, D_CLASS, D_EXTREME };
+enum { D_NORMAL = 0, D_PEAKY, D_DRIFT, D_SINK, D_SAME, D_CLASS, D_EXTREME, D_DRIFT32 };
 
 template <typename OutT>
 __global__ void gen_kernel(OutT* __restrict__ out, int tensor, int dist, uint32_t a, int64_t s_local,
                            int n_heads, int head_dim, int64_t seq_len, int rank, int world_size,
-                           int64_t chunk_local, float drift_step) {
+                           int64_t chunk_local, float drift_step, float drift_step32) {
   int64_t total = s_local * n_heads * head_dim;
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total;
        e += (int64_t)gridDim.x * blockDim.x) {
@@ -52,9 +52,9 @@ __global__ void gen_kernel(OutT* __restrict__ out, int tensor, int dist, uint32_
       x = base_value(a, ((uint64_t)g * n_heads + h) * head_dim + dim);
       if (dist == D_PEAKY && tensor == 0) x = __fmul_rn(x, 4.0f);
       if (dist == D_EXTREME && tensor == 0) x = __fmul_rn(x, 30.0f);
-      if (dist == D_DRIFT) {
+      if (dist == D_DRIFT || dist == D_DRIFT32) {
         if (tensor == 0 && dim == 0) x = __fadd_rn(x, 2.0f);
-        if (tensor == 1 && dim == 0) x = __fadd_rn(x, __fmul_rn((float)g, drift_step));
+        if (tensor == 1 && dim == 0) x = __fadd_rn(x, __fmul_rn((float)g, dist == D_DRIFT ? drift_step : drift_step32));
       }
       if (dist == D_SINK) {
         if (tensor == 0) x = __fadd_rn(x, 0.5f);
@@ -84,14 +84,14 @@ int fpdt_gen_fill(void* out, int out_dtype, int tensor, int dist, uint32_t seed,
                   int64_t chunk_size, cudaStream_t stream) {
   uint32_t a = host_mix32(seed * 0x9E3779B9u + (uint32_t)tensor * 0x85EBCA6Bu + 0x632BE5ABu);
   int64_t chunk_local = chunk_size / world_size;
-  float drift_step = (float)(32.0 / (double)seq_len);
+  float drift_step = (float)(8.0 / (double)seq_len), drift_step32 = (float)(32.0 / (double)seq_len);
   int threads = 256, blocks = 148 * 16;
   if (out_dtype == 0)
     gen_kernel<__nv_bfloat16><<<blocks, threads, 0, stream>>>((__nv_bfloat16*)out, tensor, dist, a,
-        s_local, n_heads, head_dim, seq_len, rank, world_size, chunk_local, drift_step);
+        s_local, n_heads, head_dim, seq_len, rank, world_size, chunk_local, drift_step, drift_step32);
   else
     gen_kernel<float><<<blocks, threads, 0, stream>>>((float*)out, tensor, dist, a, s_local, n_heads,
-        head_dim, seq_len, rank, world_size, chunk_local, drift_step);
+        head_dim, seq_len, rank, world_size, chunk_local, drift_step, drift_step32);
   return (int)cudaGetLastError();
 }
 

@@ -202,6 +202,28 @@ const char* fpdt_last_error(void);
 /* Global token index of rank `rank`'s local row `local_t` (rank-ordinal layout). */
 int64_t fpdt_global_token(int64_t local_t, int64_t chunk_size, int world_size, int rank);
 
+/* Key/value fetch strategy of the offloaded schedule (fig:avg_time, whose
+ * latency study compares "every GPU fetches its own chunk" with "one GPU fetches and scatters over NVLink"):
+ *   FPDT_FETCH_PER_RANK (default, A): each rank offloads its head-layout key/value chunks to its own pinned store and
+ *     fetches them back over its own host link;
+ *   FPDT_FETCH_LEADER (B): rank 0 keeps every rank's key/value chunks in its pinned store: at the offload each rank
+ *     sends its chunk to rank 0 (gather over NCCL / the in-process group), at each fetch rank 0 moves all p blocks
+ *     host -> device and sends rank r its block (scatter).  One host link carries p x the key/value bytes; the others
+ *     carry none.  Query-side chunks stay per rank.  The backward then runs the paper's KV-outer order.
+ * Collective setting (all ranks equal); read by the next forward and used by its backward; ignored at world size 1
+ * or offload = 0.  Returns FPDT_OK or FPDT_ERR_ARG. */
+enum { FPDT_FETCH_PER_RANK = 0, FPDT_FETCH_LEADER = 1 };
+int fpdt_set_fetch_strategy(fpdt_ctx* ctx, int strategy);
+
+/* Debug check of the SPMD contract: when enabled (enable != 0) and world_size > 1, every fpdt_attn_* / fpdt_block_*
+ * call first compares a 64-bit hash of its arguments and schedule options (shape, chunk, dtype, offload, hidden,
+ * backward order, residency, sparsity plan) across the ranks -- an NCCL max-reduction plus a host sync, or the
+ * in-process group -- and returns FPDT_ERR_ARG on every rank if they differ, instead of entering mismatched
+ * all-to-alls.  Off by default (it synchronises).  NCCL initialisation and every NCCL call are bounded by
+ * FPDT_NCCL_TIMEOUT_S seconds (environment, default 300): a rank that never joins makes fpdt_ctx_create return
+ * FPDT_ERR_NCCL instead of hanging.  Returns FPDT_OK or FPDT_ERR_ARG (null ctx). */
+int fpdt_set_debug_checks(fpdt_ctx* ctx, int enable);
+
 /* Counters of the context since creation (diagnostics for tests and the bench). */
 typedef struct fpdt_stats {
   int64_t bytes_h2d;          /* host -> device chunk fetches */

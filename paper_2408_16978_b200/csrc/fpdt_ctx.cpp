@@ -16,8 +16,10 @@
 #include <cuda_runtime.h>
 #include <nccl.h>
 
+#include <chrono>
 #include <cmath>
 #include <condition_variable>
+#include <thread>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -67,6 +69,28 @@ struct Fail {
     }                                                                                               \
   } while (0)
 
+// The communicator is non-blocking (so that a rank that never joins makes ncclCommInitRank time out instead of hang):
+// any NCCL call may return ncclInProgress; poll the communicator until the call has been accepted.
+void nccl_settle(ncclComm_t comm, double timeout_s, const char* what) {
+  ncclResult_t st = ncclInProgress;
+  const auto t0 = std::chrono::steady_clock::now();
+  for (;;) {
+    const ncclResult_t r = ncclCommGetAsyncError(comm, &st);
+    if (r != ncclSuccess) st = r;
+    if (st != ncclInProgress) break;
+    if (std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() > timeout_s) {
+      g_last_error = std::string(what) + ": timed out after " + std::to_string(timeout_s) +
+                     " s (a rank did not join, or the ranks' calls differ)";
+      throw Fail{FPDT_ERR_NCCL};
+    }
+    std::this_thread::sleep_for(std::chrono::microseconds(50));
+  }
+  if (st != ncclSuccess) {
+    g_last_error = std::string(what) + ": " + ncclGetErrorString(st);
+    throw Fail{FPDT_ERR_NCCL};
+  }
+}
+
 [[noreturn]] void fail(int code, const std::string& msg) {
   g_last_error = msg;
   throw Fail{code};
@@ -112,7 +136,7 @@ enum BufId {
   B_STORE, B_D, B_DQDEV, B_QSLOT0, B_QSLOT1, B_DOSLOT0, B_DOSLOT1, B_DQSLOT0, B_DQSLOT1, B_DKACC, B_DVACC,
   B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_RESSTORE, B_DORES, B_DQRES, B_DKVSLOT0,
   B_DKVSLOT1, B_DKVRES, B_KVSLOT2, B_KVSLOT3, B_DKVSLOT2, B_DKVSLOT3, B_QOSEND, B_QORECV, B_PROJ0, B_PROJ1,
-  B_PROJ2, B_DOUT, B_OHAT1, B_BWD_SEND1, B_BWD_RECV1, B_NUM
+  B_PROJ2, B_DOUT, B_OHAT1, B_BWD_SEND1, B_BWD_RECV1, B_KVALL0, B_KVALL1, B_KVSTAGE, B_KVGATHER, B_NUM
 };
 
 }  // namespace
@@ -127,6 +151,8 @@ struct fpdt_group {
   int arrived = 0;
   int64_t generation = 0;
   std::vector<const void*> send;
+  std::vector<std::vector<const void*>> send_to;  // p2p: per rank, its send buffer for each destination (or null)
+  std::vector<uint64_t> arg_hash;  // fpdt_set_debug_checks
   std::vector<cudaEvent_t> ev_sent, ev_read;
   void barrier() {
     std::unique_lock<std::mutex> lk(mu);
@@ -149,6 +175,8 @@ struct fpdt_ctx {
   // Q-outer backward: second compute stream (pairs of one query chunk run two at a time) and its slot events
   cudaStream_t s_comp2 = nullptr;
   int qo_streams = 2;  // FPDT_BWD_QO_STREAMS (1 or 2)
+  double nccl_timeout_s = 300.0;  // FPDT_NCCL_TIMEOUT_S: bound on waiting for NCCL initialisation / call acceptance
+  bool check_args = false;        // fpdt_set_debug_checks: compare the call arguments across ranks first
   // scheduler stress (debug, FPDT_STRESS_NS > 0): a random sleep kernel of up to stress_ns ns goes onto the stream of
   // every copy, all-to-all, GEMM and attention launch, before it (SURVEY §4 tier 5)
   uint32_t stress_ns = 0;
@@ -158,13 +186,17 @@ struct fpdt_ctx {
   uint8_t* host = nullptr;
   size_t host_bytes = 0;
   uint8_t* host_dkv = nullptr;  // Q-outer backward: fp32 dK/dV partials [u][2][C][hkv][d] (fpdt_set_bwd_order)
+  // fetch strategy B (fpdt_set_fetch_strategy, rank 0 only): every rank's key/value chunks [u][p][C][2hkv][d]
+  uint8_t* host_kvall = nullptr;
+  size_t host_kvall_bytes = 0;
   size_t host_dkv_bytes = 0;
   DevBuf bufs[B_NUM];
   // per-chunk events
   std::vector<cudaEvent_t> ev_off, ev_doff, ev_dqoff, ev_dkvoff, ev_a2a;
   cudaEvent_t ev_enter = nullptr, ev_slot_free[2] = {}, ev_slot_filled[2] = {}, ev_q_free[2] = {}, ev_q_filled[2] = {},
               ev_dq_ready[2] = {}, ev_kv_free[2] = {}, ev_kv_filled[2] = {}, ev_recv_used_c[2] = {},
-              ev_recv_used_d[2] = {}, ev_ohat_free[2] = {}, ev_bsend_free[2] = {}, ev_o_ready = nullptr, ev_comm_done = nullptr, ev_d2h_done = nullptr,
+              ev_recv_used_d[2] = {}, ev_ohat_free[2] = {}, ev_bsend_free[2] = {}, ev_kvall_free[2] = {}, ev_kvall_filled[2] = {},
+              ev_kvg_free = nullptr, ev_o_ready = nullptr, ev_comm_done = nullptr, ev_d2h_done = nullptr,
               ev_h2d_done = nullptr, ev_tmp = nullptr;
   // saved state
   bool fwd_done = false;
@@ -180,6 +212,7 @@ struct fpdt_ctx {
   // on the device (offload = 1 only); the forward copies the setting, its backward uses the copy
   int64_t res_kv = 0, res_q = 0, saved_res_kv = 0, saved_res_q = 0;
   int bwd_order = FPDT_BWD_KV_OUTER;  // fpdt_set_bwd_order
+  int fetch_strategy = FPDT_FETCH_PER_RANK, saved_fetch = FPDT_FETCH_PER_RANK;  // fpdt_set_fetch_strategy
   fpdt_stats stats{};
   // kernel timing
   bool timing = false;
@@ -192,11 +225,12 @@ struct fpdt_ctx {
   int64_t call_seq = 0;  // fpdt_attn_* / fpdt_block_* calls so far (kernel-gap accounting)
   // every event created once in create_ctx (destroyed by fpdt_ctx_destroy; null handles are skipped)
   std::vector<cudaEvent_t> fixed_events() const {
-    std::vector<cudaEvent_t> v = {ev_enter, ev_o_ready, ev_comm_done, ev_d2h_done, ev_h2d_done, ev_tmp, ev_fork, ev_join};
+    std::vector<cudaEvent_t> v = {ev_enter, ev_o_ready, ev_comm_done, ev_d2h_done, ev_h2d_done, ev_tmp, ev_fork, ev_join,
+                                  ev_kvg_free};
     for (int b = 0; b < 2; ++b)
       for (cudaEvent_t e : {ev_slot_free[b], ev_slot_filled[b], ev_q_free[b], ev_q_filled[b], ev_dq_ready[b],
                             ev_kv_free[b], ev_kv_filled[b], ev_recv_used_c[b], ev_recv_used_d[b], ev_ohat_free[b],
-                            ev_bsend_free[b]})
+                            ev_bsend_free[b], ev_kvall_free[b], ev_kvall_filled[b]})
         v.push_back(e);
     for (int b = 0; b < 4; ++b) v.insert(v.end(), {ev_qo_free[b], ev_qo_filled[b], ev_qo_done[b]});
     for (int b = 0; b < 3; ++b) v.push_back(ev_qo_send[b]);
@@ -413,8 +447,13 @@ void alltoall(fpdt_ctx* ctx, const void* send, void* recv, size_t count_per_peer
     rec(tev->first, ctx->s_comm);
   }
   if (!ctx->group) {
-    FPDT_CHECK_NCCL(ncclAlltoAll(send, recv, count_per_peer, dtype == FPDT_BF16 ? ncclBfloat16 : ncclFloat32,
-                                 ctx->comm, ctx->s_comm));
+    const ncclResult_t r = ncclAlltoAll(send, recv, count_per_peer, dtype == FPDT_BF16 ? ncclBfloat16 : ncclFloat32,
+                                        ctx->comm, ctx->s_comm);
+    if (r != ncclSuccess && r != ncclInProgress) {
+      g_last_error = std::string("ncclAlltoAll: ") + ncclGetErrorString(r);
+      throw Fail{FPDT_ERR_NCCL};
+    }
+    nccl_settle(ctx->comm, ctx->nccl_timeout_s, "ncclAlltoAll");
   } else {
     // local group: publish the send buffer and its ready event, pull every peer's block, then hold the
     // comm stream until every peer has read ours (a send buffer is rewritten only after that).
@@ -437,6 +476,92 @@ void alltoall(fpdt_ctx* ctx, const void* send, void* recv, size_t count_per_peer
   }
   if (tev) rec(tev->second, ctx->s_comm);
   ctx->stats.bytes_a2a += (int64_t)(count_per_peer * (ctx->p - 1) * eb);
+}
+
+// Debug check (fpdt_set_debug_checks): every rank must enter each collective call with the same arguments (SPMD);
+// a mismatch would otherwise hang or corrupt the all-to-alls.  The ranks compare a 64-bit hash of them first
+// (NCCL: max-reductions of h and ~h on the comm stream plus a host sync; local group: through the group object).
+uint64_t hash_mix(uint64_t h, uint64_t v) {
+  h ^= v + 0x9E3779B97F4A7C15ull + (h << 6) + (h >> 2);
+  return h * 0xD1B54A32D192ED03ull;
+}
+void check_collective_args(fpdt_ctx* ctx, int call, const Config& c, int hidden) {
+  if (!ctx->check_args || ctx->p == 1) return;
+  uint64_t h = hash_mix(0, (uint64_t)call);
+  for (uint64_t v : {(uint64_t)c.s_local, (uint64_t)c.Hq, (uint64_t)c.Hkv, (uint64_t)c.d, (uint64_t)c.causal,
+                     (uint64_t)c.C, (uint64_t)c.p, (uint64_t)c.dtype, (uint64_t)c.offload, (uint64_t)hidden,
+                     (uint64_t)ctx->bwd_order, (uint64_t)ctx->res_kv, (uint64_t)ctx->res_q, (uint64_t)ctx->plan_u,
+                     (uint64_t)ctx->fetch_strategy,
+                     (uint64_t)__builtin_bit_cast(uint32_t, c.scale)})
+    h = hash_mix(h, v);
+  for (uint8_t k : ctx->plan) h = hash_mix(h, k);
+  uint64_t lo = h, hi = h;
+  if (ctx->group) {
+    fpdt_group* g = ctx->group;
+    g->arg_hash[ctx->rank] = h;
+    g->barrier();
+    for (uint64_t x : g->arg_hash) lo = std::min(lo, x), hi = std::max(hi, x);
+    g->barrier();
+  } else {
+    uint64_t* buf = nullptr;
+    FPDT_CHECK_CUDA(cudaMallocAsync((void**)&buf, 16, ctx->s_comm));
+    const uint64_t hv[2] = {h, ~h};
+    FPDT_CHECK_CUDA(cudaMemcpyAsync(buf, hv, 16, cudaMemcpyHostToDevice, ctx->s_comm));
+    const ncclResult_t r = ncclAllReduce(buf, buf, 2, ncclUint64, ncclMax, ctx->comm, ctx->s_comm);
+    if (r != ncclSuccess && r != ncclInProgress) fail(FPDT_ERR_NCCL, std::string("ncclAllReduce: ") + ncclGetErrorString(r));
+    nccl_settle(ctx->comm, ctx->nccl_timeout_s, "argument check");
+    uint64_t out[2];
+    FPDT_CHECK_CUDA(cudaMemcpyAsync(out, buf, 16, cudaMemcpyDeviceToHost, ctx->s_comm));
+    FPDT_CHECK_CUDA(cudaFreeAsync(buf, ctx->s_comm));
+    FPDT_CHECK_CUDA(cudaStreamSynchronize(ctx->s_comm));
+    hi = out[0];
+    lo = ~out[1];
+  }
+  if (lo != hi) fail(FPDT_ERR_ARG, "collective call arguments differ across ranks (fpdt_set_debug_checks)");
+}
+
+// Point-to-point exchange on the comm stream (strategy B of the key/value fetch, fpdt_set_fetch_strategy): this rank
+// sends send_to[q] (bytes, nullable) to rank q and receives recv_from[q] (nullable) from rank q; the ranks' calls
+// pair up (a send to q for every receive of q).  Self-transfers are device copies.
+void p2p(fpdt_ctx* ctx, const void* const* send_to, void* const* recv_from, size_t bytes) {
+  const int p = ctx->p, r = ctx->rank;
+  stress(ctx, ctx->s_comm);
+  if (send_to[r] && recv_from[r])
+    FPDT_CHECK_CUDA(cudaMemcpyAsync(recv_from[r], send_to[r], bytes, cudaMemcpyDeviceToDevice, ctx->s_comm));
+  if (!ctx->group) {
+    FPDT_CHECK_NCCL(ncclGroupStart());
+    for (int q = 0; q < p; ++q) {
+      if (q == r) continue;
+      if (send_to[q]) {
+        const ncclResult_t e = ncclSend(send_to[q], bytes, ncclUint8, q, ctx->comm, ctx->s_comm);
+        if (e != ncclSuccess && e != ncclInProgress) fail(FPDT_ERR_NCCL, std::string("ncclSend: ") + ncclGetErrorString(e));
+      }
+      if (recv_from[q]) {
+        const ncclResult_t e = ncclRecv(recv_from[q], bytes, ncclUint8, q, ctx->comm, ctx->s_comm);
+        if (e != ncclSuccess && e != ncclInProgress) fail(FPDT_ERR_NCCL, std::string("ncclRecv: ") + ncclGetErrorString(e));
+      }
+    }
+    const ncclResult_t e = ncclGroupEnd();
+    if (e != ncclSuccess && e != ncclInProgress) fail(FPDT_ERR_NCCL, std::string("ncclGroupEnd: ") + ncclGetErrorString(e));
+    nccl_settle(ctx->comm, ctx->nccl_timeout_s, "p2p exchange");
+  } else {
+    fpdt_group* g = ctx->group;
+    for (int q = 0; q < p; ++q) g->send_to[r][q] = send_to[q];
+    FPDT_CHECK_CUDA(cudaEventRecord(g->ev_sent[r], ctx->s_comm));
+    g->barrier();
+    for (int q = 0; q < p; ++q) {
+      if (q == r || !recv_from[q]) continue;
+      if (!g->send_to[q][r]) fail(FPDT_ERR_STATE, "p2p: receive without a matching send");
+      FPDT_CHECK_CUDA(cudaStreamWaitEvent(ctx->s_comm, g->ev_sent[q], 0));
+      FPDT_CHECK_CUDA(cudaMemcpyAsync(recv_from[q], g->send_to[q][r], bytes, cudaMemcpyDeviceToDevice, ctx->s_comm));
+    }
+    FPDT_CHECK_CUDA(cudaEventRecord(g->ev_read[r], ctx->s_comm));
+    g->barrier();
+    for (int q = 0; q < p; ++q) FPDT_CHECK_CUDA(cudaStreamWaitEvent(ctx->s_comm, g->ev_read[q], 0));
+    g->barrier();
+  }
+  for (int q = 0; q < p; ++q)
+    if (q != r && send_to[q]) ctx->stats.bytes_a2a += (int64_t)bytes;
 }
 
 struct TimedScope {
@@ -511,6 +636,109 @@ void gemm_dw(fpdt_ctx* ctx, int dtype, const void* X, int64_t ldx, const void* d
   ctx->stats.kernel_launches++;
 }
 
+// ------------------------------------------------------------------------------------------ key/value fetch strategies
+// (fig:avg_time: "each GPU fetches its own chunk" (A) vs "one GPU fetches and
+// scatters over NVLink" (B)).  A: every rank offloads its head-layout key/value chunk to its own pinned store and
+// fetches it back over its own host link.  B: rank 0 holds every rank's key/value chunks: at the offload each rank
+// sends its chunk to rank 0 (gather), which writes the p blocks to its pinned store; at a fetch rank 0 moves the p
+// blocks host -> device and sends rank r its block (scatter).  Query-side chunks (q, dO, dq partials) stay per rank.
+struct KvFetch {
+  fpdt_ctx* ctx;
+  const Config& c;
+  bool leader_mode;  // strategy B at p > 1
+  size_t blk;        // bytes of one rank's key/value chunk [C][2hkv][d]
+  uint8_t* kvall[2] = {nullptr, nullptr};
+  uint8_t *stage = nullptr, *gather = nullptr;
+
+  KvFetch(fpdt_ctx* x, const Config& cfg, int strategy) : ctx(x), c(cfg) {
+    leader_mode = strategy == FPDT_FETCH_LEADER && c.p > 1 && c.offload;
+    blk = (size_t)c.C * 2 * c.hkv * c.d * c.eb;
+    if (!leader_mode) return;
+    stage = (uint8_t*)dev(ctx, B_KVSTAGE, blk);
+    if (ctx->rank == 0) {
+      gather = (uint8_t*)dev(ctx, B_KVGATHER, blk * c.p);
+      for (int b = 0; b < 2; ++b) kvall[b] = (uint8_t*)dev(ctx, b ? B_KVALL1 : B_KVALL0, blk * c.p);
+      const size_t need = (size_t)c.u * c.p * blk;
+      if (ctx->host_kvall_bytes < need) {
+        if (ctx->host_kvall) {
+          FPDT_CHECK_CUDA(cudaDeviceSynchronize());
+          cudaFreeHost(ctx->host_kvall);
+          ctx->host_kvall = nullptr;
+          ctx->host_kvall_bytes = 0;
+        }
+        void* hp = nullptr;
+        cudaError_t e = cudaHostAlloc(&hp, need, cudaHostAllocDefault);
+        if (e != cudaSuccess) {
+          cudaGetLastError();
+          fail(FPDT_ERR_HOST_OOM, "pinned all-rank key/value store of " + std::to_string(need) + " bytes: " +
+                                      cudaGetErrorString(e));
+        }
+        ctx->host_kvall = static_cast<uint8_t*>(hp);
+        ctx->host_kvall_bytes = need;
+      }
+    }
+  }
+  void init_events(cudaStream_t cs) {
+    if (!leader_mode) return;
+    for (int b = 0; b < 2; ++b) rec(ctx->ev_kvall_free[b], cs);
+    rec(ctx->ev_kvg_free, cs);
+  }
+  // offload of chunk m's key/value block (head layout, rows `pitch` bytes apart) after ev_a2a[m]; records ev_off[m]
+  // once the block is in the store it will be fetched from
+  void offload(int64_t m, const uint8_t* kv_src, size_t pitch, const HostLayout& hl) {
+    const size_t row_kv2 = (size_t)2 * c.hkv * c.d * c.eb;
+    if (!leader_mode) {
+      wait(ctx->s_d2h, ctx->ev_a2a[m]);
+      d2h_2d(ctx, ctx->host + hl.kv(m, c.u), row_kv2, kv_src, pitch, row_kv2, c.C);
+      return;
+    }
+    const int p = c.p, r = ctx->rank;
+    FPDT_CHECK_CUDA(cudaMemcpy2DAsync(stage, row_kv2, kv_src, pitch, row_kv2, c.C, cudaMemcpyDeviceToDevice,
+                                      ctx->s_comm));
+    std::vector<const void*> send(p, nullptr);
+    std::vector<void*> recv(p, nullptr);
+    send[0] = stage;
+    if (r == 0) {
+      wait(ctx->s_comm, ctx->ev_kvg_free);
+      for (int q = 0; q < p; ++q) recv[q] = gather + (size_t)q * blk;
+    }
+    p2p(ctx, send.data(), recv.data(), blk);
+    if (r == 0) {
+      rec(ctx->ev_tmp, ctx->s_comm);
+      wait(ctx->s_d2h, ctx->ev_tmp);
+      d2h(ctx, ctx->host_kvall + (size_t)m * p * blk, gather, (size_t)p * blk);
+      rec(ctx->ev_kvg_free, ctx->s_d2h);
+    }
+  }
+  // fetch of key/value chunk i into `slot` after ev_free (the slot's last reader); records ev_filled
+  void fetch(int64_t i, uint8_t* slot, int sl, cudaEvent_t ev_free, cudaEvent_t ev_filled, const HostLayout& hl) {
+    if (!leader_mode) {
+      wait(ctx->s_h2d, ev_free);
+      wait(ctx->s_h2d, ctx->ev_off[i]);
+      h2d(ctx, slot, ctx->host + hl.kv(i, c.u), blk);
+      rec(ev_filled, ctx->s_h2d);
+      return;
+    }
+    const int p = c.p, r = ctx->rank;
+    if (r == 0) {
+      wait(ctx->s_h2d, ctx->ev_kvall_free[sl]);
+      wait(ctx->s_h2d, ctx->ev_off[i]);
+      h2d(ctx, kvall[sl], ctx->host_kvall + (size_t)i * p * blk, (size_t)p * blk);
+      rec(ctx->ev_kvall_filled[sl], ctx->s_h2d);
+      wait(ctx->s_comm, ctx->ev_kvall_filled[sl]);
+    }
+    wait(ctx->s_comm, ev_free);
+    std::vector<const void*> send(p, nullptr);
+    std::vector<void*> recv(p, nullptr);
+    recv[0] = slot;
+    if (r == 0)
+      for (int q = 0; q < p; ++q) send[q] = kvall[sl] + (size_t)q * blk;
+    p2p(ctx, send.data(), recv.data(), blk);
+    rec(ev_filled, ctx->s_comm);
+    if (r == 0) rec(ctx->ev_kvall_free[sl], ctx->s_comm);
+  }
+};
+
 // ------------------------------------------------------------------------------------------ forward
 void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const void* v, void* o, float* lse,
              cudaStream_t cs, const Proj* pj = nullptr) {
@@ -567,6 +795,8 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   uint8_t* resstore = (p > 1 && R.n > 0) ? (uint8_t*)dev(ctx, B_RESSTORE, (size_t)R.n * C * hcomb * d * eb) : nullptr;
   auto res_chunk = [&](int64_t m) { return resstore + (size_t)R.slot[(size_t)m] * C * hcomb * d * eb; };
   uint8_t* kv_slot[2] = {nullptr, nullptr};
+  KvFetch kvf(ctx, c, ctx->saved_fetch);
+  kvf.init_events(cs);
   if (c.offload) {
     kv_slot[0] = (uint8_t*)dev(ctx, B_KVSLOT0, (size_t)C * row_kv2);
     kv_slot[1] = (uint8_t*)dev(ctx, B_KVSLOT1, (size_t)C * row_kv2);
@@ -626,9 +856,14 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       wait(ctx->s_d2h, ctx->ev_a2a[m]);
       const size_t pitch = (size_t)hcomb * d * eb;
       if (!R.q(m)) d2h_2d(ctx, ctx->host + hl.q(m), row_q, recv, pitch, row_q, C);
-      if (!R.kv(m)) d2h_2d(ctx, ctx->host + hl.kv(m, u), row_kv2, recv + row_q, pitch, row_kv2, C);
+      if (!R.kv(m)) kvf.offload(m, recv + row_q, pitch, hl);
       rec(ctx->ev_off[m], ctx->s_d2h);
       rec(ctx->ev_recv_used_d[b], ctx->s_d2h);
+      if (kvf.leader_mode) {  // the gather read the receive buffer on the comm stream
+        rec(ctx->ev_tmp, ctx->s_comm);
+        wait(ctx->s_d2h, ctx->ev_tmp);
+        rec(ctx->ev_recv_used_d[b], ctx->s_d2h);
+      }
     }
   };
   int fetch = 0;
@@ -725,10 +960,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
           continue;
         }
         const int sl = fetch & 1;
-        wait(ctx->s_h2d, ctx->ev_slot_free[sl]);
-        wait(ctx->s_h2d, ctx->ev_off[i]);
-        h2d(ctx, kv_slot[sl], ctx->host + hl.kv(i, u), (size_t)C * row_kv2);
-        rec(ctx->ev_slot_filled[sl], ctx->s_h2d);
+        kvf.fetch(i, kv_slot[sl], sl, ctx->ev_slot_free[sl], ctx->ev_slot_filled[sl], hl);
         high = std::max<int64_t>(high, std::min<int64_t>(fetch + 1, 2));  // slots 0/1 alternate
         wait(cs, ctx->ev_slot_filled[sl]);
         a.k = {kv_slot[sl], C, 2 * hkv, 0};
@@ -1282,6 +1514,9 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
                   ? FPDT_BWD_Q_OUTER
                   : FPDT_BWD_KV_OUTER;
     if (proj) order = FPDT_BWD_KV_OUTER;  // the fused projection backward runs per final chunk j
+    KvFetch kvf(ctx, c, ctx->saved_fetch);
+    if (kvf.leader_mode) order = FPDT_BWD_KV_OUTER;  // strategy B is implemented for the paper's loop order
+    kvf.init_events(cs);
     ctx->stats.bwd_order = order;
     if (order == FPDT_BWD_Q_OUTER && !proj) {
       backward_q_outer(ctx, c, R, keep, do_h, do_rows, do_heads, do_head0, dores, dq, dk, dv, cs);
@@ -1318,9 +1553,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
           vj = {res_chunk(j), C, hcomb, hq + hkv};
         }
       } else {
-        wait(ctx->s_h2d, ctx->ev_kv_free[ks]);
-        h2d(ctx, kvs[ks], ctx->host + hl.kv(j, u), (size_t)C * row_kv2);
-        rec(ctx->ev_kv_filled[ks], ctx->s_h2d);
+        kvf.fetch(j, kvs[ks], ks, ctx->ev_kv_free[ks], ctx->ev_kv_filled[ks], hl);
         wait(cs, ctx->ev_kv_filled[ks]);
         kj = {kvs[ks], C, 2 * hkv, 0};
         vj = {kvs[ks], C, 2 * hkv, hkv};
@@ -1459,18 +1692,33 @@ fpdt_ctx* create_ctx(int world_size, int rank, const unsigned char* nccl_id, fpd
     FPDT_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->ev_fork, cudaEventDisableTiming));
     FPDT_CHECK_CUDA(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     cudaEvent_t* evs[] = {&ctx->ev_enter, &ctx->ev_o_ready, &ctx->ev_comm_done, &ctx->ev_d2h_done, &ctx->ev_h2d_done,
-                          &ctx->ev_tmp};
+                          &ctx->ev_tmp, &ctx->ev_kvg_free};
     for (auto e : evs) FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     for (int b = 0; b < 2; ++b) {
       cudaEvent_t* pe[] = {&ctx->ev_slot_free[b], &ctx->ev_slot_filled[b], &ctx->ev_q_free[b], &ctx->ev_q_filled[b],
                            &ctx->ev_dq_ready[b], &ctx->ev_kv_free[b], &ctx->ev_kv_filled[b], &ctx->ev_recv_used_c[b],
-                           &ctx->ev_recv_used_d[b], &ctx->ev_ohat_free[b], &ctx->ev_bsend_free[b]};
+                           &ctx->ev_recv_used_d[b], &ctx->ev_ohat_free[b], &ctx->ev_bsend_free[b],
+                           &ctx->ev_kvall_free[b], &ctx->ev_kvall_filled[b]};
       for (auto e : pe) FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
+    if (const char* e = getenv("FPDT_NCCL_TIMEOUT_S")) ctx->nccl_timeout_s = std::max(1.0, atof(e));
     if (world_size > 1 && !group) {
       ncclUniqueId u;
       std::memcpy(u.internal, nccl_id, 128);
-      FPDT_CHECK_NCCL(ncclCommInitRank(&ctx->comm, world_size, u, rank));
+      ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
+      cfg.blocking = 0;
+      const ncclResult_t r = ncclCommInitRankConfig(&ctx->comm, world_size, u, rank, &cfg);
+      if (r != ncclSuccess && r != ncclInProgress) {
+        g_last_error = std::string("ncclCommInitRankConfig: ") + ncclGetErrorString(r);
+        throw Fail{FPDT_ERR_NCCL};
+      }
+      try {
+        nccl_settle(ctx->comm, ctx->nccl_timeout_s, "ncclCommInitRank");
+      } catch (...) {
+        ncclCommAbort(ctx->comm);
+        ctx->comm = nullptr;
+        throw;
+      }
     }
     if (host_arena_bytes) ensure_host(ctx, host_arena_bytes);
     } catch (...) {
@@ -1500,6 +1748,8 @@ int fpdt_group_create(int world_size, int device, fpdt_group** out) {
     fpdt_group* g = new fpdt_group();
     g->p = world_size;
     g->send.assign(world_size, nullptr);
+    g->send_to.assign(world_size, std::vector<const void*>(world_size, nullptr));
+    g->arg_hash.assign(world_size, 0);
     g->ev_sent.assign(world_size, nullptr);
     g->ev_read.assign(world_size, nullptr);
     for (int r = 0; r < world_size; ++r) {
@@ -1537,6 +1787,7 @@ int fpdt_ctx_destroy(fpdt_ctx* ctx) {
       if (b.ptr) cudaFree(b.ptr);
     if (ctx->host) cudaFreeHost(ctx->host);
     if (ctx->host_dkv) cudaFreeHost(ctx->host_dkv);
+    if (ctx->host_kvall) cudaFreeHost(ctx->host_kvall);
     for (auto v : {&ctx->ev_off, &ctx->ev_doff, &ctx->ev_dqoff, &ctx->ev_dkvoff, &ctx->ev_a2a})
       for (auto e : *v) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->fixed_events())
@@ -1568,6 +1819,8 @@ int fpdt_attn_fwd(fpdt_ctx* ctx, const void* q, const void* k, const void* v, vo
       for (int64_t m = 0; m < c.u; ++m)
         if (!ctx->plan[(size_t)(m * c.u + m)]) fail(FPDT_ERR_ARG, "sparsity plan drops a diagonal block");
     }
+    check_collective_args(ctx, 1, c, 0);
+    ctx->saved_fetch = ctx->fetch_strategy;
     ctx->saved_plan = ctx->plan;
     ctx->saved_res_kv = ctx->res_kv;
     ctx->saved_res_q = ctx->res_q;
@@ -1594,6 +1847,7 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
     if (!(c == ctx->saved)) fail(FPDT_ERR_STATE, "backward arguments differ from the saved forward's");
     if (ctx->saved_hidden) fail(FPDT_ERR_STATE, "the saved forward was fpdt_block_fwd: use fpdt_block_bwd");
     FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
+    check_collective_args(ctx, 2, c, 0);
     backward(ctx, c, o, dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
   });
 }
@@ -1618,12 +1872,14 @@ int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* 
                            softmax_scale);
     check_block_args(ctx, c, hidden);
     FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
+    check_collective_args(ctx, 3, c, hidden);
     if (!ctx->plan.empty()) {
       if (ctx->plan_u != c.u) fail(FPDT_ERR_ARG, "sparsity plan has " + std::to_string(ctx->plan_u) + " chunks, the call " + std::to_string(c.u));
       for (int64_t m = 0; m < c.u; ++m)
         if (!ctx->plan[(size_t)(m * c.u + m)]) fail(FPDT_ERR_ARG, "sparsity plan drops a diagonal block");
     }
     ctx->saved_plan = ctx->plan;
+    ctx->saved_fetch = ctx->fetch_strategy;
     ctx->saved_res_kv = 0;
     ctx->saved_res_q = 0;
     ctx->fwd_done = false;
@@ -1655,6 +1911,7 @@ int fpdt_block_bwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* 
     if (!(c == ctx->saved) || ctx->saved_hidden != hidden || ctx->saved_has_wo != (w_o != nullptr))
       fail(FPDT_ERR_STATE, "backward arguments differ from the saved block forward's");
     FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
+    check_collective_args(ctx, 4, c, hidden);
     Proj pj;
     pj.x = x;
     pj.w = w_qkv;
@@ -1684,6 +1941,19 @@ int fpdt_set_residency(fpdt_ctx* ctx, int64_t kv_chunks, int64_t q_chunks) {
     ctx->res_kv = kv_chunks;
     ctx->res_q = q_chunks;
   });
+}
+
+int fpdt_set_fetch_strategy(fpdt_ctx* ctx, int strategy) {
+  return run([&] {
+    if (!ctx || (strategy != FPDT_FETCH_PER_RANK && strategy != FPDT_FETCH_LEADER)) fail(FPDT_ERR_ARG, "bad fetch strategy");
+    ctx->fetch_strategy = strategy;
+  });
+}
+
+int fpdt_set_debug_checks(fpdt_ctx* ctx, int enable) {
+  if (!ctx) return FPDT_ERR_ARG;
+  ctx->check_args = enable != 0;
+  return FPDT_OK;
 }
 
 int fpdt_set_bwd_order(fpdt_ctx* ctx, int order) {

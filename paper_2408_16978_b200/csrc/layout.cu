@@ -13,45 +13,64 @@ inline int grid_for(int64_t n) {
 }
 
 // B1: D[h*ld + t] = <dO[t,h,:], O[t,h,:]> in fp32 (backward needs o_f, o_g; reading R9).
+// Block = 8 warps on 8 consecutive rows: warp w streams row t0 + w's heads*head_dim elements as consecutive 16-byte
+// vectors (one contiguous run per row, coalesced), writes each vector's partial dot product to shared memory, then
+// threads (head, row) add the head_dim / vector-width partials of one head and write D with consecutive threads on
+// consecutive rows (32-byte runs).  Dynamic shared memory: 8 * heads * vectors-per-head floats.
+constexpr int kDRows = 8;
 template <typename T>
-__global__ void preprocess_D_kernel(const T* __restrict__ o, const T* __restrict__ dout, int64_t rows, int heads,
-                                    int head_dim, int64_t row_ld, const __nv_bfloat16* __restrict__ resid,
-                                    int64_t resid_ld, float* __restrict__ D, int64_t ld) {
-  const int64_t n = rows * heads;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int h = (int)(idx / rows);
-    const int64_t t = idx - (int64_t)h * rows;
-    const T* po = o + t * row_ld + (int64_t)h * head_dim;
-    const T* pd = dout + t * row_ld + (int64_t)h * head_dim;
-    float acc = 0.f;
-    if constexpr (sizeof(T) == 2) {
-      for (int e = 0; e < head_dim; e += 8) {
-        const uint4 a = *reinterpret_cast<const uint4*>(po + e);
-        const uint4 b = *reinterpret_cast<const uint4*>(pd + e);
-        const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
-        const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
-        uint4 rr = make_uint4(0, 0, 0, 0);
-        if (resid) rr = *reinterpret_cast<const uint4*>(resid + t * resid_ld + (int64_t)h * head_dim + e);
-        const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rr);
+__global__ void __launch_bounds__(256) preprocess_D_kernel(const T* __restrict__ o, const T* __restrict__ dout,
+                                                           int64_t rows, int heads, int head_dim, int64_t row_ld,
+                                                           const __nv_bfloat16* __restrict__ resid, int64_t resid_ld,
+                                                           float* __restrict__ D, int64_t ld) {
+  extern __shared__ float part[];  // [kDRows][heads * vph]
+  constexpr int epv = 16 / sizeof(T);  // elements per 16-byte vector
+  const int vph = head_dim / epv, nv = heads * vph;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  for (int64_t t0 = (int64_t)blockIdx.x * kDRows; t0 < rows; t0 += (int64_t)gridDim.x * kDRows) {
+    const int64_t t = t0 + warp;
+    if (t < rows) {
+      const T* po = o + t * row_ld;
+      const T* pd = dout + t * row_ld;
+      for (int v = lane; v < nv; v += 32) {
+        float acc = 0.f;
+        if constexpr (sizeof(T) == 2) {
+          const uint4 a = *reinterpret_cast<const uint4*>(po + (int64_t)v * epv);
+          const uint4 b = *reinterpret_cast<const uint4*>(pd + (int64_t)v * epv);
+          uint4 rr = make_uint4(0, 0, 0, 0);
+          if (resid) rr = *reinterpret_cast<const uint4*>(resid + t * resid_ld + (int64_t)v * epv);
+          const __nv_bfloat162* a2 = reinterpret_cast<const __nv_bfloat162*>(&a);
+          const __nv_bfloat162* b2 = reinterpret_cast<const __nv_bfloat162*>(&b);
+          const __nv_bfloat162* r2 = reinterpret_cast<const __nv_bfloat162*>(&rr);
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const float2 fa = __bfloat1622float2(a2[i]), fb = __bfloat1622float2(b2[i]);
-          const float2 fr = __bfloat1622float2(r2[i]);
-          acc = fmaf(fa.x + fr.x, fb.x, acc);
-          acc = fmaf(fa.y + fr.y, fb.y, acc);
+          for (int i = 0; i < 4; ++i) {
+            const float2 fa = __bfloat1622float2(a2[i]), fb = __bfloat1622float2(b2[i]);
+            const float2 fr = __bfloat1622float2(r2[i]);
+            acc = fmaf(fa.x + fr.x, fb.x, acc);
+            acc = fmaf(fa.y + fr.y, fb.y, acc);
+          }
+        } else {
+          const float4 a = *reinterpret_cast<const float4*>(po + (int64_t)v * epv);
+          const float4 b = *reinterpret_cast<const float4*>(pd + (int64_t)v * epv);
+          acc = fmaf(a.x, b.x, acc);
+          acc = fmaf(a.y, b.y, acc);
+          acc = fmaf(a.z, b.z, acc);
+          acc = fmaf(a.w, b.w, acc);
         }
-      }
-    } else {
-      for (int e = 0; e < head_dim; e += 4) {
-        const float4 a = *reinterpret_cast<const float4*>(po + e);
-        const float4 b = *reinterpret_cast<const float4*>(pd + e);
-        acc = fmaf(a.x, b.x, acc);
-        acc = fmaf(a.y, b.y, acc);
-        acc = fmaf(a.z, b.z, acc);
-        acc = fmaf(a.w, b.w, acc);
+        part[warp * nv + v] = acc;
       }
     }
-    D[(int64_t)h * ld + t] = acc;
+    __syncthreads();
+    for (int i = threadIdx.x; i < heads * kDRows; i += blockDim.x) {
+      const int h = i / kDRows, rr = i - h * kDRows;
+      if (t0 + rr < rows) {
+        const float* pp = part + rr * nv + h * vph;
+        float acc = 0.f;
+        for (int k = 0; k < vph; ++k) acc += pp[k];
+        D[(int64_t)h * ld + t0 + rr] = acc;
+      }
+    }
+    __syncthreads();
   }
 }
 
@@ -103,13 +122,23 @@ __global__ void relayout_kernel(const uint4* __restrict__ src, uint4* __restrict
   }
 }
 
-__global__ void lse_to_user_kernel(const float* __restrict__ src, int64_t ld, int64_t rows, int heads,
-                                   float* __restrict__ dst, int64_t dst_ld, int dst_head0) {
-  const int64_t n = rows * heads;
-  for (int64_t idx = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; idx < n; idx += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t t = idx / heads;
-    const int h = (int)(idx - t * heads);
-    dst[t * dst_ld + dst_head0 + h] = src[(int64_t)h * ld + t] * 0.69314718055994531f;
+// lse layout change [h][t] (log2) -> [t][h] (natural log) through a shared-memory tile of 32 rows x heads: reads run
+// along t, writes along h (both coalesced)
+__global__ void __launch_bounds__(256) lse_to_user_kernel(const float* __restrict__ src, int64_t ld, int64_t rows,
+                                                          int heads, float* __restrict__ dst, int64_t dst_ld,
+                                                          int dst_head0) {
+  extern __shared__ float tile[];  // [heads][33]
+  for (int64_t t0 = (int64_t)blockIdx.x * 32; t0 < rows; t0 += (int64_t)gridDim.x * 32) {
+    for (int i = threadIdx.x; i < heads * 32; i += blockDim.x) {
+      const int h = i >> 5, tt = i & 31;
+      if (t0 + tt < rows) tile[h * 33 + tt] = src[(int64_t)h * ld + t0 + tt] * 0.69314718055994531f;
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < heads * 32; i += blockDim.x) {
+      const int tt = i / heads, h = i - tt * heads;
+      if (t0 + tt < rows) dst[(t0 + tt) * dst_ld + dst_head0 + h] = tile[h * 33 + tt];
+    }
+    __syncthreads();
   }
 }
 
@@ -129,15 +158,24 @@ int launch_stress_sleep(uint32_t ns, cudaStream_t s) {
 int launch_bwd_preprocess_D(const void* o, const void* dout, int dtype, int64_t rows, int heads, int head_dim,
                             int64_t row_ld, const void* resid, int64_t resid_ld, float* D, int64_t ld,
                             cudaStream_t s) {
-  const int64_t n = rows * heads;
+  const int epv = dtype == 0 ? 8 : 4;
+  const size_t smem = (size_t)kDRows * heads * (head_dim / epv) * sizeof(float);
+  const int64_t blocks = (rows + kDRows - 1) / kDRows;
+  const int grid = (int)(blocks < 148 * 8 ? (blocks > 0 ? blocks : 1) : 148 * 8);
+  if (smem > 48 * 1024) {
+    if (smem > 227 * 1024) return (int)cudaErrorInvalidValue;
+    if (int e = set_max_dynamic_smem(dtype == 0 ? (const void*)preprocess_D_kernel<__nv_bfloat16>
+                                                : (const void*)preprocess_D_kernel<float>,
+                                     227 * 1024))
+      return e;
+  }
   if (dtype == 0)
-    preprocess_D_kernel<__nv_bfloat16><<<grid_for(n), kBlock, 0, s>>>((const __nv_bfloat16*)o,
-                                                                      (const __nv_bfloat16*)dout, rows, heads,
-                                                                      head_dim, row_ld, (const __nv_bfloat16*)resid,
-                                                                      resid_ld, D, ld);
+    preprocess_D_kernel<__nv_bfloat16><<<grid, 256, smem, s>>>((const __nv_bfloat16*)o, (const __nv_bfloat16*)dout,
+                                                               rows, heads, head_dim, row_ld,
+                                                               (const __nv_bfloat16*)resid, resid_ld, D, ld);
   else
-    preprocess_D_kernel<float><<<grid_for(n), kBlock, 0, s>>>((const float*)o, (const float*)dout, rows, heads,
-                                                              head_dim, row_ld, nullptr, 0, D, ld);
+    preprocess_D_kernel<float><<<grid, 256, smem, s>>>((const float*)o, (const float*)dout, rows, heads, head_dim,
+                                                       row_ld, nullptr, 0, D, ld);
   return (int)cudaGetLastError();
 }
 
@@ -181,8 +219,10 @@ int launch_unpack_head2seq(const void* src, int64_t src_peer_stride_elems, int64
 
 int launch_lse_to_user(const float* src, int64_t ld, int64_t rows, int heads, float* dst, int64_t dst_ld,
                        int dst_head0, cudaStream_t s) {
-  const int64_t n = rows * heads;
-  lse_to_user_kernel<<<grid_for(n), kBlock, 0, s>>>(src, ld, rows, heads, dst, dst_ld, dst_head0);
+  const int64_t blocks = (rows + 31) / 32;
+  const int grid = (int)(blocks < 148 * 8 ? (blocks > 0 ? blocks : 1) : 148 * 8);
+  lse_to_user_kernel<<<grid, 256, (size_t)heads * 33 * sizeof(float), s>>>(src, ld, rows, heads, dst, dst_ld,
+                                                                           dst_head0);
   return (int)cudaGetLastError();
 }
 

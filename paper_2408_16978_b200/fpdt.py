@@ -15,6 +15,7 @@ FPDT_OK, FPDT_ERR_ARG, FPDT_ERR_DIVISIBILITY, FPDT_ERR_UNSUPPORTED, FPDT_ERR_HOS
     FPDT_ERR_STATE, FPDT_ERR_CUDA, FPDT_ERR_NCCL = range(9)
 FPDT_BF16, FPDT_FP32 = 0, 1
 FPDT_BWD_KV_OUTER, FPDT_BWD_Q_OUTER, FPDT_BWD_AUTO = 0, 1, 2
+FPDT_FETCH_PER_RANK, FPDT_FETCH_LEADER = 0, 1
 STATUS_NAMES = {0: "FPDT_OK", 1: "FPDT_ERR_ARG", 2: "FPDT_ERR_DIVISIBILITY", 3: "FPDT_ERR_UNSUPPORTED",
                 4: "FPDT_ERR_HOST_OOM", 5: "FPDT_ERR_DEVICE_OOM", 6: "FPDT_ERR_STATE", 7: "FPDT_ERR_CUDA",
                 8: "FPDT_ERR_NCCL"}
@@ -24,7 +25,7 @@ EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_a
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_group_create", "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity",
             "fpdt_set_residency", "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes",
-            "fpdt_kernel_gaps", "fpdt_exchange_time")
+            "fpdt_kernel_gaps", "fpdt_exchange_time", "fpdt_set_debug_checks", "fpdt_set_fetch_strategy")
 # include/fpdt_diag.h (libfpdt_diag.so: micro-benchmarks and direct kernel launches, not on the FPDT path)
 DIAG_EXPORTED = ("fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_selftest_softmax", "fpdt_selftest_reduce",
                  "fpdt_selftest_pair", "fpdt_debug_relayout", "fpdt_debug_pair")
@@ -83,6 +84,10 @@ def _declare(lib):
     lib.fpdt_bwd_host_bytes.argtypes = [c_int, c_int64, c_int, c_int, c_int, c_int64, c_int, c_int, c_int64, c_int64,
                                         P, c_int64, ctypes.POINTER(c_int64)]
     lib.fpdt_bwd_host_bytes.restype = c_int
+    lib.fpdt_set_fetch_strategy.argtypes = [P, c_int]
+    lib.fpdt_set_fetch_strategy.restype = c_int
+    lib.fpdt_set_debug_checks.argtypes = [P, c_int]
+    lib.fpdt_set_debug_checks.restype = c_int
     lib.fpdt_set_bwd_order.argtypes = [P, c_int]
     lib.fpdt_set_bwd_order.restype = c_int
     lib.fpdt_get_stats.argtypes = [P, ctypes.POINTER(Stats)]
@@ -214,6 +219,13 @@ class FPDTContext:
         """HBM residency budget for the following forward calls (offload = 1): key/value chunks i < kv_chunks and
         query-side chunks i >= u - q_chunks stay in device memory (include/fpdt.h)."""
         _check(lib().fpdt_set_residency(self.handle, int(kv_chunks), int(q_chunks)))
+
+    def set_fetch_strategy(self, strategy: int):
+        """FPDT_FETCH_PER_RANK (A) or FPDT_FETCH_LEADER (B, rank 0 fetches and scatters)."""
+        _check(lib().fpdt_set_fetch_strategy(self.handle, int(strategy)))
+
+    def set_debug_checks(self, enable: bool = True):
+        _check(lib().fpdt_set_debug_checks(self.handle, int(enable)))
 
     def set_bwd_order(self, order: int):
         """Backward loop order for the following backward calls: FPDT_BWD_KV_OUTER (the paper's), FPDT_BWD_Q_OUTER

@@ -67,3 +67,51 @@ def test_device_working_set_exhaustion():
     fpdt.fpdt_attn_fwd(ctx, q, q, q, o, None, 256, 1, 1, 64, 1, 256, 1, fpdt.FPDT_BF16, 1)
     torch.cuda.synchronize()
     ctx.close()
+
+
+def test_nccl_init_times_out_instead_of_hanging(monkeypatch):
+    """A rank whose peers never join: the non-blocking NCCL initialisation is bounded by FPDT_NCCL_TIMEOUT_S and
+    fpdt_ctx_create returns FPDT_ERR_NCCL (SURVEY §5 failure detection)."""
+    import time
+    from paper_2408_16978_b200 import fpdt
+    monkeypatch.setenv("FPDT_NCCL_TIMEOUT_S", "3")
+    nid = fpdt.fpdt_get_unique_id()
+    t0 = time.time()
+    with pytest.raises(fpdt.FpdtError) as e:
+        fpdt.FPDTContext(2, 0, nid)
+    assert e.value.code == fpdt.FPDT_ERR_NCCL
+    assert "timed out" in str(e.value)
+    assert time.time() - t0 < 60
+
+
+def test_debug_checks_catch_mismatched_ranks():
+    """fpdt_set_debug_checks: ranks entering a collective call with different arguments get FPDT_ERR_ARG on every
+    rank instead of mismatched all-to-alls; equal arguments pass (in-process group, p = 2)."""
+    import threading
+    from paper_2408_16978_b200 import fpdt
+    S, H, d, C = 1024, 2, 64, 512
+    group = fpdt.LocalGroup(2)
+    codes = {}
+
+    def rank_main(r, scale):
+        torch.cuda.set_device(0)
+        q, k, v, o = (_t(S // 2, H, d) for _ in range(4))
+        ctx = fpdt.FPDTContext(2, r, group=group)
+        ctx.set_debug_checks(True)
+        try:
+            fpdt.fpdt_attn_fwd(ctx, q, k, v, o, None, S // 2, H, H, d, 1, C, 2, 0, 1, scale)
+            torch.cuda.synchronize()
+            codes[r] = 0
+        except fpdt.FpdtError as err:
+            codes[r] = err.code
+        ctx.close()
+
+    for scales, want in (((0.0, 0.0), 0), ((0.0, 0.1), fpdt.FPDT_ERR_ARG)):
+        th = [threading.Thread(target=rank_main, args=(r, scales[r])) for r in range(2)]
+        for t in th:
+            t.start()
+        for t in th:
+            t.join(timeout=120)
+        assert not any(t.is_alive() for t in th)
+        assert codes == {0: want, 1: want}, codes
+    group.close()

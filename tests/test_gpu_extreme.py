@@ -2,8 +2,12 @@
 output ... will be rescaled in the next chunk computation").
 
 Two input distributions of fpdt_inputs:
-  * drift   — k[t, 0] += 32 t / S and q[:, 0] += 2: the running row max rises with every chunk (at d = 128 by about
-              5.7 nats over the sequence), so every chunk merge rescales;
+  * drift32 — k[t, 0] += 32 t / S and q[:, 0] += 2: the running row max rises with every chunk (at d = 128 by about
+              5.7 nats over the sequence), so every chunk merge rescales.  The key offset (up to 32 in one dimension)
+              also multiplies the rounding error of dQ = sigma sum_j dS_ij k_j (a sum that cancels): any attention that
+              forms O from bf16 P in the forward has an intrinsic dQ error of 0.5-1.5e-2 here (R28, pinned
+              on the CPU by tests/test_conditioning.py), so dQ is held to 3e-2 for this distribution and every other
+              tensor to the 1e-2 bar;
   * extreme — q x 30: logits of +-100s of nats.  The running max jumps by tens of nats between chunks (past the
               kernels' lazy-rescale threshold of 8 in log2 units, R23), and most keys of a row sit more
               than 126 log2 units below its max, where exp2 underflows (both the MUFU path and the FMA-pipe
@@ -23,13 +27,15 @@ from fpdt_testlib import TOL, inputs, oracle_full, rel_err, run_cuda
 
 pytestmark = pytest.mark.gpu
 
-DISTS = ("drift", "extreme")
+DISTS = ("drift32", "extreme")
+DQ_TOL_DRIFT32 = 3e-2  # DESIGN.md R28
 
 
-def _check(res, ref, tol):
+def _check(res, ref, tol, dist=None):
     errs = {n: rel_err(res[n], ref[n]) for n in ("o", "lse", "dq", "dk", "dv")}
     assert all(np.isfinite(res[n]).all() for n in errs), "non-finite output"
-    assert all(e <= tol for e in errs.values()), errs
+    bar = {n: (DQ_TOL_DRIFT32 if (n == "dq" and dist == "drift32" and tol > 1e-3) else tol) for n in errs}
+    assert all(errs[n] <= bar[n] for n in errs), errs
     return errs
 
 
@@ -37,7 +43,7 @@ def _check(res, ref, tol):
 @pytest.mark.parametrize("d", [64, 80, 128])
 def test_bf16_extreme_logits(dist, d):
     x = inputs(dist, 61, 2048, 4, 2, d)            # u = 4 chunks of 512, GQA G = 2
-    _check(run_cuda(x, 512, "bf16", 1), oracle_full(x), TOL["bf16"])
+    _check(run_cuda(x, 512, "bf16", 1), oracle_full(x), TOL["bf16"], dist)
 
 
 @pytest.mark.parametrize("dist", DISTS)
@@ -51,7 +57,7 @@ def test_fp32_extreme_logits(dist, d):
 def test_bf16_extreme_resident(dist):
     """offload = 0: one launch per query chunk over the whole resident key range (no chunk merge)."""
     x = inputs(dist, 63, 2048, 2, 2, 80)
-    _check(run_cuda(x, 512, "bf16", 0), oracle_full(x), TOL["bf16"])
+    _check(run_cuda(x, 512, "bf16", 0), oracle_full(x), TOL["bf16"], dist)
 
 
 @pytest.mark.parametrize("dist", DISTS)
@@ -61,7 +67,7 @@ def test_multirank_extreme_logits(dist, p):
     S, Hq, Hkv, d, C = 2048, 8, 4, 80, 512
     x = gen.make_inputs(dist, 64, S, Hq, Hkv, d)
     got = run_group(x, p, C, "bf16", 1)
-    _check(got, oracle_full(x), TOL["bf16"])
+    _check(got, oracle_full(x), TOL["bf16"], dist)
     ref1 = run_group(x, 1, C, "bf16", 1)
     for n in ("o", "lse", "dk", "dv"):   # world-size invariance: bitwise
         assert np.array_equal(got[n], ref1[n]), n
@@ -69,7 +75,7 @@ def test_multirank_extreme_logits(dist, p):
 
 @pytest.mark.parametrize("dist", DISTS)
 def test_stress_extreme_logits(dist):
-    from test_gpu_stress import _compare, _ctx, stressed
+    from test_gpu_stress import _ctx, stressed
     S, Hq, Hkv, d, C = 2048, 8, 2, 80, 256
     x = inputs(dist, 65, S, Hq, Hkv, d)
     ctx = _ctx()
@@ -79,7 +85,11 @@ def test_stress_extreme_logits(dist):
         ctx = _ctx()
         got = run_cuda(x, C, "bf16", 1, ctx=ctx)
         ctx.close()
-    _compare(got, base, oracle_full(x), TOL["bf16"])
+    ref = oracle_full(x)
+    for n in ("o", "lse", "dk", "dv"):
+        assert np.array_equal(got[n], base[n]), n
+    assert rel_err(got["dq"], base["dq"]) < 2.0 ** -8
+    _check(got, ref, TOL["bf16"], dist)
 
 
 # ---------------------------------------------------------------------------------- configs[1] at full size
@@ -144,7 +154,8 @@ def test_fullsize_extreme_sampled_rows(full_run):
     dq, o, lse = sampled.rows_dq(qr, dor, rows, kg, vg, sampled.default_scale(D))
     errs = {"o": rel_err(full_run["o"][:, h], o), "lse": rel_err(full_run["lse"][:, h], lse),
             "dq": rel_err(full_run["dq"][:, h], dq)}
-    assert all(e <= TOL["bf16"] for e in errs.values()), errs
+    bar = {"o": TOL["bf16"], "lse": TOL["bf16"], "dq": DQ_TOL_DRIFT32 if dist == "drift32" else TOL["bf16"]}
+    assert all(errs[n] <= bar[n] for n in errs), errs
 
 
 def test_fullsize_extreme_identities(full_run):

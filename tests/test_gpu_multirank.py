@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 
 def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None, residency=None, bwd_order=None,
-              stats=None) -> dict:
+              stats=None, fetch=None, debug_checks=False) -> dict:
     """Shard the global inputs x by the rank-ordinal contract, run fwd+bwd on p local ranks, unshard."""
     from paper_2408_16978_b200 import fpdt
     S, Hq, d = x["q"].shape
@@ -48,6 +48,10 @@ def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None, resi
                 ctx.set_residency(*residency)
             if bwd_order is not None:
                 ctx.set_bwd_order(bwd_order)
+            if fetch is not None:
+                ctx.set_fetch_strategy(fetch)
+            if debug_checks:
+                ctx.set_debug_checks(True)
             fpdt.fpdt_attn_fwd(ctx, q, k, v, o, lse, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
             fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
             stream.synchronize()
