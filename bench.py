@@ -262,6 +262,7 @@ def run_ours(args):
     clocks = sampler.stop()
     st1 = ctx.stats()
     gap_ms, n_gaps = ctx.kernel_gaps()
+    xch = ctx.exchange_time()
     fwd_ms, n_fwd, bwd_ms, n_bwd = ctx.kernel_time(reset=True)
     ctx.set_kernel_timing(False)
     ms = max_over_ranks(e0.elapsed_time(e1) / args.steps)
@@ -402,6 +403,13 @@ def run_ours(args):
                            "gap_ms_per_step": gap_ms / args.steps, "gaps_per_step": n_gaps // args.steps,
                            "exposed_ms_per_step": ms - (fwd_ms + bwd_ms) / args.steps},
         "max_seq_per_gpu": max_seq_record(),
+        # the all-to-alls on the comm stream (p > 1): CUDA events around each exchange; bus GB/s = bytes sent to other
+        # ranks / exchange time (NVLink 5: 900 GB/s per direction per GPU)
+        "exchange": None if world == 1 else {
+            "ms_per_step": xch["total_ms"] / args.steps, "count_per_step": xch["n"] // args.steps,
+            "bytes_per_step": xch["bytes"] // args.steps,
+            "bus_GBps": (xch["bytes"] / (xch["total_ms"] / 1e3) / 1e9) if xch["total_ms"] > 0 else None,
+            "first_ms": xch["first_ms"], "last_ms": xch["last_ms"]},
         "device_bytes_library": st1["device_bytes"],
         "wall_s_timed": wall,
         "cpu_baseline": cpu,

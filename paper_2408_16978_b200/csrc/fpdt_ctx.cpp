@@ -28,6 +28,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "fpdt.h"
 #include "kernels.h"
 
@@ -287,6 +289,13 @@ Residency make_residency(int64_t u, int64_t rkv, int64_t rq) {
   return r;
 }
 
+// NVTX ranges (header-only NVTX3: no-ops unless a tool such as nsys is attached) around the host-side enqueue of each
+// chunk's work, each exchange and each pair launch, so a timeline tool can line them up with the streams.
+struct Nvtx {
+  explicit Nvtx(const char* name) { nvtxRangePushA(name); }
+  ~Nvtx() { nvtxRangePop(); }
+};
+
 void ensure_events(std::vector<cudaEvent_t>& v, size_t n) {
   while (v.size() < n) {
     cudaEvent_t e;
@@ -414,16 +423,19 @@ void ensure_host(fpdt_ctx* ctx, size_t bytes) {
 }
 
 void h2d(fpdt_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  Nvtx nv("fpdt:fetch_h2d");
   stress(ctx, ctx->s_h2d);
   FPDT_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->s_h2d));
   ctx->stats.bytes_h2d += (int64_t)bytes;
 }
 void d2h(fpdt_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  Nvtx nv("fpdt:offload_d2h");
   stress(ctx, ctx->s_d2h);
   FPDT_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
   ctx->stats.bytes_d2h += (int64_t)bytes;
 }
 void d2h_2d(fpdt_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows) {
+  Nvtx nv("fpdt:offload_d2h");
   stress(ctx, ctx->s_d2h);
   FPDT_CHECK_CUDA(cudaMemcpy2DAsync(dst, dpitch, src, spitch, width, rows, cudaMemcpyDeviceToHost, ctx->s_d2h));
   ctx->stats.bytes_d2h += (int64_t)(width * rows);
@@ -431,6 +443,7 @@ void d2h_2d(fpdt_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spi
 
 // All-to-all on the comm stream: send [p][count] -> recv [p][count], recv block q = rank q's send block `rank`.
 void alltoall(fpdt_ctx* ctx, const void* send, void* recv, size_t count_per_peer, int dtype) {
+  Nvtx nv("fpdt:alltoall");
   const size_t eb = dtype == FPDT_BF16 ? 2 : 4;
   stress(ctx, ctx->s_comm);
   std::pair<cudaEvent_t, cudaEvent_t>* tev = nullptr;
@@ -591,6 +604,7 @@ struct TimedScope {
 };
 
 void launch_fwd(fpdt_ctx* ctx, const Config& c, const FwdArgs& a, cudaStream_t s) {
+  Nvtx nv("fpdt:pair_fwd");
   stress(ctx, s);
   TimedScope t(ctx, true, s);
   if (c.dtype == FPDT_BF16)
@@ -601,6 +615,7 @@ void launch_fwd(fpdt_ctx* ctx, const Config& c, const FwdArgs& a, cudaStream_t s
   ctx->stats.attn_launches++;
 }
 void launch_bwd(fpdt_ctx* ctx, const Config& c, const BwdArgs& a, cudaStream_t s) {
+  Nvtx nv("fpdt:pair_bwd");
   stress(ctx, s);
   TimedScope t(ctx, false, s);
   if (c.dtype == FPDT_BF16)
@@ -742,6 +757,7 @@ struct KvFetch {
 // ------------------------------------------------------------------------------------------ forward
 void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const void* v, void* o, float* lse,
              cudaStream_t cs, const Proj* pj = nullptr) {
+  Nvtx nv("fpdt:forward");
   const int64_t C = c.C, u = c.u;
   const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
   const size_t row_q = (size_t)hq * d * eb, row_kv2 = (size_t)2 * hkv * d * eb;
@@ -1274,6 +1290,7 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
 
 void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, void* dq, void* dk, void* dv,
               cudaStream_t cs, const Proj* pj = nullptr) {
+  Nvtx nv("fpdt:backward");
   const int64_t C = c.C, u = c.u;
   const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
   const int hcomb = hq + 2 * hkv;
