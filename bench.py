@@ -242,7 +242,7 @@ def run_ours(args):
     barrier()
 
     # ---------------------------------------------------------------- device-timed region
-    ctx.set_kernel_timing(True)
+    ctx.set_kernel_timing(not args.no_kernel_timing)
     ctx.kernel_time(reset=True)
     st0 = ctx.stats()
     sampler = ClockSampler(local)
@@ -281,8 +281,8 @@ def run_ours(args):
     fwd_launch_ms = fwd_ms / max(n_fwd, 1)
     bwd_flops_launch = f_bwd / world / max(n_bwd // args.steps, 1)
     fwd_flops_launch = f_fwd / world / max(n_fwd // args.steps, 1)
-    ach_bwd = bwd_flops_launch / (bwd_launch_ms / 1e3) / 1e12
-    ach_fwd = fwd_flops_launch / (fwd_launch_ms / 1e3) / 1e12
+    ach_bwd = bwd_flops_launch / (bwd_launch_ms / 1e3) / 1e12 if bwd_launch_ms > 0 else float("nan")
+    ach_fwd = fwd_flops_launch / (fwd_launch_ms / 1e3) / 1e12 if fwd_launch_ms > 0 else float("nan")
     # DRAM bytes of one backward pair launch from the committed ncu --set full capture (profiles/ncu_traffic.json:
     # the full (i > j) chunk pair at this launch shape; the diagonal pairs move about half)
     traffic = None
@@ -439,6 +439,8 @@ def main():
     ap.add_argument("--bwd-order", default="kv", choices=["kv", "q", "auto"],
                     help="backward loop order (fpdt_set_bwd_order): kv = the paper's (KV outer), q = GQA-aware Q outer")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-kernel-timing", action="store_true",
+                    help="A/B check: time the step without the library's per-launch CUDA events (no roofline)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":

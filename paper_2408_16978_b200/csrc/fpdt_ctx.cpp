@@ -994,9 +994,12 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     if (headbuf) rec(ctx->ev_recv_used_c[m & 1], cs);
     // output projection of chunk m (fpdt_block_fwd with w_o): y_m = o_m w_o once O_m is final in the sequence layout
     const int64_t od = (int64_t)c.Hq * d;
-    if (proj && pj->w_o && p == 1)
+    if (proj && pj->w_o && p == 1) {  // on the comm stream, overlapping chunk m+1's pairs
+      rec(ctx->ev_o_ready, cs);
+      wait(ctx->s_comm, ctx->ev_o_ready);
       gemm_xw(ctx, c.dtype, (const uint8_t*)o + (size_t)m * C * od * eb, od, pj->w_o, pj->hidden,
-              (uint8_t*)pj->y + (size_t)m * C * pj->hidden * eb, pj->hidden, C, od, pj->hidden, cs);
+              (uint8_t*)pj->y + (size_t)m * C * pj->hidden * eb, pj->hidden, C, od, pj->hidden, ctx->s_comm);
+    }
     if (p > 1) {
       // F10: all-to-all of O_m back to the sequence layout, then unpack into the caller's rows of slot m (on the comm
       // stream behind chunk m+1's exchange, so it overlaps chunk m+1's pairs)
@@ -1385,11 +1388,11 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   // B7 buffers (p > 1), double-buffered by the outer index j: outer iteration j+1 fills one while chunk j's final
   // dq, dk, dv leave through the other
   uint8_t *bsend2[2] = {nullptr, nullptr}, *brecv2[2] = {nullptr, nullptr};
+  for (int b = 0; b < 2; ++b) rec(ctx->ev_bsend_free[b], cs);
   if (p > 1)
     for (int b = 0; b < 2; ++b) {
       bsend2[b] = (uint8_t*)dev(ctx, b ? B_BWD_SEND1 : B_BWD_SEND, (size_t)C * hcomb * d * eb);
       brecv2[b] = (uint8_t*)dev(ctx, b ? B_BWD_RECV1 : B_BWD_RECV, (size_t)C * hcomb * d * eb);
-      rec(ctx->ev_bsend_free[b], cs);
     }
   uint8_t* bsend = nullptr;  // the send buffer of the current outer iteration
 
@@ -1429,7 +1432,13 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   // B7: after outer iteration j, dq_j, dk_j, dv_j (in bsend) go back to their owner ranks (p > 1)
   auto send_back = [&](int64_t j) {
     if (p == 1) {
-      proj_bwd(j, cs);
+      // the projection backward of chunk j on the comm stream, overlapping the next outer iteration; the
+      // chunk buffer dqkv_buf[j & 1] is rewritten two outer iterations later, after ev_bsend_free[j & 1]
+      if (!proj) return;
+      rec(ctx->ev_o_ready, cs);
+      wait(ctx->s_comm, ctx->ev_o_ready);
+      proj_bwd(j, ctx->s_comm);
+      rec(ctx->ev_bsend_free[j & 1], ctx->s_comm);
       return;
     }
     rec(ctx->ev_o_ready, cs);
@@ -1490,8 +1499,8 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       vv = {store, c.S, hcomb, hq + hkv};
     }
     for (int64_t j = 0; j < u; ++j) {
-      if (p > 1) {
-        bsend = bsend2[j & 1];
+      if (p > 1 || proj) {
+        if (p > 1) bsend = bsend2[j & 1];
         wait(cs, ctx->ev_bsend_free[j & 1]);
       }
       BwdArgs a;
@@ -1550,8 +1559,8 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
     std::vector<char> dq_started((size_t)u, 0);  // chunk i's dq partial already holds contributions (host store)
     for (int64_t j = 0; j < u; ++j) {
       const int ks = (int)(j & 1);
-      if (p > 1) {
-        bsend = bsend2[j & 1];
+      if (p > 1 || proj) {
+        if (p > 1) bsend = bsend2[j & 1];
         wait(cs, ctx->ev_bsend_free[j & 1]);  // chunk j-2's final gradients have left this buffer
       }
       int64_t last_i = j;  // the last query chunk that attends key chunk j
@@ -1799,7 +1808,17 @@ int fpdt_ctx_destroy(fpdt_ctx* ctx) {
   int rc = run([&] {
     cudaSetDevice(ctx->device);
     cudaDeviceSynchronize();
-    if (ctx->comm) ncclCommDestroy(ctx->comm);
+    if (ctx->comm) {
+      // non-blocking communicator: finalize, wait (bounded) for it, then destroy
+      if (ncclCommFinalize(ctx->comm) == ncclInProgress) {
+        ncclResult_t st = ncclInProgress;
+        const auto t0 = std::chrono::steady_clock::now();
+        while (ncclCommGetAsyncError(ctx->comm, &st) == ncclSuccess && st == ncclInProgress &&
+               std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() < ctx->nccl_timeout_s)
+          std::this_thread::sleep_for(std::chrono::microseconds(100));
+      }
+      ncclCommDestroy(ctx->comm);
+    }
     for (auto& b : ctx->bufs)
       if (b.ptr) cudaFree(b.ptr);
     if (ctx->host) cudaFreeHost(ctx->host);

@@ -88,12 +88,16 @@ def main():
         torch.cuda.synchronize()
         return e0.elapsed_time(e1) / n
 
+    from bench import ClockSampler
     run(2, True, True)
     for name, up, down in (("none", False, False), ("uploads", True, False), ("downloads", False, True),
                            ("both", True, True), ("none_again", False, False)):
+        cs = ClockSampler(torch.cuda.current_device())
+        cs.start()
         ms = run(a.steps, up, down)
+        clocks = cs.stop()
         print(json.dumps({"tool": "e2e_probe", "variant": name, "steps": a.steps, "ms_per_step": ms,
-                          "tokens_per_s": S / (ms / 1e3)}), flush=True)
+                          "tokens_per_s": S / (ms / 1e3), "clocks": clocks}), flush=True)
     ctx.close()
 
 
