@@ -24,6 +24,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--steps", type=int, default=3)
     ap.add_argument("--seq", type=int, default=524288)
+    ap.add_argument("--one-set", action="store_true", help="one buffer set for every step (as bench.py's device loop)")
+    ap.add_argument("--variants", nargs="+", default=["none", "uploads", "downloads", "both", "none_again"])
+    ap.add_argument("--warmup-copies", type=int, default=1, help="0: warm up without host copies")
+    ap.add_argument("--no-pinned", action="store_true", help="do not allocate the pinned host buffers")
     a = ap.parse_args()
     S, H, d, C = a.seq, 32, 80, 65536
     genlib = _lib.load_generator()
@@ -36,11 +40,13 @@ def main():
         return t
 
     sets = []
-    for _ in range(2):
+    for _ in range(1 if a.one_set else 2):
         q, k, v, do = g("q"), g("k"), g("v"), g("do")
         sets.append(((q, k, v, do), tuple(torch.empty_like(t) for t in (q, q, k, v))))
-    hin = [torch.empty(t.shape, dtype=bf, pin_memory=True) for t in sets[0][0]]
-    hout = [torch.empty(t.shape, dtype=bf, pin_memory=True) for t in sets[0][1]]
+    hin = [torch.empty(t.shape, dtype=bf, pin_memory=not a.no_pinned) for t in sets[0][0]]
+    for h_, t in zip(hin, sets[0][0]):  # the uploads must carry the real inputs: the GPU's power draw (and so its
+        h_.copy_(t)                      # power-capped clock) depends on the data -- zeros run at 1965 MHz, these at ~1600
+    hout = [torch.empty(t.shape, dtype=bf, pin_memory=not a.no_pinned) for t in sets[0][1]]
     ctx = fpdt.FPDTContext()
     stream = torch.cuda.current_stream()
     cp = torch.cuda.Stream()
@@ -89,14 +95,18 @@ def main():
         return e0.elapsed_time(e1) / n
 
     from bench import ClockSampler
-    run(2, True, True)
-    for name, up, down in (("none", False, False), ("uploads", True, False), ("downloads", False, True),
-                           ("both", True, True), ("none_again", False, False)):
+    if a.one_set:
+        sets.append(sets[0])
+    run(2, bool(a.warmup_copies), bool(a.warmup_copies))
+    table = {"none": (False, False), "uploads": (True, False), "downloads": (False, True), "both": (True, True),
+             "none_again": (False, False)}
+    for name in a.variants:
+        up, down = table[name]
         cs = ClockSampler(torch.cuda.current_device())
         cs.start()
         ms = run(a.steps, up, down)
         clocks = cs.stop()
-        print(json.dumps({"tool": "e2e_probe", "variant": name, "steps": a.steps, "ms_per_step": ms,
+        print(json.dumps({"tool": "e2e_probe", "variant": name, "one_set": a.one_set, "steps": a.steps, "ms_per_step": ms,
                           "tokens_per_s": S / (ms / 1e3), "clocks": clocks}), flush=True)
     ctx.close()
 
