@@ -851,9 +851,16 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     wait(ctx->s_comm, ctx->ev_recv_used_d[b]);
     const size_t per_peer = (size_t)c.c * hcomb * d;
     if (proj) {
+      // The projection GEMM runs on the compute stream, between the pairs of chunk m-1 (it is enqueued one chunk
+      // ahead); its all-to-all still overlaps chunk m-1's pairs on the comm stream.  Measured at the bench shape: on
+      // the comm stream, concurrently with the pair kernels, it only breaks their waves (block overhead 79 vs 68 ms).
+      if (p == 1) wait(cs, ctx->ev_recv_used_d[b]);              // the offload of chunk m-2 has read this buffer
+      else if (m >= 2) wait(cs, ctx->ev_a2a[m - 2]);             // chunk m-2's all-to-all has read the send buffer
       const uint8_t* xm = (const uint8_t*)pj->x + (size_t)m * c.c * pj->hidden * eb;
-      gemm_xw(ctx, c.dtype, xm, pj->hidden, pj->w, ntot, p == 1 ? recv : a2a_send[b], ntot, c.c, pj->hidden, ntot,
-              ctx->s_comm, &scat);
+      gemm_xw(ctx, c.dtype, xm, pj->hidden, pj->w, ntot, p == 1 ? recv : a2a_send[b], ntot, c.c, pj->hidden, ntot, cs,
+              &scat);
+      rec(ctx->ev_tmp, cs);
+      wait(ctx->s_comm, ctx->ev_tmp);
     } else {
       const uint8_t *qm = (const uint8_t*)q + (size_t)m * c.c * c.Hq * d * eb,
                     *km = (const uint8_t*)k + (size_t)m * c.c * c.Hkv * d * eb,
@@ -994,12 +1001,9 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     if (headbuf) rec(ctx->ev_recv_used_c[m & 1], cs);
     // output projection of chunk m (fpdt_block_fwd with w_o): y_m = o_m w_o once O_m is final in the sequence layout
     const int64_t od = (int64_t)c.Hq * d;
-    if (proj && pj->w_o && p == 1) {  // on the comm stream, overlapping chunk m+1's pairs
-      rec(ctx->ev_o_ready, cs);
-      wait(ctx->s_comm, ctx->ev_o_ready);
+    if (proj && pj->w_o && p == 1)
       gemm_xw(ctx, c.dtype, (const uint8_t*)o + (size_t)m * C * od * eb, od, pj->w_o, pj->hidden,
-              (uint8_t*)pj->y + (size_t)m * C * pj->hidden * eb, pj->hidden, C, od, pj->hidden, ctx->s_comm);
-    }
+              (uint8_t*)pj->y + (size_t)m * C * pj->hidden * eb, pj->hidden, C, od, pj->hidden, cs);
     if (p > 1) {
       // F10: all-to-all of O_m back to the sequence layout, then unpack into the caller's rows of slot m (on the comm
       // stream behind chunk m+1's exchange, so it overlaps chunk m+1's pairs)
@@ -1432,13 +1436,11 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   // B7: after outer iteration j, dq_j, dk_j, dv_j (in bsend) go back to their owner ranks (p > 1)
   auto send_back = [&](int64_t j) {
     if (p == 1) {
-      // the projection backward of chunk j on the comm stream, overlapping the next outer iteration; the
-      // chunk buffer dqkv_buf[j & 1] is rewritten two outer iterations later, after ev_bsend_free[j & 1]
+      // the projection backward of chunk j on the compute stream, right after its last pair (concurrent with the
+      // pair kernels on another stream it only breaks their waves; at p > 1 it follows the return all-to-all below)
       if (!proj) return;
-      rec(ctx->ev_o_ready, cs);
-      wait(ctx->s_comm, ctx->ev_o_ready);
-      proj_bwd(j, ctx->s_comm);
-      rec(ctx->ev_bsend_free[j & 1], ctx->s_comm);
+      proj_bwd(j, cs);
+      rec(ctx->ev_bsend_free[j & 1], cs);
       return;
     }
     rec(ctx->ev_o_ready, cs);

@@ -166,3 +166,36 @@ def test_block_with_output_projection(p, dtype):
     ref = {"o": o, "lse": lse, "y": y, "dx": dx, "dw": dw, "dwo": dwo}
     errs = {n: rel_err(got[n], ref[n]) for n in ref}
     assert all(e <= TOL[dtype] for e in errs.values()), errs
+
+
+def test_block_ragged_gemm_shapes():
+    """Projection GEMM tiles that do not divide the problem: hidden = 200 (K and, for the output projection, N not a
+    multiple of the 64 / 256 tile), Hq + 2 Hkv = 4 heads of d = 80 (N = 320), 256-row chunks."""
+    S, hidden, Hq, Hkv, d, C = 1024, 200, 2, 1, 80, 256
+    xin = gen.make_block_inputs("normal", 45, S, hidden, Hq, Hkv, d)
+    op = gen.make_output_proj_inputs(45, S, hidden, Hq, d)
+    got = run_block(xin, 1, C, "bf16", Hq, Hkv, d, oproj=op)
+    o, lse = block.block_forward(xin["x"], xin["w"], Hq, Hkv, d, bf16_intermediates=True)
+    y = block.output_forward(o, op["wo"], bf16_intermediates=True)
+    do, dwo = block.output_backward(o, op["wo"], op["dy"], bf16_intermediates=True)
+    dx, dw = block.block_backward(xin["x"], xin["w"], do, Hq, Hkv, d, bf16_intermediates=True)
+    ref = {"o": o, "lse": lse, "y": y, "dx": dx, "dw": dw, "dwo": dwo}
+    errs = {n: rel_err(got[n], ref[n]) for n in ref}
+    assert all(e <= TOL["bf16"] for e in errs.values()), errs
+
+
+def test_block_stress_world1():
+    """The fused-projection block at p = 1 with u = 8 chunks under scheduler stress (random sleeps before every copy,
+    GEMM and attention launch): the per-chunk projection of chunk m+2 writes the receive buffer chunk m's pairs read,
+    so a missing event edge there shows up as wrong numbers."""
+    from test_gpu_stress import stressed
+    S, hidden, Hq, Hkv, d, C = 2048, 256, 4, 2, 64, 256
+    xin = gen.make_block_inputs("normal", 46, S, hidden, Hq, Hkv, d)
+    op = gen.make_output_proj_inputs(46, S, hidden, Hq, d)
+    base = run_block(xin, 1, C, "bf16", Hq, Hkv, d, oproj=op)
+    with stressed(seed=6):
+        got = run_block(xin, 1, C, "bf16", Hq, Hkv, d, oproj=op)
+    for n in ("o", "lse", "y"):
+        assert np.array_equal(got[n], base[n]), n
+    for n in ("dx", "dw", "dwo"):
+        assert rel_err(got[n], base[n]) < 1e-2, n

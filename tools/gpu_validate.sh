@@ -9,3 +9,4 @@ timeout 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/smok
 timeout 900 python bench.py > gpurun_out/bench.log 2>&1; echo "bench rc=$?"; tail -1 gpurun_out/bench.log | cut -c1-400
 timeout 600 python tools/block_bench.py > gpurun_out/block_bench.log 2>&1; echo "block rc=$?"; tail -1 gpurun_out/block_bench.log | cut -c1-300
 timeout 900 python tools/overlap_probe.py > gpurun_out/overlap.jsonl 2> gpurun_out/overlap.err; echo "overlap rc=$?"
+timeout 900 python tools/e2e_probe.py --one-set --steps 3 > gpurun_out/e2e_probe.jsonl 2> gpurun_out/e2e_probe.err; echo "e2e probe rc=$?"
