@@ -133,7 +133,8 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
  *          the duration of the call) and dw_o = o^T dy (fp32 [Hq d][hidden], output, overwritten)
  *   dx [s_local][hidden] (output, overwritten), dw_qkv fp32 [hidden][(Hq + 2 Hkv) d] (output, overwritten: the sum
  *   over this rank's rows of x^T dqkv; a data-parallel caller all-reduces dw_qkv and dw_o).
- * x, w_qkv, w_o must be unchanged between the two calls, and w_o NULL in both or in neither.  All pointers are device pointers; dtype FPDT_BF16 (x, w, dx
+ * x, w_qkv, w_o must be unchanged between the two calls, and w_o NULL in both or in neither.  fpdt_block_bwd may take
+ * x = NULL when the forward offloaded the hidden state (fpdt_set_hidden_offload): it is then prefetched per chunk.  All pointers are device pointers; dtype FPDT_BF16 (x, w, dx
  * bf16) or FPDT_FP32.  Errors: as fpdt_attn_fwd/bwd; hidden * elem bytes % 16 != 0: FPDT_ERR_ARG; offload = 0 or a
  * residency budget: FPDT_ERR_UNSUPPORTED; fpdt_attn_bwd after fpdt_block_fwd (or the reverse): FPDT_ERR_STATE. */
 int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* w_o, void* o, float* lse, void* y,
@@ -201,6 +202,15 @@ const char* fpdt_last_error(void);
 
 /* Global token index of rank `rank`'s local row `local_t` (rank-ordinal layout). */
 int64_t fpdt_global_token(int64_t local_t, int64_t chunk_size, int world_size, int rank);
+
+/* Hidden-state offload of the block calls ("the prefetching of the input hidden state h_0 will only be
+ * synced in the projection backward").  When enabled (enable != 0) before fpdt_block_fwd, the forward copies each
+ * chunk's input rows x_m [c][hidden] to a pinned host store once its projection has read them, and fpdt_block_bwd may
+ * then be called with x = NULL: the backward prefetches x_j into a double-buffered device slot at the start of outer
+ * iteration j, and only the projection backward of chunk j (dW += x_j^T dqkv_j) waits for it, so the caller need not
+ * keep the hidden states on the device between the passes.  A non-NULL x in fpdt_block_bwd is used in place either
+ * way.  Read by the next fpdt_block_fwd.  Returns FPDT_OK or FPDT_ERR_ARG. */
+int fpdt_set_hidden_offload(fpdt_ctx* ctx, int enable);
 
 /* Key/value fetch strategy of the offloaded schedule (fig:avg_time, whose
  * latency study compares "every GPU fetches its own chunk" with "one GPU fetches and scatters over NVLink"):

@@ -138,7 +138,7 @@ enum BufId {
   B_STORE, B_D, B_DQDEV, B_QSLOT0, B_QSLOT1, B_DOSLOT0, B_DOSLOT1, B_DQSLOT0, B_DQSLOT1, B_DKACC, B_DVACC,
   B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_RESSTORE, B_DORES, B_DQRES, B_DKVSLOT0,
   B_DKVSLOT1, B_DKVRES, B_KVSLOT2, B_KVSLOT3, B_DKVSLOT2, B_DKVSLOT3, B_QOSEND, B_QORECV, B_PROJ0, B_PROJ1,
-  B_PROJ2, B_DOUT, B_OHAT1, B_BWD_SEND1, B_BWD_RECV1, B_KVALL0, B_KVALL1, B_KVSTAGE, B_KVGATHER, B_NUM
+  B_PROJ2, B_DOUT, B_OHAT1, B_BWD_SEND1, B_BWD_RECV1, B_KVALL0, B_KVALL1, B_KVSTAGE, B_KVGATHER, B_X0, B_X1, B_NUM
 };
 
 }  // namespace
@@ -191,6 +191,12 @@ struct fpdt_ctx {
   // fetch strategy B (fpdt_set_fetch_strategy, rank 0 only): every rank's key/value chunks [u][p][C][2hkv][d]
   uint8_t* host_kvall = nullptr;
   size_t host_kvall_bytes = 0;
+  // hidden-state offload of the block calls (fpdt_set_hidden_offload): x chunks [u][c][hidden]
+  uint8_t* host_x = nullptr;
+  size_t host_x_bytes = 0;
+  bool hidden_offload = false, saved_hidden_offload = false;
+  std::vector<cudaEvent_t> ev_xoff;
+  cudaEvent_t ev_x_free[2] = {}, ev_x_filled[2] = {};
   size_t host_dkv_bytes = 0;
   DevBuf bufs[B_NUM];
   // per-chunk events
@@ -232,7 +238,7 @@ struct fpdt_ctx {
     for (int b = 0; b < 2; ++b)
       for (cudaEvent_t e : {ev_slot_free[b], ev_slot_filled[b], ev_q_free[b], ev_q_filled[b], ev_dq_ready[b],
                             ev_kv_free[b], ev_kv_filled[b], ev_recv_used_c[b], ev_recv_used_d[b], ev_ohat_free[b],
-                            ev_bsend_free[b], ev_kvall_free[b], ev_kvall_filled[b]})
+                            ev_bsend_free[b], ev_kvall_free[b], ev_kvall_filled[b], ev_x_free[b], ev_x_filled[b]})
         v.push_back(e);
     for (int b = 0; b < 4; ++b) v.insert(v.end(), {ev_qo_free[b], ev_qo_filled[b], ev_qo_done[b]});
     for (int b = 0; b < 3; ++b) v.push_back(ev_qo_send[b]);
@@ -774,6 +780,26 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   ++ctx->call_seq;
   ensure_events(ctx->ev_off, u);
   ensure_events(ctx->ev_a2a, u);
+  ensure_events(ctx->ev_xoff, u);
+  if (pj && ctx->saved_hidden_offload) {
+    const size_t need = (size_t)u * c.c * pj->hidden * c.eb;
+    if (ctx->host_x_bytes < need) {
+      if (ctx->host_x) {
+        FPDT_CHECK_CUDA(cudaDeviceSynchronize());
+        cudaFreeHost(ctx->host_x);
+        ctx->host_x = nullptr;
+        ctx->host_x_bytes = 0;
+      }
+      void* hp = nullptr;
+      cudaError_t e = cudaHostAlloc(&hp, need, cudaHostAllocDefault);
+      if (e != cudaSuccess) {
+        cudaGetLastError();
+        fail(FPDT_ERR_HOST_OOM, "pinned hidden-state store of " + std::to_string(need) + " bytes: " + cudaGetErrorString(e));
+      }
+      ctx->host_x = static_cast<uint8_t*>(hp);
+      ctx->host_x_bytes = need;
+    }
+  }
   rec(ctx->ev_enter, cs);
   for (cudaStream_t s : {ctx->s_comm, ctx->s_h2d, ctx->s_d2h}) wait(s, ctx->ev_enter);
   HostLayout hl{};
@@ -861,6 +887,15 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
               &scat);
       rec(ctx->ev_tmp, cs);
       wait(ctx->s_comm, ctx->ev_tmp);
+      if (ctx->saved_hidden_offload) {
+        // the input hidden state chunk goes to the pinned store; the backward prefetches it for the projection
+        // backward of chunk m ("the prefetching of the input hidden state h_0 will only be synced in the
+        // projection backward")
+        const size_t xb = (size_t)c.c * pj->hidden * eb;
+        wait(ctx->s_d2h, ctx->ev_tmp);
+        d2h(ctx, ctx->host_x + (size_t)m * xb, xm, xb);
+        rec(ctx->ev_xoff[m], ctx->s_d2h);
+      }
     } else {
       const uint8_t *qm = (const uint8_t*)q + (size_t)m * c.c * c.Hq * d * eb,
                     *km = (const uint8_t*)k + (size_t)m * c.c * c.Hkv * d * eb,
@@ -1410,13 +1445,35 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   if (proj)
     for (int b = 0; b < 2; ++b) dqkv_buf[b] = (uint8_t*)dev(ctx, B_PROJ1 + b, (size_t)c.c * ntot * eb);
   int proj_chunks_done = 0;
+  // hidden-state chunks (x == nullptr: offloaded by the forward, fpdt_set_hidden_offload): prefetched into a double
+  // buffer at the start of outer iteration j, synced only by the projection backward of chunk j
+  const bool x_from_host = proj && pj->x == nullptr;
+  const size_t xbytes = proj ? (size_t)c.c * pj->hidden * eb : 0;
+  uint8_t* xslot[2] = {nullptr, nullptr};
+  if (x_from_host)
+    for (int b = 0; b < 2; ++b) {
+      xslot[b] = (uint8_t*)dev(ctx, b ? B_X1 : B_X0, xbytes);
+      rec(ctx->ev_x_free[b], cs);
+    }
+  auto prefetch_x = [&](int64_t j) {
+    if (!x_from_host) return;
+    wait(ctx->s_h2d, ctx->ev_x_free[j & 1]);
+    wait(ctx->s_h2d, ctx->ev_xoff[j]);
+    h2d(ctx, xslot[j & 1], ctx->host_x + (size_t)j * xbytes, xbytes);
+    rec(ctx->ev_x_filled[j & 1], ctx->s_h2d);
+  };
   auto proj_bwd = [&](int64_t j, cudaStream_t st) {
     if (!proj) return;
     const uint8_t* dy = dqkv_buf[j & 1];
     const size_t xoff = (size_t)j * c.c * pj->hidden * eb;
     gemm_dx(ctx, c.dtype, dy, ntot, pj->w, ntot, (uint8_t*)pj->dx + xoff, pj->hidden, c.c, pj->hidden, ntot, st);
-    gemm_dw(ctx, c.dtype, (const uint8_t*)pj->x + xoff, pj->hidden, dy, ntot, pj->dw, c.c, pj->hidden, ntot,
-            proj_chunks_done++ > 0, st);
+    const uint8_t* xj = (const uint8_t*)pj->x + xoff;
+    if (x_from_host) {
+      wait(st, ctx->ev_x_filled[j & 1]);
+      xj = xslot[j & 1];
+    }
+    gemm_dw(ctx, c.dtype, xj, pj->hidden, dy, ntot, pj->dw, c.c, pj->hidden, ntot, proj_chunks_done++ > 0, st);
+    if (x_from_host) rec(ctx->ev_x_free[j & 1], st);
   };
   // B6: dq_j final (fp32, already scaled) -> the caller's rows (p == 1) or the head-side send buffer (p > 1)
   // dq_final: head-major fp32 rows of chunk j, heads head_stride elements apart
@@ -1568,6 +1625,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       int64_t last_i = j;  // the last query chunk that attends key chunk j
       for (int64_t i = j; i < u; ++i)
         if (keep(i, j)) last_i = i;
+      prefetch_x(j);
       // B3: fetch kv_j (resident key/value chunks are read in place)
       HeadView kj, vj;
       int64_t kv_row0 = 0;
@@ -1726,7 +1784,8 @@ fpdt_ctx* create_ctx(int world_size, int rank, const unsigned char* nccl_id, fpd
       cudaEvent_t* pe[] = {&ctx->ev_slot_free[b], &ctx->ev_slot_filled[b], &ctx->ev_q_free[b], &ctx->ev_q_filled[b],
                            &ctx->ev_dq_ready[b], &ctx->ev_kv_free[b], &ctx->ev_kv_filled[b], &ctx->ev_recv_used_c[b],
                            &ctx->ev_recv_used_d[b], &ctx->ev_ohat_free[b], &ctx->ev_bsend_free[b],
-                           &ctx->ev_kvall_free[b], &ctx->ev_kvall_filled[b]};
+                           &ctx->ev_kvall_free[b], &ctx->ev_kvall_filled[b], &ctx->ev_x_free[b],
+                           &ctx->ev_x_filled[b]};
       for (auto e : pe) FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
     if (const char* e = getenv("FPDT_NCCL_TIMEOUT_S")) ctx->nccl_timeout_s = std::max(1.0, atof(e));
@@ -1826,7 +1885,8 @@ int fpdt_ctx_destroy(fpdt_ctx* ctx) {
     if (ctx->host) cudaFreeHost(ctx->host);
     if (ctx->host_dkv) cudaFreeHost(ctx->host_dkv);
     if (ctx->host_kvall) cudaFreeHost(ctx->host_kvall);
-    for (auto v : {&ctx->ev_off, &ctx->ev_doff, &ctx->ev_dqoff, &ctx->ev_dkvoff, &ctx->ev_a2a})
+    if (ctx->host_x) cudaFreeHost(ctx->host_x);
+    for (auto v : {&ctx->ev_off, &ctx->ev_doff, &ctx->ev_dqoff, &ctx->ev_dkvoff, &ctx->ev_a2a, &ctx->ev_xoff})
       for (auto e : *v) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->fixed_events())
       if (e) cudaEventDestroy(e);
@@ -1921,6 +1981,7 @@ int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* 
     ctx->saved_res_kv = 0;
     ctx->saved_res_q = 0;
     ctx->fwd_done = false;
+    ctx->saved_hidden_offload = ctx->hidden_offload;
     Proj pj;
     pj.x = x;
     pj.w = w_qkv;
@@ -1940,8 +2001,10 @@ int fpdt_block_bwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* 
                    void* dx, float* dw_qkv, float* dw_o, int64_t s_local, int hidden, int n_q_heads, int n_kv_heads, int head_dim, int causal,
                    int64_t chunk_size, int world_size, int dtype, int offload, float softmax_scale, void* stream) {
   return run([&] {
-    if (!ctx || !x || !w_qkv || !o || !dout || !dx || !dw_qkv || (w_o && !dw_o))
+    if (!ctx || !w_qkv || !o || !dout || !dx || !dw_qkv || (w_o && !dw_o))
       fail(FPDT_ERR_ARG, "null pointer argument");
+    if (!x && !ctx->saved_hidden_offload)
+      fail(FPDT_ERR_ARG, "x is NULL but the forward did not offload the hidden state (fpdt_set_hidden_offload)");
     if (world_size != ctx->p) fail(FPDT_ERR_ARG, "world_size differs from the context's");
     Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
                            softmax_scale);
@@ -1979,6 +2042,12 @@ int fpdt_set_residency(fpdt_ctx* ctx, int64_t kv_chunks, int64_t q_chunks) {
     ctx->res_kv = kv_chunks;
     ctx->res_q = q_chunks;
   });
+}
+
+int fpdt_set_hidden_offload(fpdt_ctx* ctx, int enable) {
+  if (!ctx) return FPDT_ERR_ARG;
+  ctx->hidden_offload = enable != 0;
+  return FPDT_OK;
 }
 
 int fpdt_set_fetch_strategy(fpdt_ctx* ctx, int strategy) {

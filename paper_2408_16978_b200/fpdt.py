@@ -25,7 +25,8 @@ EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_a
             "fpdt_last_error", "fpdt_global_token", "fpdt_get_stats", "fpdt_set_kernel_timing", "fpdt_kernel_time",
             "fpdt_group_create", "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity",
             "fpdt_set_residency", "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes",
-            "fpdt_kernel_gaps", "fpdt_exchange_time", "fpdt_set_debug_checks", "fpdt_set_fetch_strategy")
+            "fpdt_kernel_gaps", "fpdt_exchange_time", "fpdt_set_debug_checks", "fpdt_set_fetch_strategy",
+            "fpdt_set_hidden_offload")
 # include/fpdt_diag.h (libfpdt_diag.so: micro-benchmarks and direct kernel launches, not on the FPDT path)
 DIAG_EXPORTED = ("fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_selftest_softmax", "fpdt_selftest_reduce",
                  "fpdt_selftest_pair", "fpdt_debug_relayout", "fpdt_debug_pair")
@@ -84,6 +85,8 @@ def _declare(lib):
     lib.fpdt_bwd_host_bytes.argtypes = [c_int, c_int64, c_int, c_int, c_int, c_int64, c_int, c_int, c_int64, c_int64,
                                         P, c_int64, ctypes.POINTER(c_int64)]
     lib.fpdt_bwd_host_bytes.restype = c_int
+    lib.fpdt_set_hidden_offload.argtypes = [P, c_int]
+    lib.fpdt_set_hidden_offload.restype = c_int
     lib.fpdt_set_fetch_strategy.argtypes = [P, c_int]
     lib.fpdt_set_fetch_strategy.restype = c_int
     lib.fpdt_set_debug_checks.argtypes = [P, c_int]
@@ -219,6 +222,10 @@ class FPDTContext:
         """HBM residency budget for the following forward calls (offload = 1): key/value chunks i < kv_chunks and
         query-side chunks i >= u - q_chunks stay in device memory (include/fpdt.h)."""
         _check(lib().fpdt_set_residency(self.handle, int(kv_chunks), int(q_chunks)))
+
+    def set_hidden_offload(self, enable: bool = True):
+        """fpdt_block_fwd offloads the hidden-state chunks; fpdt_block_bwd may then take x = None."""
+        _check(lib().fpdt_set_hidden_offload(self.handle, int(enable)))
 
     def set_fetch_strategy(self, strategy: int):
         """FPDT_FETCH_PER_RANK (A) or FPDT_FETCH_LEADER (B, rank 0 fetches and scatters)."""

@@ -15,8 +15,10 @@ from oracle import attention, block
 pytestmark = pytest.mark.gpu
 
 
-def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, keep=None, oproj=None) -> dict:
-    """oproj: {"wo", "dy"} for the output projection (y = o wo; the backward starts from dy)."""
+def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, keep=None, oproj=None,
+              hidden_offload=False, stats=None) -> dict:
+    """oproj: {"wo", "dy"} for the output projection (y = o wo; the backward starts from dy).  hidden_offload: the
+    forward offloads x and the backward gets x = None (fpdt_set_hidden_offload)."""
     from paper_2408_16978_b200 import fpdt
     S, hidden = xin["x"].shape
     s_local = S // p
@@ -51,15 +53,19 @@ def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, 
             ctx = fpdt.FPDTContext(p, r, group=group) if p > 1 else fpdt.FPDTContext()
             if keep is not None:
                 ctx.set_sparsity(keep)
+            if hidden_offload:
+                ctx.set_hidden_offload(True)
             fpdt.fpdt_block_fwd(ctx, x, w, o, lse, s_local, hidden, Hq, Hkv, d, 1, C, p, code, 1, 0.0, stream,
                                 w_o=wo, y=y)
-            fpdt.fpdt_block_bwd(ctx, x, w, o, do, dx, dw, s_local, hidden, Hq, Hkv, d, 1, C, p, code, 1, 0.0, stream,
-                                w_o=wo, dw_o=dwo)
+            fpdt.fpdt_block_bwd(ctx, None if hidden_offload else x, w, o, do, dx, dw, s_local, hidden, Hq, Hkv, d, 1, C,
+                                p, code, 1, 0.0, stream, w_o=wo, dw_o=dwo)
             stream.synchronize()
             out["o"][rows[r]] = o.float().cpu().numpy()
             out["lse"][rows[r]] = lse.cpu().numpy()
             out["dx"][rows[r]] = dx.float().cpu().numpy()
             out["dw"][r] = dw.cpu().numpy()
+            if stats is not None:
+                stats[r] = ctx.stats()
             if oproj is not None:
                 out["y"][rows[r]] = y.float().cpu().numpy()
                 out["dwo"][r] = dwo.cpu().numpy()
@@ -199,3 +205,25 @@ def test_block_stress_world1():
         assert np.array_equal(got[n], base[n]), n
     for n in ("dx", "dw", "dwo"):
         assert rel_err(got[n], base[n]) < 1e-2, n
+
+
+@pytest.mark.parametrize("p", [1, 2])
+def test_block_hidden_offload(p):
+    """The forward offloads the hidden-state chunks and the backward, called with x = None, prefetches them for the
+    projection backward: same O, dx, dW as with x on the device; the host link carries the x bytes."""
+    S, hidden, Hq, Hkv, d, C = 2048, 256, 4, 2, 64, 512
+    xin = gen.make_block_inputs("normal", 47, S, hidden, Hq, Hkv, d)
+    st_a, st_b = {}, {}
+    a = run_block(xin, p, C, "bf16", Hq, Hkv, d, stats=st_a)
+    b = run_block(xin, p, C, "bf16", Hq, Hkv, d, hidden_offload=True, stats=st_b)
+    for n in ("o", "lse"):
+        assert np.array_equal(a[n], b[n]), n
+    for n in ("dx", "dw"):
+        assert rel_err(b[n], a[n]) < 1e-2, n
+    ref = oracle_block(xin, Hq, Hkv, d, "bf16")
+    errs = {n: rel_err(b[n], ref[n]) for n in ref}
+    assert all(e <= TOL["bf16"] for e in errs.values()), errs
+    xbytes = (S // p) * hidden * 2
+    for r in range(p):
+        assert st_b[r]["bytes_d2h"] - st_a[r]["bytes_d2h"] == xbytes
+        assert st_b[r]["bytes_h2d"] - st_a[r]["bytes_h2d"] == xbytes
