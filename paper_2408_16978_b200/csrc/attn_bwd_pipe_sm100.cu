@@ -53,7 +53,11 @@ static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs -
 // (sum_j dS_ij = 0), so a common offset of the keys multiplies the rounding error of dS -- a key drift of 32 in one
 // dimension (fpdt_inputs "drift") costs ~1.2e-2 normwise in dQ with bf16 dS, ~1.5e-3 with fp16 (measured: bf16
 // 0.012-0.026 on the GPU drift cases).  The fp16 copy of K takes the shared memory of a third Q stage (2 stages:
-// 858 vs 871 TFLOP/s for the bf16 product with 3 stages, C = 64K, 32 x 80 diagonal pair).
+// 858 vs 871 TFLOP/s for the bf16 product with 3 stages, C = 64K, 32 x 80 diagonal pair).  The third stage is not
+// what the 1.5% went to (tools/gpu_ab_qs.sh, same box): d = 64, where it fits, gains 0.5% from it (817 -> 821), and
+// at d = 80 buying it back with a 3-slot 16-column dQ staging ring per half (a wait for the reduce-add to read the
+// ring in the middle of every tile) loses 13% (856 -> 746): the bulk reduce-add's read of the staging is slow enough
+// that the staging must hold a whole tile.
 template <int D>
 struct PipeCfg {
   using T = Tile<D>;
