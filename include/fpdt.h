@@ -115,11 +115,34 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
                   int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
                   int dtype, int offload, float softmax_scale, void* stream);
 
+/* Forward and backward with the caller's tensors in HOST memory (the paper's setting: activations live in host
+ * memory and each chunk is brought to the GPU when it is needed, "we offload ... to the host memory"
+ * "the prefetching of the input hidden state").  Same arguments, shapes, layouts and errors as fpdt_attn_fwd /
+ * fpdt_attn_bwd, except that q, k, v, o, lse (forward) and o, dout, dq, dk, dv (backward) are host pointers, pinned
+ * (cudaHostAlloc / cudaHostRegister) for the copies to run asynchronously.  The library stages the rows through
+ * device mirrors (library-owned, s_local rows of each tensor) chunk by chunk on its own copy streams: chunk m's upload
+ * is enqueued just ahead of its first reader and each chunk's output rows leave as soon as they are final, so the
+ * host copies share the host link with the chunk fetches in the schedule's own order.  With world_size 1 the backward
+ * fetches q_i and dO_i straight from the caller's host rows (the forward does not offload q): the forward's host q
+ * must stay valid and unmodified until fpdt_attn_bwd_host.  The backward reuses the forward's device copy of o when
+ * `o` is the forward's output pointer (else it uploads o first).  Outputs are complete when `stream` reaches the end
+ * of the call.  offload must be 1 and no residency budget set (FPDT_ERR_UNSUPPORTED); the backward runs the paper's
+ * KV-outer order; the sparsity plan and the fetch strategy apply as for fpdt_attn_fwd.  fpdt_attn_bwd_host needs a
+ * saved fpdt_attn_fwd_host (and fpdt_attn_bwd an fpdt_attn_fwd): else FPDT_ERR_STATE.  Host bytes moved for the
+ * caller's rows are counted in fpdt_stats.bytes_io_h2d / bytes_io_d2h. */
+int fpdt_attn_fwd_host(fpdt_ctx* ctx, const void* q, const void* k, const void* v, void* o, float* lse,
+                       int64_t s_local, int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size,
+                       int world_size, int dtype, int offload, float softmax_scale, void* stream);
+int fpdt_attn_bwd_host(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void* dk, void* dv, int64_t s_local,
+                       int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
+                       int dtype, int offload, float softmax_scale, void* stream);
+
 /* Attention block with the chunked QKV projection fused in front.  PAPER.md P:L206: "we
  * directly slice the local sequence tensor into u chunks ... T_i is projected to query q_i, key k_i, and value v_i.
  * Then, we perform the Alltoall"; the final dq_j, dk_j, dv_j, all-to-all'd back, "are used to compute the
- * gradient of the input hidden state".  Per chunk the projection is a plain GEMM (cuBLAS, fp32 accumulation; fp32
- * mode without TF32) on the comm stream just before the chunk's all-to-all, so the full-sequence q, k, v never exist;
+ * gradient of the input hidden state".  Per chunk the projection is the library's tcgen05 GEMM (fp32 accumulation;
+ * fp32 mode: a SIMT fp32 GEMM) whose epilogue writes the all-to-all send layout, enqueued one chunk ahead of the
+ * chunk's all-to-all, so the full-sequence q, k, v never exist;
  * in the backward each chunk's projection gradient runs as soon as its dq, dk, dv are final (the paper's KV-outer
  * order; fpdt_set_bwd_order is ignored here).
  *   x      [s_local][hidden]                         hidden state, rank-ordinal rows (as q of fpdt_attn_fwd)
@@ -247,6 +270,8 @@ typedef struct fpdt_stats {
   int64_t bwd_order;          /* loop order of the last fpdt_attn_bwd (FPDT_BWD_KV_OUTER / FPDT_BWD_Q_OUTER) */
   int64_t host_dkv_bytes;     /* pinned store of the Q-outer backward's dK/dV partials (0 until first used) */
   int64_t stress_sleeps;      /* debug sleep kernels enqueued by the scheduler stress mode (env FPDT_STRESS_NS) */
+  int64_t bytes_io_h2d;       /* caller rows uploaded by fpdt_attn_fwd_host / fpdt_attn_bwd_host */
+  int64_t bytes_io_d2h;       /* caller rows downloaded by fpdt_attn_fwd_host / fpdt_attn_bwd_host */
 } fpdt_stats;
 int fpdt_get_stats(const fpdt_ctx* ctx, fpdt_stats* out);
 

@@ -138,7 +138,8 @@ enum BufId {
   B_STORE, B_D, B_DQDEV, B_QSLOT0, B_QSLOT1, B_DOSLOT0, B_DOSLOT1, B_DQSLOT0, B_DQSLOT1, B_DKACC, B_DVACC,
   B_BWD_SEND, B_BWD_RECV, B_LSE_T, B_LSE_RECV, B_DOSTORE, B_ORESID, B_RESSTORE, B_DORES, B_DQRES, B_DKVSLOT0,
   B_DKVSLOT1, B_DKVRES, B_KVSLOT2, B_KVSLOT3, B_DKVSLOT2, B_DKVSLOT3, B_QOSEND, B_QORECV, B_PROJ0, B_PROJ1,
-  B_PROJ2, B_DOUT, B_OHAT1, B_BWD_SEND1, B_BWD_RECV1, B_KVALL0, B_KVALL1, B_KVSTAGE, B_KVGATHER, B_X0, B_X1, B_NUM
+  B_PROJ2, B_DOUT, B_OHAT1, B_BWD_SEND1, B_BWD_RECV1, B_KVALL0, B_KVALL1, B_KVSTAGE, B_KVGATHER, B_X0, B_X1,
+  B_HQ, B_HK, B_HV, B_HO, B_HLSE, B_HDO, B_HDQ, B_HDK, B_HDV, B_NUM
 };
 
 }  // namespace
@@ -200,7 +201,7 @@ struct fpdt_ctx {
   size_t host_dkv_bytes = 0;
   DevBuf bufs[B_NUM];
   // per-chunk events
-  std::vector<cudaEvent_t> ev_off, ev_doff, ev_dqoff, ev_dkvoff, ev_a2a;
+  std::vector<cudaEvent_t> ev_off, ev_doff, ev_dqoff, ev_dkvoff, ev_a2a, ev_up;
   cudaEvent_t ev_enter = nullptr, ev_slot_free[2] = {}, ev_slot_filled[2] = {}, ev_q_free[2] = {}, ev_q_filled[2] = {},
               ev_dq_ready[2] = {}, ev_kv_free[2] = {}, ev_kv_filled[2] = {}, ev_recv_used_c[2] = {},
               ev_recv_used_d[2] = {}, ev_ohat_free[2] = {}, ev_bsend_free[2] = {}, ev_kvall_free[2] = {}, ev_kvall_filled[2] = {},
@@ -216,6 +217,10 @@ struct fpdt_ctx {
   std::vector<uint8_t> plan, saved_plan;
   int64_t plan_u = 0;
   const void *saved_q = nullptr, *saved_k = nullptr, *saved_v = nullptr;
+  // the saved forward was fpdt_attn_fwd_host: its caller's host q (the world-size-1 backward fetches q_i from it) and
+  // host o (the backward's o argument; the forward's device mirror of it still holds the output)
+  bool saved_hostio = false;
+  const void *saved_host_q = nullptr, *saved_host_o = nullptr;
   // HBM residency budget (fpdt_set_residency): key/value chunks i < res_kv and query-side chunks i >= u - res_q stay
   // on the device (offload = 1 only); the forward copies the setting, its backward uses the copy
   int64_t res_kv = 0, res_q = 0, saved_res_kv = 0, saved_res_q = 0;
@@ -439,6 +444,19 @@ void d2h(fpdt_ctx* ctx, void* dst, const void* src, size_t bytes) {
   stress(ctx, ctx->s_d2h);
   FPDT_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
   ctx->stats.bytes_d2h += (int64_t)bytes;
+}
+// the caller's rows of the host-memory calls (fpdt_attn_fwd_host / fpdt_attn_bwd_host), on the same two copy streams
+void h2d_io(fpdt_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  Nvtx nv("fpdt:io_h2d");
+  stress(ctx, ctx->s_h2d);
+  FPDT_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, ctx->s_h2d));
+  ctx->stats.bytes_io_h2d += (int64_t)bytes;
+}
+void d2h_io(fpdt_ctx* ctx, void* dst, const void* src, size_t bytes) {
+  Nvtx nv("fpdt:io_d2h");
+  stress(ctx, ctx->s_d2h);
+  FPDT_CHECK_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, ctx->s_d2h));
+  ctx->stats.bytes_io_d2h += (int64_t)bytes;
 }
 void d2h_2d(fpdt_ctx* ctx, void* dst, size_t dpitch, const void* src, size_t spitch, size_t width, size_t rows) {
   Nvtx nv("fpdt:offload_d2h");
@@ -761,8 +779,21 @@ struct KvFetch {
 };
 
 // ------------------------------------------------------------------------------------------ forward
+// Caller rows in host memory (fpdt_attn_fwd_host / fpdt_attn_bwd_host).  forward() and backward() then run on device
+// mirrors of the caller's tensors (the q, k, v, o, ... arguments) and stage the caller's rows through them chunk by
+// chunk on the library's own copy streams: chunk m's upload is enqueued just ahead of its first reader (one chunk
+// ahead of the compute, in the same stream order as the chunk fetches), each chunk's output rows leave as soon as
+// they are final.  World size 1 also fetches q_i and dO_i for the backward straight from the caller's host rows
+// (their layout is the host store's), so those are never offloaded.
+struct HostIO {
+  const void *q = nullptr, *k = nullptr, *v = nullptr, *dout = nullptr;  // host inputs
+  void *o = nullptr, *dq = nullptr, *dk = nullptr, *dv = nullptr;        // host outputs
+  float* lse = nullptr;
+  bool upload_o = false;  // backward: o is not the saved forward's output (its mirror is stale): upload it first
+};
+
 void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const void* v, void* o, float* lse,
-             cudaStream_t cs, const Proj* pj = nullptr) {
+             cudaStream_t cs, const Proj* pj = nullptr, const HostIO* io = nullptr) {
   Nvtx nv("fpdt:forward");
   const int64_t C = c.C, u = c.u;
   const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
@@ -781,6 +812,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   ensure_events(ctx->ev_off, u);
   ensure_events(ctx->ev_a2a, u);
   ensure_events(ctx->ev_xoff, u);
+  if (io) ensure_events(ctx->ev_up, u);
   if (pj && ctx->saved_hidden_offload) {
     const size_t need = (size_t)u * c.c * pj->hidden * c.eb;
     if (ctx->host_x_bytes < need) {
@@ -849,8 +881,28 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     rec(ctx->ev_recv_used_d[b], cs);
     rec(ctx->ev_ohat_free[b], cs);
   }
+  // host rows: chunk m's q, k, v rows -> the device mirrors (records ev_up[m])
+  auto upload = [&](int64_t m) {
+    const size_t bq = (size_t)c.c * c.Hq * d * eb, bkv = (size_t)c.c * c.Hkv * d * eb;
+    h2d_io(ctx, (uint8_t*)q + (size_t)m * bq, (const uint8_t*)io->q + (size_t)m * bq, bq);
+    h2d_io(ctx, (uint8_t*)k + (size_t)m * bkv, (const uint8_t*)io->k + (size_t)m * bkv, bkv);
+    h2d_io(ctx, (uint8_t*)v + (size_t)m * bkv, (const uint8_t*)io->v + (size_t)m * bkv, bkv);
+    rec(ctx->ev_up[(size_t)m], ctx->s_h2d);
+  };
+  // p == 1, host rows: upload chunk m, then offload its key/value rows (q_m stays in the caller's host rows, from
+  // which the backward fetches it)
+  auto stage_p1 = [&](int64_t m) {
+    upload(m);
+    wait(ctx->s_d2h, ctx->ev_up[(size_t)m]);
+    const size_t wkv = (size_t)hkv * d * eb;
+    d2h_2d(ctx, ctx->host + hl.kv(m, u), row_kv2, (const uint8_t*)k + (size_t)m * C * wkv, wkv, wkv, C);
+    d2h_2d(ctx, ctx->host + hl.kv(m, u) + wkv, row_kv2, (const uint8_t*)v + (size_t)m * C * wkv, wkv, wkv, C);
+    rec(ctx->ev_off[(size_t)m], ctx->s_d2h);
+  };
+  const bool io_p1 = io && p == 1;
+  if (io_p1) stage_p1(0);
   // p == 1 with offload: the head-layout chunk IS the caller's rows; offload all chunks up front
-  if (p == 1 && c.offload && !proj) {
+  if (p == 1 && c.offload && !proj && !io) {
     for (int64_t m = 0; m < u; ++m) {
       if (!R.q(m)) d2h(ctx, ctx->host + hl.q(m), (const uint8_t*)q + (size_t)m * C * row_q, (size_t)C * row_q);
       if (!R.kv(m)) {
@@ -897,6 +949,10 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
         rec(ctx->ev_xoff[m], ctx->s_d2h);
       }
     } else {
+      if (io) {
+        upload(m);
+        wait(ctx->s_comm, ctx->ev_up[(size_t)m]);
+      }
       const uint8_t *qm = (const uint8_t*)q + (size_t)m * c.c * c.Hq * d * eb,
                     *km = (const uint8_t*)k + (size_t)m * c.c * c.Hkv * d * eb,
                     *vm = (const uint8_t*)v + (size_t)m * c.c * c.Hkv * d * eb;
@@ -932,6 +988,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   if (headbuf) exchange(0);
   for (int64_t m = 0; m < u; ++m) {
     if (headbuf && m + 1 < u) exchange(m + 1);
+    if (io_p1 && m + 1 < u) stage_p1(m + 1);  // overlaps chunk m's pairs, ahead of their fetches on s_h2d
     int64_t last_kept = -1;  // the last earlier key chunk chunk m attends
     for (int64_t i = 0; i < m; ++i)
       if (keep(m, i)) last_kept = i;
@@ -939,6 +996,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     HeadView qv, kv, vv;
     int64_t q_row0, kv_row0_cur;
     if (!headbuf) {
+      if (io_p1) wait(cs, ctx->ev_up[(size_t)m]);
       qv = {q, c.S, hq, 0};
       kv = {k, c.S, hkv, 0};
       vv = {v, c.S, hkv, 0};
@@ -1039,6 +1097,18 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     if (proj && pj->w_o && p == 1)
       gemm_xw(ctx, c.dtype, (const uint8_t*)o + (size_t)m * C * od * eb, od, pj->w_o, pj->hidden,
               (uint8_t*)pj->y + (size_t)m * C * pj->hidden * eb, pj->hidden, C, od, pj->hidden, cs);
+    // host rows: chunk m's output rows (final now at p == 1, after the return exchange at p > 1) leave at once
+    auto download_o = [&](cudaStream_t from) {
+      rec(ctx->ev_tmp, from);
+      wait(ctx->s_d2h, ctx->ev_tmp);
+      const size_t bo = (size_t)c.c * od * eb;
+      d2h_io(ctx, (uint8_t*)io->o + (size_t)m * bo, (const uint8_t*)o + (size_t)m * bo, bo);
+      if (io->lse) {
+        const size_t bl = (size_t)c.c * c.Hq * 4;
+        d2h_io(ctx, (uint8_t*)io->lse + (size_t)m * bl, (const uint8_t*)lse + (size_t)m * bl, bl);
+      }
+    };
+    if (io_p1) download_o(cs);
     if (p > 1) {
       // F10: all-to-all of O_m back to the sequence layout, then unpack into the caller's rows of slot m (on the comm
       // stream behind chunk m+1's exchange, so it overlaps chunk m+1's pairs)
@@ -1066,6 +1136,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
                                             cudaMemcpyDeviceToDevice, ctx->s_comm));
         ctx->stats.kernel_launches++;
       }
+      if (io) download_o(ctx->s_comm);
     }
   }
   ctx->stats.fetch_slots_highwater = std::max(ctx->stats.fetch_slots_highwater, high);
@@ -1331,7 +1402,7 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
 }
 
 void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, void* dq, void* dk, void* dv,
-              cudaStream_t cs, const Proj* pj = nullptr) {
+              cudaStream_t cs, const Proj* pj = nullptr, const HostIO* io = nullptr) {
   Nvtx nv("fpdt:backward");
   const int64_t C = c.C, u = c.u;
   const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
@@ -1354,10 +1425,19 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   ensure_events(ctx->ev_doff, u);
   ensure_events(ctx->ev_dqoff, u);
   ensure_events(ctx->ev_a2a, u);
+  if (io) ensure_events(ctx->ev_up, u);
   rec(ctx->ev_enter, cs);
   for (cudaStream_t s : {ctx->s_comm, ctx->s_h2d, ctx->s_d2h}) wait(s, ctx->ev_enter);
   HostLayout hl{};
   if (c.offload) hl = host_layout(c);
+  const bool io_p1 = io && p == 1;
+  if (io && io->upload_o) {
+    // o is not the saved forward's output: its device mirror is stale
+    h2d_io(ctx, const_cast<void*>(o), io->o, (size_t)c.s_local * c.Hq * d * eb);
+    rec(ctx->ev_tmp, ctx->s_h2d);
+    wait(cs, ctx->ev_tmp);
+    wait(ctx->s_comm, ctx->ev_tmp);
+  }
   const Residency R = make_residency(u, c.offload ? ctx->saved_res_kv : 0, c.offload ? ctx->saved_res_q : 0);
   uint8_t* resstore = (uint8_t*)ctx->bufs[B_RESSTORE].ptr;  // p > 1: the forward's resident head-layout chunks
   auto res_chunk = [&](int64_t m) { return resstore + (size_t)R.slot[(size_t)m] * C * hcomb * d * eb; };
@@ -1368,7 +1448,10 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   int64_t do_rows = c.S;
   int do_heads = hq, do_head0 = 0;
   uint8_t* gathered = nullptr;        // p > 1: [S or C][2hq][d] gathered (O, dO)
-  if (p == 1) {
+  if (io_p1) {
+    // host rows: D_i is formed at the first pair of query chunk i from its fetched dO_i (below); dO_i and q_i are
+    // fetched from the caller's host rows
+  } else if (p == 1) {
     FPDT_CHECK_LAUNCH(launch_bwd_preprocess_D(o, dout, c.dtype, c.S, hq, d, (int64_t)c.Hq * d, o_resid,
                                               (int64_t)hq * d, Dh, c.S, cs));
     ctx->stats.kernel_launches++;
@@ -1391,6 +1474,12 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
                       : R.q(m)   ? dores + (size_t)R.qslot[(size_t)m] * C * 2 * hq * d * eb
                                  : gathered + (size_t)(m & 1) * C * 2 * hq * d * eb;
       if (c.offload && !R.q(m) && m >= 2) wait(ctx->s_comm, ctx->ev_doff[m - 2]);
+      if (io) {
+        const size_t bo = (size_t)c.c * c.Hq * d * eb;
+        h2d_io(ctx, (uint8_t*)dout + (size_t)m * bo, (const uint8_t*)io->dout + (size_t)m * bo, bo);
+        rec(ctx->ev_up[(size_t)m], ctx->s_h2d);
+        wait(ctx->s_comm, ctx->ev_up[(size_t)m]);
+      }
       FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)o + (size_t)m * c.c * c.Hq * d * eb, c.c, c.Hq, d, p, eb,
                                              send, per_peer, (int64_t)2 * hq * d, 0, ctx->s_comm));
       FPDT_CHECK_LAUNCH(launch_pack_seq2head((const uint8_t*)dout + (size_t)m * c.c * c.Hq * d * eb, c.c, c.Hq, d, p,
@@ -1599,6 +1688,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
                   ? FPDT_BWD_Q_OUTER
                   : FPDT_BWD_KV_OUTER;
     if (proj) order = FPDT_BWD_KV_OUTER;  // the fused projection backward runs per final chunk j
+    if (io) order = FPDT_BWD_KV_OUTER;    // host rows: chunk j's gradients leave after outer iteration j
     KvFetch kvf(ctx, c, ctx->saved_fetch);
     if (kvf.leader_mode) order = FPDT_BWD_KV_OUTER;  // strategy B is implemented for the paper's loop order
     kvf.init_events(cs);
@@ -1616,6 +1706,14 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
     }
     int step = 0;
     std::vector<char> dq_started((size_t)u, 0);  // chunk i's dq partial already holds contributions (host store)
+    std::vector<char> d_done((size_t)u, 0);      // host rows, p == 1: D_i formed
+    // host-side source of q_i / dO_i: the store, or (host rows, p == 1) the caller's rows in the same layout
+    auto src_q = [&](int64_t i) -> const uint8_t* {
+      return io_p1 ? (const uint8_t*)io->q + (size_t)i * C * row_q : ctx->host + hl.q(i);
+    };
+    auto src_do = [&](int64_t i) -> const uint8_t* {
+      return io_p1 ? (const uint8_t*)io->dout + (size_t)i * C * row_q : ctx->host + hl.dO(i, u);
+    };
     for (int64_t j = 0; j < u; ++j) {
       const int ks = (int)(j & 1);
       if (p > 1 || proj) {
@@ -1667,9 +1765,9 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
         } else {
           // B4: fetch q_i, dO_i and (when it already holds contributions) the dq partial of chunk i
           wait(ctx->s_h2d, ctx->ev_q_free[sl]);
-          wait(ctx->s_h2d, ctx->ev_doff[i]);
-          h2d(ctx, qs[sl], ctx->host + hl.q(i), (size_t)C * row_q);
-          h2d(ctx, dos[sl], ctx->host + hl.dO(i, u), (size_t)C * row_q);
+          if (!io_p1) wait(ctx->s_h2d, ctx->ev_doff[i]);
+          h2d(ctx, qs[sl], src_q(i), (size_t)C * row_q);
+          h2d(ctx, dos[sl], src_do(i), (size_t)C * row_q);
           if (dq_started[i]) {
             wait(ctx->s_h2d, ctx->ev_dqoff[i]);
             h2d(ctx, dqs[sl], ctx->host + hl.dq(i, u), (size_t)C * hq * d * 4);
@@ -1677,6 +1775,14 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
           rec(ctx->ev_q_filled[sl], ctx->s_h2d);
           wait(cs, ctx->ev_q_filled[sl]);
           if (!dq_started[i]) FPDT_CHECK_CUDA(cudaMemsetAsync(dqs[sl], 0, (size_t)C * hq * d * 4, cs));
+          if (io_p1 && !d_done[i]) {
+            FPDT_CHECK_LAUNCH(launch_bwd_preprocess_D((const uint8_t*)o + (size_t)i * C * row_q, dos[sl], c.dtype, C,
+                                                      hq, d, (int64_t)hq * d,
+                                                      o_resid ? o_resid + (size_t)i * C * hq * d : nullptr,
+                                                      (int64_t)hq * d, Dh + i * C, c.S, cs));
+            ctx->stats.kernel_launches++;
+            d_done[i] = 1;
+          }
           qi = {qs[sl], C, hq, 0};
           doi = {dos[sl], C, hq, 0};
           dqi = dqs[sl];
@@ -1704,6 +1810,16 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       }
       send_back(j);  // dk_j, dv_j are final after the last inner iteration
       rec(ctx->ev_kv_free[ks], cs);
+      if (io) {
+        // host rows: chunk j's dq, dk, dv rows are final (p == 1: on the compute stream; p > 1: unpacked on the comm
+        // stream by send_back)
+        rec(ctx->ev_tmp, p == 1 ? cs : ctx->s_comm);
+        wait(ctx->s_d2h, ctx->ev_tmp);
+        const size_t bq = (size_t)c.c * c.Hq * d * eb, bkv = (size_t)c.c * c.Hkv * d * eb;
+        d2h_io(ctx, (uint8_t*)io->dq + (size_t)j * bq, (const uint8_t*)dq + (size_t)j * bq, bq);
+        d2h_io(ctx, (uint8_t*)io->dk + (size_t)j * bkv, (const uint8_t*)dk + (size_t)j * bkv, bkv);
+        d2h_io(ctx, (uint8_t*)io->dv + (size_t)j * bkv, (const uint8_t*)dv + (size_t)j * bkv, bkv);
+      }
     }
     }
   }
@@ -1886,7 +2002,7 @@ int fpdt_ctx_destroy(fpdt_ctx* ctx) {
     if (ctx->host_dkv) cudaFreeHost(ctx->host_dkv);
     if (ctx->host_kvall) cudaFreeHost(ctx->host_kvall);
     if (ctx->host_x) cudaFreeHost(ctx->host_x);
-    for (auto v : {&ctx->ev_off, &ctx->ev_doff, &ctx->ev_dqoff, &ctx->ev_dkvoff, &ctx->ev_a2a, &ctx->ev_xoff})
+    for (auto v : {&ctx->ev_off, &ctx->ev_doff, &ctx->ev_dqoff, &ctx->ev_dkvoff, &ctx->ev_a2a, &ctx->ev_xoff, &ctx->ev_up})
       for (auto e : *v) cudaEventDestroy(e);
     for (cudaEvent_t e : ctx->fixed_events())
       if (e) cudaEventDestroy(e);
@@ -1925,6 +2041,7 @@ int fpdt_attn_fwd(fpdt_ctx* ctx, const void* q, const void* k, const void* v, vo
     ctx->fwd_done = false;
     forward(ctx, c, q, k, v, o, lse, static_cast<cudaStream_t>(stream));
     ctx->saved_hidden = 0;
+    ctx->saved_hostio = false;
     ctx->saved = c;
     ctx->saved_q = q;
     ctx->saved_k = k;
@@ -1944,9 +2061,78 @@ int fpdt_attn_bwd(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void
     if (!ctx->fwd_done) fail(FPDT_ERR_STATE, "fpdt_attn_bwd without a preceding fpdt_attn_fwd on this context");
     if (!(c == ctx->saved)) fail(FPDT_ERR_STATE, "backward arguments differ from the saved forward's");
     if (ctx->saved_hidden) fail(FPDT_ERR_STATE, "the saved forward was fpdt_block_fwd: use fpdt_block_bwd");
+    if (ctx->saved_hostio) fail(FPDT_ERR_STATE, "the saved forward was fpdt_attn_fwd_host: use fpdt_attn_bwd_host");
     FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
     check_collective_args(ctx, 2, c, 0);
     backward(ctx, c, o, dout, dq, dk, dv, static_cast<cudaStream_t>(stream));
+  });
+}
+
+int fpdt_attn_fwd_host(fpdt_ctx* ctx, const void* q, const void* k, const void* v, void* o, float* lse,
+                       int64_t s_local, int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size,
+                       int world_size, int dtype, int offload, float softmax_scale, void* stream) {
+  return run([&] {
+    if (!ctx || !q || !k || !v || !o) fail(FPDT_ERR_ARG, "null pointer argument");
+    if (world_size != ctx->p) fail(FPDT_ERR_ARG, "world_size differs from the context's");
+    Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
+                           softmax_scale);
+    if (!c.offload) fail(FPDT_ERR_UNSUPPORTED, "fpdt_attn_fwd_host needs offload = 1 (per-chunk staging)");
+    if (ctx->res_kv || ctx->res_q) fail(FPDT_ERR_UNSUPPORTED, "fpdt_attn_fwd_host does not take a residency budget");
+    FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
+    if (!ctx->plan.empty()) {
+      if (ctx->plan_u != c.u) fail(FPDT_ERR_ARG, "sparsity plan has " + std::to_string(ctx->plan_u) + " chunks, the call " + std::to_string(c.u));
+      for (int64_t m = 0; m < c.u; ++m)
+        if (!ctx->plan[(size_t)(m * c.u + m)]) fail(FPDT_ERR_ARG, "sparsity plan drops a diagonal block");
+    }
+    check_collective_args(ctx, 5, c, 0);
+    const size_t bq = (size_t)s_local * n_q_heads * head_dim * c.eb, bkv = (size_t)s_local * n_kv_heads * head_dim * c.eb;
+    void* qd = dev(ctx, B_HQ, bq);
+    void* kd = dev(ctx, B_HK, bkv);
+    void* vd = dev(ctx, B_HV, bkv);
+    void* od = dev(ctx, B_HO, bq);
+    float* ld = lse ? (float*)dev(ctx, B_HLSE, (size_t)s_local * n_q_heads * 4) : nullptr;
+    HostIO io;
+    io.q = q; io.k = k; io.v = v; io.o = o; io.lse = lse;
+    ctx->saved_fetch = ctx->fetch_strategy;
+    ctx->saved_plan = ctx->plan;
+    ctx->saved_res_kv = ctx->saved_res_q = 0;
+    ctx->fwd_done = false;
+    forward(ctx, c, qd, kd, vd, od, ld, static_cast<cudaStream_t>(stream), nullptr, &io);
+    ctx->saved_hidden = 0;
+    ctx->saved = c;
+    ctx->saved_q = qd;
+    ctx->saved_k = kd;
+    ctx->saved_v = vd;
+    ctx->saved_hostio = true;
+    ctx->saved_host_q = q;
+    ctx->saved_host_o = o;
+    ctx->fwd_done = true;
+  });
+}
+
+int fpdt_attn_bwd_host(fpdt_ctx* ctx, const void* o, const void* dout, void* dq, void* dk, void* dv, int64_t s_local,
+                       int n_q_heads, int n_kv_heads, int head_dim, int causal, int64_t chunk_size, int world_size,
+                       int dtype, int offload, float softmax_scale, void* stream) {
+  return run([&] {
+    if (!ctx || !o || !dout || !dq || !dk || !dv) fail(FPDT_ERR_ARG, "null pointer argument");
+    if (world_size != ctx->p) fail(FPDT_ERR_ARG, "world_size differs from the context's");
+    Config c = make_config(s_local, n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
+                           softmax_scale);
+    if (!ctx->fwd_done) fail(FPDT_ERR_STATE, "fpdt_attn_bwd_host without a preceding fpdt_attn_fwd_host on this context");
+    if (!(c == ctx->saved)) fail(FPDT_ERR_STATE, "backward arguments differ from the saved forward's");
+    if (!ctx->saved_hostio) fail(FPDT_ERR_STATE, "the saved forward was not fpdt_attn_fwd_host: use fpdt_attn_bwd");
+    FPDT_CHECK_CUDA(cudaSetDevice(ctx->device));
+    check_collective_args(ctx, 6, c, 0);
+    const size_t bq = (size_t)s_local * n_q_heads * head_dim * c.eb, bkv = (size_t)s_local * n_kv_heads * head_dim * c.eb;
+    void* od = ctx->bufs[B_HO].ptr;
+    void* dod = c.p > 1 ? dev(ctx, B_HDO, bq) : nullptr;  // p == 1 fetches dO_i from the caller's rows directly
+    void* dqd = dev(ctx, B_HDQ, bq);
+    void* dkd = dev(ctx, B_HDK, bkv);
+    void* dvd = dev(ctx, B_HDV, bkv);
+    HostIO io;
+    io.q = ctx->saved_host_q; io.dout = dout; io.o = const_cast<void*>(o); io.dq = dq; io.dk = dk; io.dv = dv;
+    io.upload_o = o != ctx->saved_host_o;
+    backward(ctx, c, od, dod, dqd, dkd, dvd, static_cast<cudaStream_t>(stream), nullptr, &io);
   });
 }
 
@@ -1992,6 +2178,7 @@ int fpdt_block_fwd(fpdt_ctx* ctx, const void* x, const void* w_qkv, const void* 
     ctx->saved = c;
     ctx->saved_q = ctx->saved_k = ctx->saved_v = nullptr;
     ctx->saved_hidden = hidden;
+    ctx->saved_hostio = false;
     ctx->saved_has_wo = w_o != nullptr;
     ctx->fwd_done = true;
   });

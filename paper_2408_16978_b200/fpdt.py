@@ -26,7 +26,7 @@ EXPORTED = ("fpdt_get_unique_id", "fpdt_ctx_create", "fpdt_ctx_destroy", "fpdt_a
             "fpdt_group_create", "fpdt_group_destroy", "fpdt_ctx_create_local", "fpdt_set_sparsity",
             "fpdt_set_residency", "fpdt_set_bwd_order", "fpdt_block_fwd", "fpdt_block_bwd", "fpdt_bwd_host_bytes",
             "fpdt_kernel_gaps", "fpdt_exchange_time", "fpdt_set_debug_checks", "fpdt_set_fetch_strategy",
-            "fpdt_set_hidden_offload")
+            "fpdt_set_hidden_offload", "fpdt_attn_fwd_host", "fpdt_attn_bwd_host")
 # include/fpdt_diag.h (libfpdt_diag.so: micro-benchmarks and direct kernel launches, not on the FPDT path)
 DIAG_EXPORTED = ("fpdt_selftest_umma", "fpdt_selftest_perf", "fpdt_selftest_softmax", "fpdt_selftest_reduce",
                  "fpdt_selftest_pair", "fpdt_debug_relayout", "fpdt_debug_pair")
@@ -42,7 +42,8 @@ class Stats(ctypes.Structure):
     _fields_ = [("bytes_h2d", c_int64), ("bytes_d2h", c_int64), ("bytes_a2a", c_int64),
                 ("kernel_launches", c_int64), ("attn_launches", c_int64), ("fetch_slots_highwater", c_int64),
                 ("host_arena_bytes", c_int64), ("device_bytes", c_int64), ("bwd_order", c_int64),
-                ("host_dkv_bytes", c_int64), ("stress_sleeps", c_int64)]
+                ("host_dkv_bytes", c_int64), ("stress_sleeps", c_int64), ("bytes_io_h2d", c_int64),
+                ("bytes_io_d2h", c_int64)]
 
     def as_dict(self):
         return {k: getattr(self, k) for k, _ in self._fields_}
@@ -68,6 +69,10 @@ def _declare(lib):
     lib.fpdt_attn_bwd.argtypes = [P, P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int64, c_int, c_int, c_int,
                                   c_float, P]
     lib.fpdt_attn_bwd.restype = c_int
+    for name in ("fpdt_attn_fwd_host", "fpdt_attn_bwd_host"):
+        getattr(lib, name).argtypes = [P, P, P, P, P, P, c_int64, c_int, c_int, c_int, c_int, c_int64, c_int, c_int,
+                                       c_int, c_float, P]
+        getattr(lib, name).restype = c_int
     lib.fpdt_last_error.argtypes = []
     lib.fpdt_last_error.restype = ctypes.c_char_p
     lib.fpdt_global_token.argtypes = [c_int64, c_int64, c_int, c_int]
@@ -280,6 +285,24 @@ def fpdt_attn_bwd(ctx: FPDTContext, o, dout, dq, dk, dv, s_local: int, n_q_heads
     _check(lib().fpdt_attn_bwd(ctx.handle, _ptr(o), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), s_local, n_q_heads,
                                n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload, softmax_scale,
                                _stream(stream)))
+
+
+def fpdt_attn_fwd_host(ctx: FPDTContext, q, k, v, o, lse, s_local: int, n_q_heads: int, n_kv_heads: int,
+                       head_dim: int, causal: int, chunk_size: int, world_size: int, dtype: int, offload: int,
+                       softmax_scale: float = 0.0, stream=None):
+    """q, k, v, o, lse: pinned host tensors (include/fpdt.h fpdt_attn_fwd_host)."""
+    _check(lib().fpdt_attn_fwd_host(ctx.handle, _ptr(q), _ptr(k), _ptr(v), _ptr(o), _ptr(lse), s_local, n_q_heads,
+                                    n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
+                                    softmax_scale, _stream(stream)))
+
+
+def fpdt_attn_bwd_host(ctx: FPDTContext, o, dout, dq, dk, dv, s_local: int, n_q_heads: int, n_kv_heads: int,
+                       head_dim: int, causal: int, chunk_size: int, world_size: int, dtype: int, offload: int,
+                       softmax_scale: float = 0.0, stream=None):
+    """o, dout, dq, dk, dv: pinned host tensors (include/fpdt.h fpdt_attn_bwd_host)."""
+    _check(lib().fpdt_attn_bwd_host(ctx.handle, _ptr(o), _ptr(dout), _ptr(dq), _ptr(dk), _ptr(dv), s_local,
+                                    n_q_heads, n_kv_heads, head_dim, causal, chunk_size, world_size, dtype, offload,
+                                    softmax_scale, _stream(stream)))
 
 
 def fpdt_block_fwd(ctx: FPDTContext, x, w_qkv, o, lse, s_local: int, hidden: int, n_q_heads: int, n_kv_heads: int,

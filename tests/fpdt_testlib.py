@@ -17,24 +17,28 @@ def rel_err(x, ref) -> float:
     return float(np.abs(x - ref).max() / max(np.abs(ref).max(), 1e-30))
 
 
-def run_cuda(x: dict, chunk: int, dtype: str, offload: int, ctx=None, want_grad: bool = True):
-    """x: numpy q, k, v, do (bf16-representable fp32 values), sequence layout, world_size 1."""
+def run_cuda(x: dict, chunk: int, dtype: str, offload: int, ctx=None, want_grad: bool = True, host_io: bool = False):
+    """x: numpy q, k, v, do (bf16-representable fp32 values), sequence layout, world_size 1.
+    host_io: every tensor in pinned host memory, through fpdt_attn_fwd_host / fpdt_attn_bwd_host."""
     from paper_2408_16978_b200 import fpdt
     tdt = torch.bfloat16 if dtype == "bf16" else torch.float32
-    q, k, v, do = (torch.tensor(x[n]).to(tdt).cuda().contiguous() for n in ("q", "k", "v", "do"))
+    place = (lambda t: t.pin_memory()) if host_io else (lambda t: t.cuda())
+    q, k, v, do = (place(torch.tensor(x[n]).to(tdt).contiguous()) for n in ("q", "k", "v", "do"))
     S, Hq, d = q.shape
     Hkv = k.shape[1]
     own = ctx is None
     if own:
         ctx = fpdt.FPDTContext()
-    o = torch.empty_like(q)
-    lse = torch.empty(S, Hq, dtype=torch.float32, device="cuda")
+    empty = (lambda t: torch.empty_like(t).pin_memory()) if host_io else torch.empty_like
+    o = empty(q)
+    lse = empty(torch.empty(S, Hq, dtype=torch.float32, device=q.device))
     code = fpdt.dtype_code(tdt)
-    fpdt.fpdt_attn_fwd(ctx, q, k, v, o, lse, S, Hq, Hkv, d, 1, chunk, 1, code, offload)
+    fwd, bwd = (fpdt.fpdt_attn_fwd_host, fpdt.fpdt_attn_bwd_host) if host_io else (fpdt.fpdt_attn_fwd, fpdt.fpdt_attn_bwd)
+    fwd(ctx, q, k, v, o, lse, S, Hq, Hkv, d, 1, chunk, 1, code, offload)
     out = {"o": o, "lse": lse}
     if want_grad:
-        dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
-        fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, S, Hq, Hkv, d, 1, chunk, 1, code, offload)
+        dq, dk, dv = empty(q), empty(k), empty(v)
+        bwd(ctx, o, do, dq, dk, dv, S, Hq, Hkv, d, 1, chunk, 1, code, offload)
         out.update(dq=dq, dk=dk, dv=dv)
     torch.cuda.synchronize()
     res = {n: t.float().cpu().numpy() for n, t in out.items()}

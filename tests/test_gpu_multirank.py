@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 
 def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None, residency=None, bwd_order=None,
-              stats=None, fetch=None, debug_checks=False) -> dict:
+              stats=None, fetch=None, debug_checks=False, host_io=False) -> dict:
     """Shard the global inputs x by the rank-ordinal contract, run fwd+bwd on p local ranks, unshard."""
     from paper_2408_16978_b200 import fpdt
     S, Hq, d = x["q"].shape
@@ -36,10 +36,12 @@ def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None, resi
             torch.cuda.set_device(0)
             stream = torch.cuda.Stream()
             with torch.cuda.stream(stream):
-                q, k, v, do = (torch.tensor(x[n][rows[r]]).to(tdt).cuda().contiguous() for n in ("q", "k", "v", "do"))
-                o = torch.empty_like(q)
-                lse = torch.empty(s_local, Hq, dtype=torch.float32, device="cuda")
-                dq, dk, dv = torch.empty_like(q), torch.empty_like(k), torch.empty_like(v)
+                place = (lambda t: t.pin_memory()) if host_io else (lambda t: t.cuda())
+                q, k, v, do = (place(torch.tensor(x[n][rows[r]]).to(tdt).contiguous()) for n in ("q", "k", "v", "do"))
+                empty = (lambda t: torch.empty_like(t).pin_memory()) if host_io else torch.empty_like
+                o = empty(q)
+                lse = empty(torch.empty(s_local, Hq, dtype=torch.float32, device=q.device))
+                dq, dk, dv = empty(q), empty(k), empty(v)
             stream.synchronize()
             ctx = fpdt.FPDTContext(p, r, group=group) if p > 1 else fpdt.FPDTContext()
             if keep is not None:
@@ -52,8 +54,10 @@ def run_group(x: dict, p: int, C: int, dtype: str, offload: int, keep=None, resi
                 ctx.set_fetch_strategy(fetch)
             if debug_checks:
                 ctx.set_debug_checks(True)
-            fpdt.fpdt_attn_fwd(ctx, q, k, v, o, lse, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
-            fpdt.fpdt_attn_bwd(ctx, o, do, dq, dk, dv, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
+            fwd, bwd = ((fpdt.fpdt_attn_fwd_host, fpdt.fpdt_attn_bwd_host) if host_io
+                        else (fpdt.fpdt_attn_fwd, fpdt.fpdt_attn_bwd))
+            fwd(ctx, q, k, v, o, lse, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
+            bwd(ctx, o, do, dq, dk, dv, s_local, Hq, Hkv, d, 1, C, p, code, offload, 0.0, stream)
             stream.synchronize()
             for n, t in (("o", o), ("lse", lse), ("dq", dq), ("dk", dk), ("dv", dv)):
                 out[n][rows[r]] = t.float().cpu().numpy()
