@@ -271,7 +271,10 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
       tc_fence_after();
       if constexpr (C::kSepP) {
         // per key tile j: S_t(j+1) as soon as the softmax warps have read S_t(j) out of TMEM; PV_t(j) when P_t(j)
-        // is in the shared P buffer (the softmax warps of the other tile wait for PV_t(j) before overwriting it)
+        // is in the shared P buffer (the softmax warps of the other tile wait for PV_t(j) before overwriting it).
+        // (Measured, not kept: the order S_0(j+1), PV_1(j-1), S_1(j+1), PV_0(j), which serves each warpgroup's events
+        // in arrival order: same speed, 910-926 vs 911-927 TFLOP/s, tools/round1/gpu_ab_fwdorder.sh — the S tiles
+        // were never late enough to matter; the exponential phases, 2.0 elem/clk per warp, set the pace.)
         mbar_wait(smem_u32(&bar_k[0]), 0);
         tc_fence_after();
         issue_S(0, 0);
