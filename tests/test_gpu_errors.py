@@ -30,6 +30,15 @@ def test_status_codes():
         fpdt.fpdt_attn_fwd(ctx, _t(1024, 3, 64), _t(1024, 2, 64), _t(1024, 2, 64), _t(1024, 3, 64), None,
                            1024, 3, 2, 64, 1, 256, 1, 0, 1)
     assert e.value.code == fpdt.FPDT_ERR_DIVISIBILITY
+    with pytest.raises(fpdt.FpdtError) as e:      # empty sequence
+        fpdt.fpdt_attn_fwd(ctx, q, k, v, o, None, 0, 2, 2, 64, 1, 256, 1, 0, 1)
+    assert e.value.code == fpdt.FPDT_ERR_ARG
+    with pytest.raises(fpdt.FpdtError) as e:      # empty sequence, host-memory form
+        fpdt.fpdt_attn_fwd_host(ctx, q.cpu(), k.cpu(), v.cpu(), o.cpu(), None, 0, 2, 2, 64, 1, 256, 1, 0, 1)
+    assert e.value.code == fpdt.FPDT_ERR_ARG
+    with pytest.raises(fpdt.FpdtError) as e:      # null pointer
+        fpdt.fpdt_attn_fwd(ctx, None, k, v, o, None, 1024, 2, 2, 64, 1, 256, 1, 0, 1)
+    assert e.value.code == fpdt.FPDT_ERR_ARG
     with pytest.raises(fpdt.FpdtError) as e:      # non-causal not supported
         fpdt.fpdt_attn_fwd(ctx, q, k, v, o, None, 1024, 2, 2, 64, 0, 256, 1, 0, 1)
     assert e.value.code == fpdt.FPDT_ERR_UNSUPPORTED
