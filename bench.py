@@ -357,6 +357,8 @@ def run_ours(args):
         "vs_baseline": None, "dtype": "bf16", "data": "synthetic (seeded counter-based generator, normal)",
         "tflops_per_gpu": tflops_gpu,
         "frac_of_peak": tflops_gpu / sustained,
+        # MFU-style "model FLOPs": 12d per causal pair per q-head, no backward recompute of Q K^T
+        "model_tflops_per_gpu": tflops_gpu * 12 / 14,
         "config": {"workload": W["name"], "S": S, "heads_q": Hq, "heads_kv": Hkv, "head_dim": d, "chunk": C,
                    "chunks": S // C, "s_local": s_local, "offload": offload, "causal": 1,
                    "parallelism": f"ulysses-sp{world}", "l2": "inputs 2.7 GB/tensor >> 126 MB L2, no flush",
