@@ -19,6 +19,11 @@
 // (an FA4-style polynomial offload of a fraction of them measured slower here: one pair in 4 / 8 / 16 on the FMA pipe
 // gave 848-858 / 868 / 871 TFLOP/s against 872-875 all on MUFU, C = 64K, 32 x 80 diagonal pair).
 //
+// Launched in clusters of two CTAs (adjacent key tiles of one head, same query-tile walk) that multicast the halves of
+// every Q and dO tile to each other (template flag MC, see the kernel): 877 vs 862 TFLOP/s on the d = 80 diagonal pair,
+// 859 vs 846 on a full pair (tools/gpu_ab.sh, same box).  Measured along the way (timing-only builds, results wrong):
+// no dQ reduce-add 1000 / 1011, no Q / dO loads 944 / 959, neither 1038 / 1075 TFLOP/s; Q / dO through the
+// load/store unit (cp.async by two warps) instead of TMA 574-695 (slower).
 // Warps (512 threads = 4 warpgroups, registers rebalanced with setmaxnreg):
 //   WG0 (0-3)   softmax-gradient, query columns [0,64)   (thread = key row = TMEM lane); final dK    168 regs
 //   WG1 (4-7)   softmax-gradient, query columns [64,128)                                ; final dV    168 regs
@@ -80,6 +85,7 @@ struct PipeCfg {
 
 struct TmapSet {
   CUtensorMap q, k, v, o;
+  CUtensorMap q64, o64;  // 64-row boxes: each CTA of a cluster pair multicasts one half of a Q / dO tile
   CUtensorMap dq32h, dq16h;  // fp32 dq_acc, 64-row boxes: 32 columns (128B swizzle) / 16 columns (64B swizzle)
 };
 
@@ -100,6 +106,22 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
                : "memory");
 }
+// TMA tile load multicast to the CTAs of `mask` (same shared-memory offset and mbarrier offset in each)
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2,
+                                               uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6, %7;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "h"(mask), "l"(policy)
+      : "memory");
+}
+// arrive on the mbarrier at the same offset in every CTA of `mask` when this thread's issued MMAs complete
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   bar),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -112,7 +134,12 @@ __device__ __forceinline__ uint32_t pack_f16x2(float lo, float hi) {
   return r;
 }
 
-template <int D>
+// MC: launched in clusters of two CTAs on adjacent key tiles of one head, which walk the same query tiles; each CTA
+// loads one 64-row half of every Q and dO tile and multicasts it into both, so each SM's TMA engine issues half of the
+// loads (it also carries the dQ reduce-adds, and the loads queued behind them were late: skipping the Q or the dO
+// loads in a timing-only build ran the pair at 946 / 901 instead of 850 TFLOP/s).  A stage is refilled once both CTAs
+// have consumed it (the MMA commit arrives on the empty barrier of both).
+template <int D, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdArgs a) {
   using T = Tile<D>;
@@ -136,10 +163,13 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
   const int g = blockIdx.y;
   const int G = a.G;
   const int64_t kv_base = a.kv_pos0 + (int64_t)kt * 128;
+  const uint32_t crank = MC ? cluster_ctarank() : 0;
   int qt_first = 0;
   const int n_qt_total = a.n_q_rows / 128;
   if (a.causal) {
-    const int64_t rel = kv_base - a.q_pos0;  // first query tile that can see this key tile
+    // first query tile that can see this key tile (MC: the pair's first key tile; the second CTA's first tile of a
+    // diagonal pair is then fully masked, P = 0)
+    const int64_t rel = a.kv_pos0 + (int64_t)(MC ? (kt & ~1) : kt) * 128 - a.q_pos0;
     if (rel > 0) qt_first = (int)(rel / 128);
     if (qt_first > n_qt_total) qt_first = n_qt_total;
   }
@@ -155,11 +185,11 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
     mbar_init(bar(B_KV), 1);
     for (int s = 0; s < QS; ++s) {
       mbar_init(bar(B_QF + s), 1);
-      mbar_init(bar(B_QE + s), 1);
+      mbar_init(bar(B_QE + s), MC ? 2 : 1);
     }
     for (int s = 0; s < OS; ++s) {
       mbar_init(bar(B_OF + s), 1);
-      mbar_init(bar(B_OE + s), 1);
+      mbar_init(bar(B_OE + s), MC ? 2 : 1);
     }
     mbar_init(bar(B_S), 1);
     mbar_init(bar(B_SFREE), 256);
@@ -176,6 +206,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (MC) cluster_sync();  // the partner's barriers exist before any multicast load or commit reaches them
   const uint32_t tmem = *tmem_slot;
 
   if (warp >= 12) {
@@ -197,12 +228,26 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
           const uint32_t fq = bar(B_QF + qs);
           const uint32_t stats = base + C::oStats + qs * C::kStats;
           mbar_expect_tx(fq, C::TB + 1024);
-          T::load(base + C::oQ + qs * C::TB, &tm.q, fq, a.q.head0 + h, qrow, pol_q);
+          if constexpr (MC) {
+#pragma unroll
+            for (int at = 0; at < T::kAtoms; ++at)
+              tma_load_3d_mc(base + C::oQ + qs * C::TB + at * T::kAtomBytes + crank * 64 * T::kRowBytes, &tm.q64, fq,
+                             at * T::kAtomCols, a.q.head0 + h, qrow + 64 * (int)crank, 3, pol_q);
+          } else {
+            T::load(base + C::oQ + qs * C::TB, &tm.q, fq, a.q.head0 + h, qrow, pol_q);
+          }
           bulk_load(stats, a.lse2 + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, fq);
           bulk_load(stats + 512, a.Dstat + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, fq);
           if (n >= OS) mbar_wait(bar(B_OE + os), ((n / OS) - 1) & 1);
           mbar_expect_tx(bar(B_OF + os), C::TB);
-          T::load(base + C::oO + os * C::TB, &tm.o, bar(B_OF + os), a.dout.head0 + h, qrow, pol_q);
+          if constexpr (MC) {
+#pragma unroll
+            for (int at = 0; at < T::kAtoms; ++at)
+              tma_load_3d_mc(base + C::oO + os * C::TB + at * T::kAtomBytes + crank * 64 * T::kRowBytes, &tm.o64,
+                             bar(B_OF + os), at * T::kAtomCols, a.dout.head0 + h, qrow + 64 * (int)crank, 3, pol_q);
+          } else {
+            T::load(base + C::oO + os * C::TB, &tm.o, bar(B_OF + os), a.dout.head0 + h, qrow, pol_q);
+          }
         }
       }
     } else if (warp == 13) {
@@ -256,7 +301,8 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             mma_ts(tdV, tdP + 64 * (kk >> 2) + (kk & 3) * 8, T::desc_mn(sO(n), kk), idG, (n > 0 || kk > 0));
-          mma_commit(bar(B_OE + n % OS));  // dO_n consumed (dP_n precedes dV_n)
+          if constexpr (MC) mma_commit_mc(bar(B_OE + n % OS), 3);  // dO_n consumed (dP_n precedes dV_n), both CTAs
+          else mma_commit(bar(B_OE + n % OS));
           // dK += dS^T Q_n   (A = dS^T in TMEM); first, so that Q_n is released early
           mbar_wait(bar(B_DS), n & 1);
           TRACE(5, n);
@@ -264,7 +310,8 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             mma_ts(tdK, tdP + 64 * (kk >> 2) + 32 + (kk & 3) * 8, T::desc_mn(sQ(n), kk), idG, (n > 0 || kk > 0));
-          mma_commit(bar(B_QE + n % QS));  // Q_n consumed
+          if constexpr (MC) mma_commit_mc(bar(B_QE + n % QS), 3);  // Q_n consumed
+          else mma_commit(bar(B_QE + n % QS));
           if (more) issue_dP(n + 1);
           // dQ_n = dS K   (A = the dS smem tile, MN-major)
           if (n > 0) {
@@ -514,6 +561,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // no CTA leaves while its partner may still multicast into it or arrive on it
   if (warp == 13) tmem_dealloc<512>(tmem);
 #undef TRACE
 }
@@ -522,7 +570,11 @@ template <int D>
 int launch_pipe(const BwdArgs& a, cudaStream_t s) {
   using C = PipeCfg<D>;
   TmapSet tm;
+  constexpr uint32_t kAtomCols = Tile<D>::kAtomCols;
+  constexpr CUtensorMapSwizzle kSw = D == 80 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B;
   bool ok = make_tile_tmap<D>(&tm.q, a.q.base, a.q.rows, a.q.heads);
+  ok &= make_tmap_rows_heads_dim(&tm.q64, a.q.base, a.q.rows, a.q.heads, D, kAtomCols, 64, kSw);
+  ok &= make_tmap_rows_heads_dim(&tm.o64, a.dout.base, a.dout.rows, a.dout.heads, D, kAtomCols, 64, kSw);
   ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
   ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
   ok &= make_tile_tmap<D>(&tm.o, a.dout.base, a.dout.rows, a.dout.heads);
@@ -531,8 +583,29 @@ int launch_pipe(const BwdArgs& a, cudaStream_t s) {
   ok &= make_tmap_f32_head_major(&tm.dq16h, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 16, 64,
                                  CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return -1;
-  if (int e = set_max_dynamic_smem((const void*)attn_bwd_pipe_kernel<D>, C::kSmem)) return e;
-  attn_bwd_pipe_kernel<D><<<dim3(a.n_kv_rows / 128, a.hq / a.G), kThreads, C::kSmem, s>>>(tm, a);
+  const dim3 grid(a.n_kv_rows / 128, a.hq / a.G);
+#ifndef FPDT_BWD_MC
+#define FPDT_BWD_MC 1
+#endif
+  if (FPDT_BWD_MC && grid.x % 2 == 0) {
+    if (int e = set_max_dynamic_smem((const void*)attn_bwd_pipe_kernel<D, true>, C::kSmem)) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_pipe_kernel<D, true>, tm, a)) return (int)e;
+    return (int)cudaGetLastError();
+  }
+  if (int e = set_max_dynamic_smem((const void*)attn_bwd_pipe_kernel<D, false>, C::kSmem)) return e;
+  attn_bwd_pipe_kernel<D, false><<<grid, kThreads, C::kSmem, s>>>(tm, a);
   return (int)cudaGetLastError();
 }
 

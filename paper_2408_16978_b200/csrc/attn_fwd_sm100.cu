@@ -118,8 +118,11 @@ __device__ __forceinline__ float2 ex2_poly2(float2 x) {
                      __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
 }
 
-// (Measured and not kept: the MUFU exponentials as ex2.approx.f16x2 on f16-rounded arguments, twice the MUFU rate
-// but more instructions: 924 vs 956 TFLOP/s on the d = 80 pair.)
+// (Measured and not kept: the MUFU exponentials as ex2.approx.f16x2 on f16-rounded arguments (ptxas splits it into two
+// MUFU.EX2.F16 and a PRMT, no faster per element than MUFU.EX2): with a conversion back to bf16, 924 vs 956 TFLOP/s on
+// the d = 80 pair; with fp16 P and an fp16 PV product (V converted in shared memory by the idle warps), 844 vs 954
+// (round 2, tools/gpu_ab.sh) — more accurate (lse error 2x lower, dQ on drift32 3.4e-3 vs 8.3e-3) but slower.  A
+// mixed fp16 x bf16 kind::f16 MMA is an illegal instruction.)
 
 // P = exp2(x*sl2 - mb) for the 128 columns of a row, packed to bf16 and stored to TMEM columns [tS, tS+64); returns
 // the sum of the fp32 values when kSum (else 0).  kEvery > 0: every kEvery-th pair on the FMA pipe.

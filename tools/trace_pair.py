@@ -17,6 +17,7 @@ H = int(sys.argv[3]) if len(sys.argv) > 3 else 32
 d = int(sys.argv[4]) if len(sys.argv) > 4 else 80
 cta = int(sys.argv[5]) if len(sys.argv) > 5 else 0
 kern = int(sys.argv[6]) if len(sys.argv) > 6 else 1
+causal = int(os.environ.get("CAUSAL", "1"))  # 0: a full (off-diagonal) pair
 lib = _lib.load_diag()
 torch.manual_seed(0)
 bf = torch.bfloat16
@@ -33,9 +34,9 @@ P = lambda t: ctypes.c_void_p(t.data_ptr()) if t is not None else None
 
 def launch(tr):
     if which == "fwd":
-        rc = lib.fpdt_debug_pair(0, d, 1, P(q), P(k), P(v), None, None, None, P(o), P(lse), None, C, H, H, tr, cta, None)
+        rc = lib.fpdt_debug_pair(0, d, causal, P(q), P(k), P(v), None, None, None, P(o), P(lse), None, C, H, H, tr, cta, None)
     else:
-        rc = lib.fpdt_debug_pair(kern, d, 1, P(q), P(k), P(v), P(do), P(lse2), P(Dst), P(dq), P(dk), P(dv), C, H, H, tr,
+        rc = lib.fpdt_debug_pair(kern, d, causal, P(q), P(k), P(v), P(do), P(lse2), P(Dst), P(dq), P(dk), P(dv), C, H, H, tr,
                                  cta, None)
     assert rc == 0, rc
 
@@ -50,8 +51,8 @@ for _ in range(3):
 e1.record()
 torch.cuda.synchronize()
 ms = e0.elapsed_time(e1) / 3
-fl = (4 if which == "fwd" else 10) * d * H * C * (C + 1) / 2
-print(f"{which} pair C={C} H={H} d={d} kernel={kern}: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s")
+fl = (4 if which == "fwd" else 10) * d * H * C * ((C + 1) / 2 if causal else C)
+print(f"{which} {'pair' if causal else 'full pair'} C={C} H={H} d={d} kernel={kern}: {ms:.3f} ms  {fl / ms / 1e9:.1f} TFLOP/s")
 if len(sys.argv) > 7 and sys.argv[7] == "x":
     sys.exit(0)
 launch(ctypes.c_void_p(trace.data_ptr()))
