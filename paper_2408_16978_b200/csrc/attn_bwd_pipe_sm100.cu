@@ -23,7 +23,9 @@
 // every Q and dO tile to each other (template flag MC, see the kernel): 877 vs 862 TFLOP/s on the d = 80 diagonal pair,
 // 859 vs 846 on a full pair (tools/gpu_ab.sh, same box).  Measured along the way (timing-only builds, results wrong):
 // no dQ reduce-add 1000 / 1011, no Q / dO loads 944 / 959, neither 1038 / 1075 TFLOP/s; Q / dO through the
-// load/store unit (cp.async by two warps) instead of TMA 574-695 (slower).
+// load/store unit (cp.async by two warps) instead of TMA 574-695 (slower); each CTA of the pair reduce-adding only its
+// 64 query rows of the pair's summed dQ partials, the other 64 rows sent to the partner with st.shared::cluster (DSMEM)
+// 556-562 (the remote stores move ~4 B/clk/SM; parity-green, not kept).
 // Warps (512 threads = 4 warpgroups, registers rebalanced with setmaxnreg):
 //   WG0 (0-3)   softmax-gradient, query columns [0,64)   (thread = key row = TMEM lane); final dK    168 regs
 //   WG1 (4-7)   softmax-gradient, query columns [64,128)                                ; final dV    168 regs
