@@ -106,7 +106,8 @@ struct Cfg {
 };
 
 struct TmapSet {
-  CUtensorMap q, k, v, o, dq64, dq16;  // dq boxes: [64 rows][64 cols] and [64 rows][16 cols] fp32, no swizzle
+  CUtensorMap q, k, v, o, dq64, dq16;
+  CUtensorMap qh, oh;  // half-tile boxes (BQ / 2 rows): each CTA of a cluster pair multicasts one half  // dq boxes: [64 rows][64 cols] and [64 rows][16 cols] fp32, no swizzle
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -125,6 +126,21 @@ __device__ __forceinline__ void bulk_load(uint32_t dst, const void* src, uint32_
                "l"(reinterpret_cast<uint64_t>(src)), "r"(bytes), "r"(bar)
                : "memory");
 }
+// TMA tile load multicast to the CTAs of `mask` (same shared-memory offset and mbarrier offset in each)
+__device__ __forceinline__ void tma_load_3d_mc(uint32_t dst, const CUtensorMap* m, uint32_t bar, int c0, int c1, int c2,
+                                               uint16_t mask, uint64_t policy) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cluster.global.tile.mbarrier::complete_tx::bytes.multicast::cluster"
+      ".L2::cache_hint [%0], [%1, {%2, %3, %4}], [%5], %6, %7;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(c0), "r"(c1), "r"(c2), "r"(bar), "h"(mask), "l"(policy)
+      : "memory");
+}
+__device__ __forceinline__ void mma_commit_mc(uint32_t bar, uint16_t mask) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64 [%0], %1;" ::"r"(
+                   bar),
+               "h"(mask)
+               : "memory");
+}
 __device__ __forceinline__ void bulk_commit() { asm volatile("cp.async.bulk.commit_group;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait_read0() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
 __device__ __forceinline__ void bulk_wait0() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
@@ -138,7 +154,9 @@ __device__ __forceinline__ void sts32(uint32_t addr, float v) {
   asm volatile("st.shared.f32 [%0], %1;" ::"r"(addr), "f"(v) : "memory");
 }
 
-template <int D>
+// MC: clusters of two CTAs on adjacent key tiles that walk the same query tiles and multicast the halves of every Q and
+// dO tile into each other (as in attn_bwd_pipe_sm100.cu)
+template <int D, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ BwdArgs a) {
   using C = Cfg<D>;
@@ -162,10 +180,13 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
   const int g = blockIdx.y;
   const int G = a.G;
   const int64_t kv_base = a.kv_pos0 + (int64_t)kt * 128;
+  const uint32_t crank = MC ? cluster_ctarank() : 0;
   int qt_first = 0;
   const int n_qt_total = a.n_q_rows / BQ;
   if (a.causal) {
-    const int64_t rel = kv_base - a.q_pos0;  // first query tile that can see this key tile
+    // first query tile that can see this key tile (MC: the pair's first key tile; the second CTA's first tiles of a
+    // diagonal pair are then fully masked, P = 0)
+    const int64_t rel = a.kv_pos0 + (int64_t)(MC ? (kt & ~1) : kt) * 128 - a.q_pos0;
     if (rel > 0) qt_first = (int)(rel / BQ);
     if (qt_first > n_qt_total) qt_first = n_qt_total;
   }
@@ -181,11 +202,11 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
     mbar_init(bar(B_KV), 1);
     for (int s = 0; s < QS; ++s) {
       mbar_init(bar(B_QF + s), 1);
-      mbar_init(bar(B_QE + s), 1);
+      mbar_init(bar(B_QE + s), MC ? 2 : 1);
     }
     for (int s = 0; s < OS; ++s) {
       mbar_init(bar(B_OF + s), 1);
-      mbar_init(bar(B_OE + s), 1);
+      mbar_init(bar(B_OE + s), MC ? 2 : 1);
     }
     mbar_init(bar(B_S), 1);
     mbar_init(bar(B_SFREE), 256);
@@ -204,6 +225,7 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (MC) cluster_sync();  // the partner's barriers exist before any multicast load or commit reaches them
   const uint32_t tmem = *tmem_slot;
   const uint32_t sKH = base + C::oKH;
 
@@ -226,12 +248,26 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
           const uint32_t fq = bar(B_QF + qs);
           const uint32_t stats = base + C::oStats + qs * C::kStats;
           mbar_expect_tx(fq, TQ::kBytes + C::kStats);
-          TQ::load(base + C::oQ + qs * TQ::kBytes, &tm.q, fq, a.q.head0 + h, qrow, pol_q);
+          if constexpr (MC) {
+#pragma unroll
+            for (int at = 0; at < D / TQ::kAC; ++at)
+              tma_load_3d_mc(base + C::oQ + qs * TQ::kBytes + at * TQ::kAtom + crank * (BQ / 2) * TQ::kAC * 2, &tm.qh,
+                             fq, at * TQ::kAC, a.q.head0 + h, qrow + (BQ / 2) * (int)crank, 3, pol_q);
+          } else {
+            TQ::load(base + C::oQ + qs * TQ::kBytes, &tm.q, fq, a.q.head0 + h, qrow, pol_q);
+          }
           bulk_load(stats, a.lse2 + (int64_t)h * a.stat_ld + (int64_t)qt * BQ, BQ * 4, fq);
           bulk_load(stats + BQ * 4, a.Dstat + (int64_t)h * a.stat_ld + (int64_t)qt * BQ, BQ * 4, fq);
           if (n >= OS) mbar_wait(bar(B_OE + os), ((n / OS) - 1) & 1);
           mbar_expect_tx(bar(B_OF + os), TQ::kBytes);
-          TQ::load(base + C::oO + os * TQ::kBytes, &tm.o, bar(B_OF + os), a.dout.head0 + h, qrow, pol_q);
+          if constexpr (MC) {
+#pragma unroll
+            for (int at = 0; at < D / TQ::kAC; ++at)
+              tma_load_3d_mc(base + C::oO + os * TQ::kBytes + at * TQ::kAtom + crank * (BQ / 2) * TQ::kAC * 2, &tm.oh,
+                             bar(B_OF + os), at * TQ::kAC, a.dout.head0 + h, qrow + (BQ / 2) * (int)crank, 3, pol_q);
+          } else {
+            TQ::load(base + C::oO + os * TQ::kBytes, &tm.o, bar(B_OF + os), a.dout.head0 + h, qrow, pol_q);
+          }
         }
       }
     } else if (warp == 13) {
@@ -278,7 +314,8 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)
             mma_ts(tdV, tPS + 8 * kk, TQ::mn(sO(n), kk), idG, (n > 0 || kk > 0));
-          mma_commit(bar(B_OE + n % OS));
+          if constexpr (MC) mma_commit_mc(bar(B_OE + n % OS), 3);  // dO_n consumed in both CTAs
+          else mma_commit(bar(B_OE + n % OS));
           mma_commit(bar(B_PFREE));
           if (more) {
             mbar_wait(bar(B_DPFREE), n & 1);
@@ -291,7 +328,8 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
 #pragma unroll
           for (int kk = 0; kk < BQ / 16; ++kk)
             mma_ts(tdK, tPS + 32 + 8 * kk, TQ::mn(sQ(n), kk), idG, (n > 0 || kk > 0));
-          mma_commit(bar(B_QE + n % QS));
+          if constexpr (MC) mma_commit_mc(bar(B_QE + n % QS), 3);  // Q_n consumed
+          else mma_commit(bar(B_QE + n % QS));
           if (n > 0)
             mbar_wait(bar(B_DQE), (n - 1) & 1);
           else
@@ -534,6 +572,7 @@ attn_bwd_q64_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ 
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // no CTA leaves while its partner may still multicast into it or arrive on it
   if (warp == 13) tmem_dealloc<512>(tmem);
 #undef TRACE
 }
@@ -552,9 +591,32 @@ int launch_q64(const BwdArgs& a, cudaStream_t s) {
                                  CU_TENSOR_MAP_SWIZZLE_NONE);
   ok &= make_tmap_f32_head_major(&tm.dq16, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 16, BQ,
                                  CU_TENSOR_MAP_SWIZZLE_NONE);
+  ok &= make_tmap_rows_heads_dim(&tm.qh, a.q.base, a.q.rows, a.q.heads, D, ac, BQ / 2, sw);
+  ok &= make_tmap_rows_heads_dim(&tm.oh, a.dout.base, a.dout.rows, a.dout.heads, D, ac, BQ / 2, sw);
   if (!ok) return -1;
-  if (int e = set_max_dynamic_smem((const void*)attn_bwd_q64_kernel<D>, C::kSmem)) return e;
-  attn_bwd_q64_kernel<D><<<dim3(a.n_kv_rows / 128, a.hq / a.G), kThreads, C::kSmem, s>>>(tm, a);
+  const dim3 grid(a.n_kv_rows / 128, a.hq / a.G);
+#ifndef FPDT_BWD_MC
+#define FPDT_BWD_MC 1
+#endif
+  if (FPDT_BWD_MC && grid.x % 2 == 0) {
+    if (int e = set_max_dynamic_smem((const void*)attn_bwd_q64_kernel<D, true>, C::kSmem)) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaError_t e = cudaLaunchKernelEx(&cfg, attn_bwd_q64_kernel<D, true>, tm, a)) return (int)e;
+    return (int)cudaGetLastError();
+  }
+  if (int e = set_max_dynamic_smem((const void*)attn_bwd_q64_kernel<D, false>, C::kSmem)) return e;
+  attn_bwd_q64_kernel<D, false><<<grid, kThreads, C::kSmem, s>>>(tm, a);
   return (int)cudaGetLastError();
 }
 
