@@ -57,11 +57,13 @@ int fpdt_debug_relayout(int which, const void* src, void* dst, int64_t c, int H,
 /* Diagnostic: launch ONE bf16 chunk-pair kernel directly (no scheduler) on caller device buffers, rows
  * [0, n_rows) of q/k/v/dout against each other (the diagonal pair when causal = 1).
  *   which 0 (forward):  out0 = o bf16 [n_rows][n_q_heads][head_dim], out1 = log2-domain lse fp32 [n_q_heads][n_rows]
- *   which 1 (backward; 2 / 3 / 4 force the single-CTA, CTA-pair or 64-row-query-tile kernel): lse2 / Dstat fp32 [n_q_heads][n_rows] (log2-domain lse, rowsum(dO o O)),
+ *   which 1 (backward; 2 / 3 / 4 force the pipe kernel (multicast CTA pairs when n_rows / 128 is even), the
+ *            cta_group::2 kernel or the 64-row-query-tile kernel): lse2 / Dstat fp32 [n_q_heads][n_rows] (log2-domain lse, rowsum(dO o O)),
  *                       out0 = dq accumulator fp32 [n_q_heads][n_rows][head_dim] (zeroed by the caller; scaled
  *                       dQ is added), out1 / out2 = dK / dV bf16 [n_rows][n_kv_heads][head_dim]
  * trace (nullable): device int64 [16][4096] receiving SM-clock timestamps of warp-role protocol events of
- * CTA (trace_cta, 0).  Returns FPDT_OK or a status. */
+ * CTA (trace_cta, 0).  n_rows: a multiple of 256 for which 0 and 3, of 128 otherwise (else FPDT_ERR_DIVISIBILITY).
+ * Returns FPDT_OK or a status. */
 int fpdt_debug_pair(int which, int head_dim, int causal, const void* q, const void* k, const void* v, const void* dout,
                     const float* lse2, const float* Dstat, void* out0, void* out1, void* out2, int64_t n_rows,
                     int n_q_heads, int n_kv_heads, long long* trace, int trace_cta, void* stream);

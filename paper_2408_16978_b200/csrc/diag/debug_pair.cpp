@@ -19,7 +19,8 @@ extern "C" int fpdt_debug_pair(int which, int head_dim, int causal, const void* 
                                void* out2, int64_t n_rows, int n_q_heads, int n_kv_heads, long long* trace,
                                int trace_cta, void* stream) {
   if (head_dim != 64 && head_dim != 80 && head_dim != 128) return FPDT_ERR_UNSUPPORTED;
-  if (n_rows % 256 || n_q_heads % n_kv_heads) return FPDT_ERR_DIVISIBILITY;
+  // forward (2 query tiles per CTA) and the CTA-pair backward: 256-row multiples; the other backward kernels: 128
+  if (n_rows % ((which == 0 || which == 3) ? 256 : 128) || n_q_heads % n_kv_heads) return FPDT_ERR_DIVISIBILITY;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   const float scale = (float)(1.0 / std::sqrt((double)head_dim));
   if (which == 0) {
