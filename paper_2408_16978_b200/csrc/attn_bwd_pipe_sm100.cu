@@ -15,6 +15,10 @@
 // the tensor pipe, is the scarce resource here (128 B/clk/SM; an SS-MMA with M = 128, N <= 128 already needs all
 // of it), so per query tile only dQ = dS K (A = the dS smem tile) reads two smem operands.  Shared-memory bytes per
 // tile (d = 80): TMA Q, dO 40K + MMA operands 172K + dS 32K + dQ staging 80K.
+// (Round 2: per-warp traces show the softmax warps on SMSPs 0 and 1 -- with the TMA and MMA issuing warps, whose
+// instructions share the MIO queue with MUFU -- ~200-400 clk behind those on SMSPs 2 and 3 per tile; moving one
+// exponential pair in 2 / 4 / 8 of those warps to the FMA pipe evened them but left the step at 843-847 vs 848 TFLOP/s:
+// the tile period here is set by the dQ reduce-add chain, not by the slowest softmax warp.)
 // Element-wise math uses packed f32x2 FMA-pipe instructions (FFMA2/FADD2/FMUL2); the exponentials all run on MUFU
 // (an FA4-style polynomial offload of a fraction of them measured slower here: one pair in 4 / 8 / 16 on the FMA pipe
 // gave 848-858 / 868 / 871 TFLOP/s against 872-875 all on MUFU, C = 64K, 32 x 80 diagonal pair).
@@ -388,7 +392,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
           p[i + 3] = ex2(x1.y);
         }
       }
-      if (warp == 0 && lane == 0) TRACE(14, n);
+      if (lane == 0 && n < 512) TRACE(14, 512 * warp + n);  // per softmax warp: slot 512 * warp + n
       // dP^T_n -> registers; its TMEM columns then receive P^T_n and dS^T_n (bf16), the A operands of dV and dK
       mbar_wait(bar(B_DP), n & 1);
       if (warp == 0 && lane == 0) TRACE(2, n);
@@ -408,7 +412,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       tmem_wait_st();
       tc_fence_before();
       mbar_arrive(bar(B_P));
-      if (warp == 0 && lane == 0) TRACE(1, n);
+      if (lane == 0 && n < 512) TRACE(1, 512 * warp + n);  // per softmax warp: slot 512 * warp + n
       // dS = P o (dP - D) -> TMEM (dS^T bf16, A of dK) and smem (MN-major dS tile fp16, A of dQ)
       uint32_t pk[32];
       {
@@ -442,7 +446,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       fence_async_shared();
       tc_fence_before();
       mbar_arrive(bar(B_DS));
-      if (warp == 0 && lane == 0) TRACE(3, n);
+      if (lane == 0 && n < 512) TRACE(3, 512 * warp + n);  // per softmax warp: slot 512 * warp + n
     }
     // ---- final dK (half 0) / dV (half 1), thread = key row
     const int64_t row = (int64_t)kt * 128 + r;  // row within the launch's key range

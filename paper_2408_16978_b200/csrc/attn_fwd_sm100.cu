@@ -60,6 +60,16 @@ constexpr float kRescaleThreshold = 8.0f;
 #define FPDT_FWD_STAGES 3  // K/V ring depth at d <= 80 (d = 128: 2, the shared-memory limit); in the bench step on one
                            // box (tools/gpu_ab_stages.sh) 3 stages: fwd 912, 4 stages: 885-886 TFLOP/s
 #endif
+// The softmax warps that share an SMSP with the MMA-issuing warp (9: warps 1 and 5) run one exponential pair in
+// FPDT_FWD_POLY_MMA_SMSP on the FMA pipe (0 = the same split as the others).  MUFU instructions go through the SMSP's
+// MIO queue, where the MMA instructions waiting for the tensor pipe hold them up: per-warp traces (tools/trace_pair.py)
+// showed warp 1 finishing its exponentials ~600 clk after warps 2 and 3 every key tile, and PV_0 waits for the slowest
+// warp.  Measured (round 2, same box): 3 -> the four warps even, standalone pair 953 vs 947, in the bench step fwd 912
+// vs 891 TFLOP/s; 4 -> 891; 2 -> 901 standalone (warp 1 then FMA-bound).  (Also measured: making the MMA thread wait
+// for each MMA group to complete before issuing the next evens the warps too, but serialises the pipe: 870-917.)
+#ifndef FPDT_FWD_POLY_MMA_SMSP
+#define FPDT_FWD_POLY_MMA_SMSP 3
+#endif
 #ifndef FPDT_FWD_POLY_EVERY_D128
 #define FPDT_FWD_POLY_EVERY_D128 8
 #endif
@@ -99,23 +109,6 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
   float y;
   asm("max.f32 %0, %1, %2, %3;" : "=f"(y) : "f"(a), "f"(b), "f"(c));
   return y;
-}
-
-// 2^x for a pair on the FMA pipe (FA4-style MUFU offload): x = j + f, j = rint(x), f in [-1/2, 1/2];
-// degree-3 minimax for 2^f (max rel. error 7.5e-5 << bf16's 2^-9); the exponent is added as an integer.
-// x is clamped to >= -126 (callers use it only where x is finite; at -127 the exponent addition would wrap into
-// the sign bit and give a NaN, so keys far below the running max must still give ~0).
-__device__ __forceinline__ float2 ex2_poly2(float2 x) {
-  x.x = fmaxf(x.x, -126.f);
-  x.y = fmaxf(x.y, -126.f);
-  const float2 kRnd = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
-  const float2 j = __fadd2_rn(x, kRnd);
-  const float2 f = __fadd2_rn(x, __fadd2_rn(kRnd, make_float2(-j.x, -j.y)));
-  float2 p = __ffma2_rn(f, make_float2(0.055169348f, 0.055169348f), make_float2(0.24260798f, 0.24260798f));
-  p = __ffma2_rn(p, f, make_float2(0.69326115f, 0.69326115f));
-  p = __ffma2_rn(p, f, make_float2(0.9999283f, 0.9999283f));
-  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
-                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
 }
 
 // (Measured and not kept: the MUFU exponentials as ex2.approx.f16x2 on f16-rounded arguments (ptxas splits it into two
@@ -295,10 +288,12 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
             tc_fence_after();
             issue_S(0, s2);
             mma_commit(smem_u32(&bar_s[0]));
+            if (j < 1024) TRACE(6, 1024 + j);  // S_0(j+1) issued
             mbar_wait(smem_u32(&bar_sfree[1]), j & 1);
             tc_fence_after();
             issue_S(1, s2);
             mma_commit(smem_u32(&bar_s[1]));
+            if (j < 1024) TRACE(6, 2048 + j);  // S_1(j+1) issued
           }
           mbar_wait(smem_u32(&bar_v[s]), ph);
 #pragma unroll
@@ -310,6 +305,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
             mma_commit(smem_u32(&bar_pvdone[t]));
             if (t == 1) mma_commit(smem_u32(&bar_kv_empty[s]));
             if (!more) mma_commit(smem_u32(&bar_o[t]));
+            if (j < 1024) TRACE(4 + t, 1024 + j);  // PV_t(j) issued and committed
           }
         }
       } else
@@ -436,8 +432,13 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
       if constexpr (C::kSepP) {
         // P in registers first; then the shared P buffer: P_0(j) after PV_1(j-1) has read it, P_1(j) after PV_0(j)
         uint32_t pk[64];
-        sum = any_masked ? exp_pack_store<0, kSumHere, false>(x, sl2, mb, 0, pk)
-                         : exp_pack_store<C::kPolyEvery, kSumHere, false>(x, sl2, mb, 0, pk);
+        if (any_masked)
+          sum = exp_pack_store<0, kSumHere, false>(x, sl2, mb, 0, pk);
+        else if (FPDT_FWD_POLY_MMA_SMSP > 0 && (warp & 3) == 1)
+          sum = exp_pack_store<(FPDT_FWD_POLY_MMA_SMSP > 0 ? FPDT_FWD_POLY_MMA_SMSP : 1), kSumHere, false>(x, sl2, mb, 0,
+                                                                                                     pk);
+        else
+          sum = exp_pack_store<C::kPolyEvery, kSumHere, false>(x, sl2, mb, 0, pk);
         if (t == 0 && j > 0) mbar_wait(smem_u32(&bar_pvdone[1]), (j - 1) & 1);
         if (t == 1) mbar_wait(smem_u32(&bar_pvdone[0]), j & 1);
         tc_fence_after();
@@ -448,12 +449,12 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
                          : exp_pack_store<C::kPolyEvery, kSumHere>(x, sl2, mb, tPw);
       }
       if constexpr (kSumHere) l_run += sum;
-      if ((warp & 3) == 0 && lane == 0) TRACE(10 + 4 * t, j);
+      if (lane == 0 && j < 1024) TRACE(10 + 4 * t, 1024 * (warp & 3) + j);
       tmem_wait_st();
       if ((warp & 3) == 0 && lane == 0) TRACE(11 + 4 * t, j);
       tc_fence_before();
       mbar_arrive(smem_u32(&bar_p[t]));
-      if ((warp & 3) == 0 && lane == 0) TRACE(1 + 2 * t, j);
+      if (lane == 0 && j < 1024) TRACE(1 + 2 * t, 1024 * (warp & 3) + j);
     }
     // epilogue: normalise, merge with the running partial result, write
     mbar_wait(smem_u32(&bar_o[t]), 0);

@@ -49,4 +49,21 @@ struct Tile {
   static constexpr uint32_t kBoxCols = kAtomCols;
 };
 
+// 2^x for a pair on the FMA pipe (FA4-style MUFU offload): x = j + f, j = rint(x), f in [-1/2, 1/2];
+// degree-3 minimax for 2^f (max rel. error 7.5e-5 << bf16's 2^-9); the exponent is added as an integer.
+// x is clamped to >= -126 (callers use it only where x is finite; at -127 the exponent addition would wrap into
+// the sign bit and give a NaN, so keys far below the running max must still give ~0).
+__device__ __forceinline__ float2 ex2_poly2(float2 x) {
+  x.x = fmaxf(x.x, -126.f);
+  x.y = fmaxf(x.y, -126.f);
+  const float2 kRnd = make_float2(12582912.f, 12582912.f);  // 1.5 * 2^23
+  const float2 j = __fadd2_rn(x, kRnd);
+  const float2 f = __fadd2_rn(x, __fadd2_rn(kRnd, make_float2(-j.x, -j.y)));
+  float2 p = __ffma2_rn(f, make_float2(0.055169348f, 0.055169348f), make_float2(0.24260798f, 0.24260798f));
+  p = __ffma2_rn(p, f, make_float2(0.69326115f, 0.69326115f));
+  p = __ffma2_rn(p, f, make_float2(0.9999283f, 0.9999283f));
+  return make_float2(__int_as_float(__float_as_int(p.x) + (__float_as_int(j.x) << 23)),
+                     __int_as_float(__float_as_int(p.y) + (__float_as_int(j.y) << 23)));
+}
+
 }  // namespace fpdt

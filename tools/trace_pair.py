@@ -64,7 +64,7 @@ names = {"bwd": ["sm:got_S", "sm:arr_P", "sm:got_dP", "sm:arr_dS", "mma:got_P", 
          "fwd": ["sm0:got_S", "sm0:arr_P", "sm1:got_S", "sm1:arr_P", "mma:got_P0", "mma:got_P1", "mma:got_K+1",
                  "prod:got_kvempty", "sm0:S_loaded", "sm0:max_done", "sm0:exp_done", "sm0:st_done",
                  "sm1:S_loaded", "sm1:max_done", "sm1:exp_done", "sm1:st_done"]}[which]
-n = int((t[0] > 0).sum())
+n = int((t[0][:1024] > 0).sum()) if which == "fwd" else int((t[0][:512] > 0).sum())
 base = t[0][0]
 print(f"traced CTA {cta}: {n} iterations; per-iteration deltas (SM clocks), iterations 4..{min(n, 12)}")
 for i in range(4, min(n, 12)):
@@ -79,3 +79,24 @@ if n > 8:
         valid = [(t[e][i] - t[0][i]) for i in range(4, n - 1) if t[e][i] > 0]
         if valid:
             print(f"  {nm:>18s} - sm:got_S : median {np.median(valid):8.0f}")
+if which == "fwd" and n > 8:
+    # per-warp spread (events recorded by all four warps of a tile at slot 1024 * warp + iteration)
+    for e, nm in ((10, "sm0:exp_done"), (1, "sm0:arr_P"), (14, "sm1:exp_done"), (3, "sm1:arr_P")):
+        meds = []
+        for w in range(4):
+            valid = [(t[e][1024 * w + i] - t[0][i]) for i in range(4, min(n, 1024) - 1) if t[e][1024 * w + i] > 0]
+            meds.append(f"{np.median(valid):7.0f}" if valid else "      -")
+        print(f"  {nm:>14s} - sm:got_S per warp 0..3: " + " ".join(meds))
+if which == "fwd" and n > 8:
+    for e, sl, nm in ((6, 1024, "mma:S0(j+1) issued"), (6, 2048, "mma:S1(j+1) issued"), (4, 1024, "mma:PV0(j) issued"),
+                      (5, 1024, "mma:PV1(j) issued")):
+        valid = [(t[e][sl + i] - t[0][i]) for i in range(4, min(n, 1024) - 1) if t[e][sl + i] > 0]
+        if valid:
+            print(f"  {nm:>20s} - sm:got_S : median {np.median(valid):8.0f}")
+if which == "bwd" and n > 8:
+    for e, nm in ((14, "sm:exp_done"), (1, "sm:arr_P"), (3, "sm:arr_dS")):
+        meds = []
+        for w in range(8):
+            valid = [(t[e][512 * w + i] - t[0][i]) for i in range(4, min(n, 512) - 1) if t[e][512 * w + i] > 0]
+            meds.append(f"{np.median(valid):6.0f}" if valid else "     -")
+        print(f"  {nm:>12s} - sm:got_S per warp 0..7: " + " ".join(meds))
