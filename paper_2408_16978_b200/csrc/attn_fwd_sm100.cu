@@ -66,7 +66,9 @@ constexpr float kRescaleThreshold = 8.0f;
 // showed warp 1 finishing its exponentials ~600 clk after warps 2 and 3 every key tile, and PV_0 waits for the slowest
 // warp.  Measured (round 2, same box): 3 -> the four warps even, standalone pair 953 vs 947, in the bench step fwd 912
 // vs 891 TFLOP/s; 4 -> 891; 2 -> 901 standalone (warp 1 then FMA-bound).  (Also measured: making the MMA thread wait
-// for each MMA group to complete before issuing the next evens the warps too, but serialises the pipe: 870-917.)
+// for each MMA group to complete before issuing the next evens the warps too, but serialises the pipe: 870-917.  A third
+// code path -- warps 0 and 4, beside the TMA producer, with their own split -- dropped the forward to 785-803 in the
+// step: the unrolled exponential loops are large, and each SMSP's path has to stay in the instruction caches.)
 #ifndef FPDT_FWD_POLY_MMA_SMSP
 #define FPDT_FWD_POLY_MMA_SMSP 3
 #endif
