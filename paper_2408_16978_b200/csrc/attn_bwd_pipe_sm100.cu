@@ -18,7 +18,8 @@
 // (Round 2: per-warp traces show the softmax warps on SMSPs 0 and 1 -- with the TMA and MMA issuing warps, whose
 // instructions share the MIO queue with MUFU -- ~200-400 clk behind those on SMSPs 2 and 3 per tile; moving one
 // exponential pair in 2 / 4 / 8 of those warps to the FMA pipe evened them but left the step at 843-847 vs 848 TFLOP/s:
-// the tile period here is set by the dQ reduce-add chain, not by the slowest softmax warp.)
+// the tile period here is set by the dQ reduce-add chain, not by the slowest softmax warp.  Moving the TMA / MMA warps
+// to SMSPs 2 / 3 (warps 14 / 15) changed nothing either: 844.5-845.1 vs 844.8-845.3 in the step.)
 // Element-wise math uses packed f32x2 FMA-pipe instructions (FFMA2/FADD2/FMUL2); the exponentials all run on MUFU
 // (an FA4-style polynomial offload of a fraction of them measured slower here: one pair in 4 / 8 / 16 on the FMA pipe
 // gave 848-858 / 868 / 871 TFLOP/s against 872-875 all on MUFU, C = 64K, 32 x 80 diagonal pair).
