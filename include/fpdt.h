@@ -67,7 +67,10 @@ enum fpdt_dtype { FPDT_BF16 = 0, FPDT_FP32 = 1 };
 int fpdt_get_unique_id(unsigned char id[128]);
 
 /* Create a context on CUDA device `device` for rank `rank` of a group of `world_size` ranks.
- * nccl_id: the 128-byte id from fpdt_get_unique_id (ignored, may be NULL, when world_size == 1).
+ * nccl_id: the 128-byte id from fpdt_get_unique_id.  world_size == 1: NULL (the schedules work on the caller's rows
+ *   in place), or an id of its own, which makes a one-rank NCCL communicator and runs the sequence-parallel path with
+ *   every exchange an ncclAlltoAll of the rank with itself (pack, exchange, unpack; the results equal the NULL case):
+ *   the production NCCL data plane on one GPU.
  * host_arena_bytes: pinned host chunk store to reserve now; 0 = allocate on the first offloaded
  * forward (sized for that call).  The context owns the NCCL communicator, its streams and events,
  * the pinned host store, the device slots and the saved state of ONE attention layer.

@@ -77,7 +77,8 @@ fpdt_ctx* create_ctx(int world_size, int rank, const unsigned char* nccl_id, fpd
       for (auto e : pe) FPDT_CHECK_CUDA(cudaEventCreateWithFlags(e, cudaEventDisableTiming));
     }
     if (const char* e = getenv("FPDT_NCCL_TIMEOUT_S")) ctx->nccl_timeout_s = std::max(1.0, atof(e));
-    if (world_size > 1 && !group) {
+    if ((world_size > 1 || nccl_id) && !group) {
+      ctx->xch1 = world_size == 1;
       ncclUniqueId u;
       std::memcpy(u.internal, nccl_id, 128);
       ncclConfig_t cfg = NCCL_CONFIG_INITIALIZER;
@@ -112,6 +113,7 @@ int fpdt_ctx_create(int world_size, int rank, const unsigned char* nccl_id, int 
   return run([&] {
     if (!out || world_size < 1 || rank < 0 || rank >= world_size) fail(FPDT_ERR_ARG, "bad world_size/rank/out");
     if (world_size > 1 && !nccl_id) fail(FPDT_ERR_ARG, "nccl_id required for world_size > 1");
+    // world_size 1 with an id: one-rank communicator, the exchange path (fpdt_ctx::xch1)
     *out = create_ctx(world_size, rank, nccl_id, nullptr, device, host_arena_bytes);
   });
 }
@@ -297,7 +299,7 @@ int fpdt_attn_bwd_host(fpdt_ctx* ctx, const void* o, const void* dout, void* dq,
     check_collective_args(ctx, 6, c, 0);
     const size_t bq = (size_t)s_local * n_q_heads * head_dim * c.eb, bkv = (size_t)s_local * n_kv_heads * head_dim * c.eb;
     void* od = ctx->bufs[B_HO].ptr;
-    void* dod = c.p > 1 ? dev(ctx, B_HDO, bq) : nullptr;  // p == 1 fetches dO_i from the caller's rows directly
+    void* dod = exchanges(ctx) ? dev(ctx, B_HDO, bq) : nullptr;  // p == 1 fetches dO_i from the caller's rows directly
     void* dqd = dev(ctx, B_HDQ, bq);
     void* dkd = dev(ctx, B_HDK, bkv);
     void* dvd = dev(ctx, B_HDV, bkv);

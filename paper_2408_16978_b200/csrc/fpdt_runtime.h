@@ -146,6 +146,9 @@ struct fpdt_ctx {
   int p = 1, rank = 0, device = 0;
   ncclComm_t comm = nullptr;
   fpdt_group* group = nullptr;  // non-null: in-process group instead of NCCL
+  // world size 1 created with an NCCL id: the sequence-parallel path with a one-rank communicator (every exchange an
+  // ncclAlltoAll of the rank with itself), so that one GPU runs the production NCCL data plane
+  bool xch1 = false;
   cudaStream_t s_comm = nullptr, s_h2d = nullptr, s_d2h = nullptr;
   // Q-outer backward: second compute stream (pairs of one query chunk run two at a time) and its slot events
   cudaStream_t s_comp2 = nullptr;
@@ -224,6 +227,10 @@ struct fpdt_ctx {
 };
 
 namespace fpdt_rt {
+
+// true when the schedules run the sequence-parallel exchanges (world size > 1, or world size 1 with a one-rank NCCL
+// communicator: fpdt_ctx::xch1); false: world size 1 works on the caller's rows in place
+inline bool exchanges(const fpdt_ctx* ctx) { return ctx->p > 1 || ctx->xch1; }
 
 void* dev(fpdt_ctx* ctx, int id, size_t bytes);
 

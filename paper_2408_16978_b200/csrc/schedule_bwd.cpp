@@ -58,6 +58,7 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
                       cudaStream_t cs) {
   const int64_t C = c.C, u = c.u;
   const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
+  const bool X = exchanges(ctx);  // sequence-parallel exchanges (p > 1, or p = 1 through a one-rank communicator)
   const int hcomb = hq + 2 * hkv;
   const size_t row_q = (size_t)hq * d * eb, row_kv2 = (size_t)2 * hkv * d * eb;
   const size_t dkv_elems = (size_t)C * 2 * hkv * d, dkv_bytes = dkv_elems * 4;
@@ -116,7 +117,7 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
   // final key chunks (ev_qo_send[0] = dq part free, [1 + r] = part r free)
   uint8_t *qsend = nullptr, *qrecv = nullptr;
   const size_t kvpart = (size_t)C * row_kv2;
-  if (p > 1) {
+  if (X) {
     qsend = (uint8_t*)dev(ctx, B_QOSEND, (size_t)C * row_q + 2 * kvpart);
     qrecv = (uint8_t*)dev(ctx, B_QORECV, (size_t)C * row_q + 2 * kvpart);
     for (int b = 0; b < 3; ++b) rec(ctx->ev_qo_send[b], cs);
@@ -152,7 +153,7 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
     HeadView qi, doi;
     int64_t q_row0 = 0;
     if (R.q(i)) {
-      if (p == 1) {
+      if (!X) {
         qi = {ctx->saved_q, c.S, hq, 0};
         doi = {do_h, do_rows, do_heads, do_head0};
         q_row0 = i * C;
@@ -188,7 +189,7 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
       float* acc = nullptr;
       int sl = -1;
       if (R.kv(j)) {
-        if (p == 1) {
+        if (!X) {
           kj = {ctx->saved_k, c.S, hkv, 0};
           vj = {ctx->saved_v, c.S, hkv, 0};
           kv_row0 = j * C;
@@ -216,7 +217,7 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
       BwdArgs a = pair_bwd_args(c, qi, doi, kj, vj, q_row0, kv_row0, i, j, lse_save, Dh, dqi, acc,
                                 acc + (size_t)C * hkv * d, first, fin);
       int part = 0;
-      if (p == 1) {
+      if (!X) {
         a.dk_out = (uint8_t*)dk + (size_t)j * C * c.Hkv * d * eb;
         a.dv_out = (uint8_t*)dv + (size_t)j * C * c.Hkv * d * eb;
         a.kv_out_ld = (int64_t)c.Hkv * d;
@@ -243,22 +244,22 @@ void backward_q_outer(fpdt_ctx* ctx, const Config& c, const Residency& R, const 
           rec(ctx->ev_qo_free[sl], st);
         }
       }
-      if (fin && p > 1) send_back(st, part, j);
+      if (fin && X) send_back(st, part, j);
     }
     if (ns > 1) {  // join: dq_i is complete when both streams' pairs are
       rec(ctx->ev_join, ctx->s_comp2);
       wait(cs, ctx->ev_join);
     }
     // dq_i is final after its last key chunk
-    if (p > 1) wait(cs, ctx->ev_qo_send[0]);
+    if (X) wait(cs, ctx->ev_qo_send[0]);
     FPDT_CHECK_LAUNCH(launch_convert_out(dqi, C, hq, d, C * d, 1.f,
-                                         p == 1 ? (uint8_t*)dq + (size_t)i * C * c.Hq * d * eb : qsend, c.dtype,
-                                         p == 1 ? (int64_t)c.Hq * d : (int64_t)hq * d, 0, cs));
+                                         !X ? (uint8_t*)dq + (size_t)i * C * c.Hq * d * eb : qsend, c.dtype,
+                                         !X ? (int64_t)c.Hq * d : (int64_t)hq * d, 0, cs));
     ctx->stats.kernel_launches++;
-    if (p > 1) send_back(cs, 0, i);
+    if (X) send_back(cs, 0, i);
     if (!R.q(i)) rec(ctx->ev_q_free[qsl], cs);
   }
-  if (p > 1) {
+  if (X) {
     rec(ctx->ev_comm_done, ctx->s_comm);
     wait(cs, ctx->ev_comm_done);
   }
@@ -271,6 +272,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   Nvtx nv("fpdt:backward");
   const int64_t C = c.C, u = c.u;
   const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
+  const bool X = exchanges(ctx);  // sequence-parallel exchanges (p > 1, or p = 1 through a one-rank communicator)
   const int hcomb = hq + 2 * hkv;
   const size_t row_q = (size_t)hq * d * eb, row_kv2 = (size_t)2 * hkv * d * eb;
   const float sl2 = c.scale * 1.4426950408889634f;
@@ -295,7 +297,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   for (cudaStream_t s : {ctx->s_comm, ctx->s_h2d, ctx->s_d2h}) wait(s, ctx->ev_enter);
   HostLayout hl{};
   if (c.offload) hl = host_layout(c);
-  const bool io_p1 = io && p == 1;
+  const bool io_p1 = io && !X;
   if (io && io->upload_o) {
     // o is not the saved forward's output: its device mirror is stale
     h2d_io(ctx, const_cast<void*>(o), io->o, (size_t)c.s_local * c.Hq * d * eb);
@@ -306,7 +308,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   const Residency R = make_residency(u, c.offload ? ctx->saved_res_kv : 0, c.offload ? ctx->saved_res_q : 0);
   uint8_t* resstore = (uint8_t*)ctx->bufs[B_RESSTORE].ptr;  // p > 1: the forward's resident head-layout chunks
   auto res_chunk = [&](int64_t m) { return resstore + (size_t)R.slot[(size_t)m] * C * hcomb * d * eb; };
-  uint8_t* dores = (p > 1 && R.nq > 0) ? (uint8_t*)dev(ctx, B_DORES, (size_t)R.nq * C * 2 * hq * d * eb) : nullptr;
+  uint8_t* dores = (X && R.nq > 0) ? (uint8_t*)dev(ctx, B_DORES, (size_t)R.nq * C * 2 * hq * d * eb) : nullptr;
   float* dqres = R.nq > 0 ? (float*)dev(ctx, B_DQRES, (size_t)R.nq * C * hq * d * 4) : nullptr;
   // ---- B1/B2: D and the head-layout dO
   const void* do_h = dout;            // head-layout dO view base (p == 1: the caller's dO)
@@ -316,7 +318,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   if (io_p1) {
     // host rows: D_i is formed at the first pair of query chunk i from its fetched dO_i (below); dO_i and q_i are
     // fetched from the caller's host rows
-  } else if (p == 1) {
+  } else if (!X) {
     FPDT_CHECK_LAUNCH(launch_bwd_preprocess_D(o, dout, c.dtype, c.S, hq, d, (int64_t)c.Hq * d, o_resid,
                                               (int64_t)hq * d, Dh, c.S, cs));
     ctx->stats.kernel_launches++;
@@ -382,7 +384,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   // dq, dk, dv leave through the other
   uint8_t *bsend2[2] = {nullptr, nullptr}, *brecv2[2] = {nullptr, nullptr};
   for (int b = 0; b < 2; ++b) rec(ctx->ev_bsend_free[b], cs);
-  if (p > 1)
+  if (X)
     for (int b = 0; b < 2; ++b) {
       bsend2[b] = (uint8_t*)dev(ctx, b ? B_BWD_SEND1 : B_BWD_SEND, (size_t)C * hcomb * d * eb);
       brecv2[b] = (uint8_t*)dev(ctx, b ? B_BWD_RECV1 : B_BWD_RECV, (size_t)C * hcomb * d * eb);
@@ -432,10 +434,10 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   // B6: dq_j final (fp32, already scaled) -> the caller's rows (p == 1) or the head-side send buffer (p > 1)
   // dq_final: head-major fp32 rows of chunk j, heads head_stride elements apart
   auto emit_dq = [&](int64_t j, const float* dq_final, int64_t head_stride) {
-    if (p == 1 && proj)
+    if (!X && proj)
       FPDT_CHECK_LAUNCH(launch_convert_out(dq_final, C, hq, d, head_stride, 1.f, dqkv_buf[j & 1], c.dtype, ntot, 0,
                                            cs));
-    else if (p == 1)
+    else if (!X)
       FPDT_CHECK_LAUNCH(launch_convert_out(dq_final, C, hq, d, head_stride, 1.f,
                                            (uint8_t*)dq + (size_t)j * C * c.Hq * d * eb, c.dtype, (int64_t)c.Hq * d,
                                            0, cs));
@@ -446,7 +448,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
   };
   // B7: after outer iteration j, dq_j, dk_j, dv_j (in bsend) go back to their owner ranks (p > 1)
   auto send_back = [&](int64_t j) {
-    if (p == 1) {
+    if (!X) {
       // the projection backward of chunk j on the compute stream, right after its last pair (concurrent with the
       // pair kernels on another stream it only breaks their waves; at p > 1 it follows the return all-to-all below)
       if (!proj) return;
@@ -477,12 +479,12 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
     rec(ctx->ev_bsend_free[j & 1], ctx->s_comm);  // bsend / brecv [j & 1] reusable by outer iteration j + 2
   };
   auto set_kv_out = [&](BwdArgs& a, int64_t j) {
-    if (p == 1 && proj) {
+    if (!X && proj) {
       a.dk_out = dqkv_buf[j & 1];
       a.dv_out = dqkv_buf[j & 1] + (size_t)hkv * d * eb;
       a.kv_out_ld = ntot;
       a.kv_out_head0 = hq;  // as the p > 1 send buffer: dk heads [hq, hq + hkv), dv pre-offset by hkv heads
-    } else if (p == 1) {
+    } else if (!X) {
       a.dk_out = (uint8_t*)dk + (size_t)j * C * c.Hkv * d * eb;
       a.dv_out = (uint8_t*)dv + (size_t)j * C * c.Hkv * d * eb;
       a.kv_out_ld = (int64_t)c.Hkv * d;
@@ -501,7 +503,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
     float* dq_dev = (float*)dev(ctx, B_DQDEV, (size_t)c.S * hq * d * 4);
     FPDT_CHECK_CUDA(cudaMemsetAsync(dq_dev, 0, (size_t)c.S * hq * d * 4, cs));
     HeadView qv, kv, vv;
-    if (p == 1) {
+    if (!X) {
       qv = {ctx->saved_q, c.S, hq, 0};
       kv = {ctx->saved_k, c.S, hkv, 0};
       vv = {ctx->saved_v, c.S, hkv, 0};
@@ -512,8 +514,8 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       vv = {store, c.S, hcomb, hq + hkv};
     }
     for (int64_t j = 0; j < u; ++j) {
-      if (p > 1 || proj) {
-        if (p > 1) bsend = bsend2[j & 1];
+      if (X || proj) {
+        if (X) bsend = bsend2[j & 1];
         wait(cs, ctx->ev_bsend_free[j & 1]);
       }
       BwdArgs a;
@@ -581,8 +583,8 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
     };
     for (int64_t j = 0; j < u; ++j) {
       const int ks = (int)(j & 1);
-      if (p > 1 || proj) {
-        if (p > 1) bsend = bsend2[j & 1];
+      if (X || proj) {
+        if (X) bsend = bsend2[j & 1];
         wait(cs, ctx->ev_bsend_free[j & 1]);  // chunk j-2's final gradients have left this buffer
       }
       int64_t last_i = j;  // the last query chunk that attends key chunk j
@@ -593,7 +595,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       HeadView kj, vj;
       int64_t kv_row0 = 0;
       if (R.kv(j)) {
-        if (p == 1) {
+        if (!X) {
           kj = {ctx->saved_k, c.S, hkv, 0};
           vj = {ctx->saved_v, c.S, hkv, 0};
           kv_row0 = j * C;
@@ -616,7 +618,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
         float* dqi = nullptr;
         if (qres) {
           // query-side resident chunk: q_i, dO_i in place, its dq partial accumulates in device memory
-          if (p == 1) {
+          if (!X) {
             qi = {ctx->saved_q, c.S, hq, 0};
             doi = {do_h, do_rows, do_heads, do_head0};
             q_row0 = i * C;
@@ -625,7 +627,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
             doi = {dores + (size_t)R.qslot[(size_t)i] * C * 2 * hq * d * eb, C, 2 * hq, hq};
           }
           dqi = dqres + (size_t)R.qslot[(size_t)i] * C * hq * d;
-          if (p > 1) wait(cs, ctx->ev_a2a[i]);  // its (O, dO) exchange and D_i (a no-op after the first pair)
+          if (X) wait(cs, ctx->ev_a2a[i]);  // its (O, dO) exchange and D_i (a no-op after the first pair)
           if (!dq_started[i]) FPDT_CHECK_CUDA(cudaMemsetAsync(dqi, 0, (size_t)C * hq * d * 4, cs));
         } else {
           // B4: fetch q_i, dO_i and (when it already holds contributions) the dq partial of chunk i
@@ -678,7 +680,7 @@ void backward(fpdt_ctx* ctx, const Config& c, const void* o, const void* dout, v
       if (io) {
         // host rows: chunk j's dq, dk, dv rows are final (p == 1: on the compute stream; p > 1: unpacked on the comm
         // stream by send_back)
-        rec(ctx->ev_tmp, p == 1 ? cs : ctx->s_comm);
+        rec(ctx->ev_tmp, !X ? cs : ctx->s_comm);
         wait(ctx->s_d2h, ctx->ev_tmp);
         const size_t bq = (size_t)c.c * c.Hq * d * eb, bkv = (size_t)c.c * c.Hkv * d * eb;
         d2h_io(ctx, (uint8_t*)io->dq + (size_t)j * bq, (const uint8_t*)dq + (size_t)j * bq, bq);

@@ -13,6 +13,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   Nvtx nv("fpdt:forward");
   const int64_t C = c.C, u = c.u;
   const int d = c.d, hq = c.hq, hkv = c.hkv, eb = c.eb, p = c.p;
+  const bool X = exchanges(ctx);  // sequence-parallel exchanges (p > 1, or p = 1 through a one-rank communicator)
   const size_t row_q = (size_t)hq * d * eb, row_kv2 = (size_t)2 * hkv * d * eb;
   const int hcomb = hq + 2 * hkv;  // combined head-layout buffer: q heads, k heads, v heads
   const float sl2 = c.scale * 1.4426950408889634f;
@@ -57,15 +58,15 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   }
   // device store for resident mode with p > 1: gathered [S][hcomb][d]
   uint8_t* store = nullptr;
-  if (!c.offload && p > 1) store = (uint8_t*)dev(ctx, B_STORE, (size_t)c.S * hcomb * d * eb);
+  if (!c.offload && X) store = (uint8_t*)dev(ctx, B_STORE, (size_t)c.S * hcomb * d * eb);
   // head-layout output of a chunk before its return all-to-all (p > 1), double-buffered so that chunk m+1's pairs
   // run while chunk m's output is exchanged
   uint8_t* o_hat[2] = {nullptr, nullptr};
-  if (p > 1)
+  if (X)
     for (int b = 0; b < 2; ++b) o_hat[b] = (uint8_t*)dev(ctx, b ? B_OHAT1 : B_OHAT, (size_t)C * hq * d * eb);
   uint8_t* a2a_send[2] = {nullptr, nullptr};
   uint8_t* a2a_recv[2] = {nullptr, nullptr};
-  if (p > 1) {
+  if (X) {
     for (int b = 0; b < 2; ++b) {
       a2a_send[b] = (uint8_t*)dev(ctx, B_A2A_SEND0 + b, (size_t)C * hcomb * d * eb);
       if (c.offload) a2a_recv[b] = (uint8_t*)dev(ctx, B_A2A_RECV0 + b, (size_t)C * hcomb * d * eb);
@@ -74,15 +75,15 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
   // fused projection (fpdt_block_fwd): chunk m of the hidden state is projected on the comm stream just before
   // its all-to-all; the GEMM's epilogue writes the all-to-all send layout [p][c][hq + 2hkv][d] directly
   // (the pack fused into the GEMM); at p = 1 that layout is the combined head layout [C][Hq + 2Hkv][d] itself.
-  const bool proj = pj != nullptr, headbuf = p > 1 || proj;
+  const bool proj = pj != nullptr, headbuf = X || proj;
   const int64_t ntot = (int64_t)(c.Hq + 2 * c.Hkv) * d;
   ScatterOut scat;
   scat.d = d; scat.Hq = c.Hq; scat.Hkv = c.Hkv; scat.hq = hq; scat.hkv = hkv;
   scat.peer_stride = c.c * hcomb * d;
-  if (proj && p == 1)
+  if (proj && !X)
     for (int b = 0; b < 2; ++b) a2a_recv[b] = (uint8_t*)dev(ctx, B_A2A_RECV0 + b, (size_t)C * hcomb * d * eb);
   const Residency R = make_residency(u, c.offload ? ctx->saved_res_kv : 0, c.offload ? ctx->saved_res_q : 0);
-  uint8_t* resstore = (p > 1 && R.n > 0) ? (uint8_t*)dev(ctx, B_RESSTORE, (size_t)R.n * C * hcomb * d * eb) : nullptr;
+  uint8_t* resstore = (X && R.n > 0) ? (uint8_t*)dev(ctx, B_RESSTORE, (size_t)R.n * C * hcomb * d * eb) : nullptr;
   auto res_chunk = [&](int64_t m) { return resstore + (size_t)R.slot[(size_t)m] * C * hcomb * d * eb; };
   uint8_t* kv_slot[2] = {nullptr, nullptr};
   KvFetch kvf(ctx, c, ctx->saved_fetch);
@@ -115,10 +116,10 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     d2h_2d(ctx, ctx->host + hl.kv(m, u) + wkv, row_kv2, (const uint8_t*)v + (size_t)m * C * wkv, wkv, wkv, C);
     rec(ctx->ev_off[(size_t)m], ctx->s_d2h);
   };
-  const bool io_p1 = io && p == 1;
+  const bool io_p1 = io && !X;
   if (io_p1) stage_p1(0);
   // p == 1 with offload: the head-layout chunk IS the caller's rows; offload all chunks up front
-  if (p == 1 && c.offload && !proj && !io) {
+  if (!X && c.offload && !proj && !io) {
     for (int64_t m = 0; m < u; ++m) {
       if (!R.q(m)) d2h(ctx, ctx->host + hl.q(m), (const uint8_t*)q + (size_t)m * C * row_q, (size_t)C * row_q);
       if (!R.kv(m)) {
@@ -148,10 +149,10 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       // The projection GEMM runs on the compute stream, between the pairs of chunk m-1 (it is enqueued one chunk
       // ahead); its all-to-all still overlaps chunk m-1's pairs on the comm stream.  Measured at the bench shape: on
       // the comm stream, concurrently with the pair kernels, it only breaks their waves (block overhead 79 vs 68 ms).
-      if (p == 1) wait(cs, ctx->ev_recv_used_d[b]);              // the offload of chunk m-2 has read this buffer
+      if (!X) wait(cs, ctx->ev_recv_used_d[b]);              // the offload of chunk m-2 has read this buffer
       else if (m >= 2) wait(cs, ctx->ev_a2a[m - 2]);             // chunk m-2's all-to-all has read the send buffer
       const uint8_t* xm = (const uint8_t*)pj->x + (size_t)m * c.c * pj->hidden * eb;
-      gemm_xw(ctx, c.dtype, xm, pj->hidden, pj->w, ntot, p == 1 ? recv : a2a_send[b], ntot, c.c, pj->hidden, ntot, cs,
+      gemm_xw(ctx, c.dtype, xm, pj->hidden, pj->w, ntot, !X ? recv : a2a_send[b], ntot, c.c, pj->hidden, ntot, cs,
               &scat);
       rec(ctx->ev_tmp, cs);
       wait(ctx->s_comm, ctx->ev_tmp);
@@ -180,7 +181,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
                                              hq + hkv, ctx->s_comm));
       ctx->stats.kernel_launches += 3;
     }
-    if (p > 1) alltoall(ctx, a2a_send[b], recv, per_peer, c.dtype);
+    if (X) alltoall(ctx, a2a_send[b], recv, per_peer, c.dtype);
     rec(ctx->ev_a2a[m], ctx->s_comm);
     if (c.offload) {
       wait(ctx->s_d2h, ctx->ev_a2a[m]);
@@ -238,7 +239,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     a.scale_log2 = sl2;
     a.o_acc = o_acc;
     a.lse_acc = lse_acc;
-    if (p == 1) {
+    if (!X) {
       a.o_out = (uint8_t*)o + (size_t)m * C * c.Hq * d * eb;
       a.o_ld = (int64_t)c.Hq * d;
       a.lse_user = lse ? lse + (size_t)m * C * c.Hq : nullptr;
@@ -310,7 +311,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
     if (headbuf) rec(ctx->ev_recv_used_c[m & 1], cs);
     // output projection of chunk m (fpdt_block_fwd with w_o): y_m = o_m w_o once O_m is final in the sequence layout
     const int64_t od = (int64_t)c.Hq * d;
-    if (proj && pj->w_o && p == 1)
+    if (proj && pj->w_o && !X)
       gemm_xw(ctx, c.dtype, (const uint8_t*)o + (size_t)m * C * od * eb, od, pj->w_o, pj->hidden,
               (uint8_t*)pj->y + (size_t)m * C * pj->hidden * eb, pj->hidden, C, od, pj->hidden, cs);
     // host rows: chunk m's output rows (final now at p == 1, after the return exchange at p > 1) leave at once
@@ -325,7 +326,7 @@ void forward(fpdt_ctx* ctx, const Config& c, const void* q, const void* k, const
       }
     };
     if (io_p1) download_o(cs);
-    if (p > 1) {
+    if (X) {
       // F10: all-to-all of O_m back to the sequence layout, then unpack into the caller's rows of slot m (on the comm
       // stream behind chunk m+1's exchange, so it overlaps chunk m+1's pairs)
       rec(ctx->ev_o_ready, cs);
