@@ -16,9 +16,10 @@ pytestmark = pytest.mark.gpu
 
 
 def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, keep=None, oproj=None,
-              hidden_offload=False, stats=None) -> dict:
+              hidden_offload=False, stats=None, nccl1=False) -> dict:
     """oproj: {"wo", "dy"} for the output projection (y = o wo; the backward starts from dy).  hidden_offload: the
-    forward offloads x and the backward gets x = None (fpdt_set_hidden_offload)."""
+    forward offloads x and the backward gets x = None (fpdt_set_hidden_offload).  nccl1: world size 1 through a one-rank
+    NCCL communicator (the exchange path, tests/test_gpu_nccl.py)."""
     from paper_2408_16978_b200 import fpdt
     S, hidden = xin["x"].shape
     s_local = S // p
@@ -50,7 +51,10 @@ def run_block(xin: dict, p: int, C: int, dtype: str, Hq: int, Hkv: int, d: int, 
                 dx = torch.empty_like(x)
                 dw = torch.full(tuple(w.shape), float("nan"), dtype=torch.float32, device="cuda")
             stream.synchronize()
-            ctx = fpdt.FPDTContext(p, r, group=group) if p > 1 else fpdt.FPDTContext()
+            if p > 1:
+                ctx = fpdt.FPDTContext(p, r, group=group)
+            else:
+                ctx = fpdt.FPDTContext(1, 0, fpdt.fpdt_get_unique_id()) if nccl1 else fpdt.FPDTContext()
             if keep is not None:
                 ctx.set_sparsity(keep)
             if hidden_offload:
@@ -227,3 +231,22 @@ def test_block_hidden_offload(p):
     for r in range(p):
         assert st_b[r]["bytes_d2h"] - st_a[r]["bytes_d2h"] == xbytes
         assert st_b[r]["bytes_h2d"] - st_a[r]["bytes_h2d"] == xbytes
+
+
+@pytest.mark.parametrize("oproj", [False, True])
+def test_block_one_rank_nccl(oproj):
+    """The fused-projection block through a one-rank NCCL communicator: the forward GEMM's epilogue scatters into the
+    all-to-all send layout and ncclAlltoAll delivers it; equal to the direct world-size-1 block (O, lse bitwise) and to
+    the oracle."""
+    S, hidden, Hq, Hkv, d, C = 2048, 320, 4, 4, 80, 512
+    xin = gen.make_block_inputs("normal", 43, S, hidden, Hq, Hkv, d)
+    op = gen.make_output_proj_inputs(45, S, hidden, Hq, d) if oproj else None
+    got = run_block(xin, 1, C, "bf16", Hq, Hkv, d, oproj=op, nccl1=True)
+    ref = run_block(xin, 1, C, "bf16", Hq, Hkv, d, oproj=op)
+    assert np.array_equal(got["o"], ref["o"]) and np.array_equal(got["lse"], ref["lse"])
+    for n in ("dx", "y") if oproj else ("dx",):
+        assert rel_err(got[n], ref[n]) < 1e-2, n
+    if not oproj:
+        exact = oracle_block(xin, Hq, Hkv, d, "bf16")
+        errs = {n: rel_err(got[n], exact[n]) for n in exact}
+        assert all(e <= TOL["bf16"] for e in errs.values()), errs
