@@ -201,6 +201,8 @@ def run_ours(args):
 
     # NCCL id through torch.distributed (plumbing only)
     nid = distributed.broadcast_nccl_id(rank, world, fpdt.fpdt_get_unique_id)
+    if world == 1 and args.exchange_path:
+        nid = fpdt.fpdt_get_unique_id()  # one-rank communicator: the world-size > 1 schedule with NCCL self-exchanges
     ctx = fpdt.FPDTContext(world, rank, nid, local)
     if args.residency:
         ctx.set_residency(*args.residency)
@@ -361,7 +363,7 @@ def run_ours(args):
         "model_tflops_per_gpu": tflops_gpu * 12 / 14,
         "config": {"workload": W["name"], "S": S, "heads_q": Hq, "heads_kv": Hkv, "head_dim": d, "chunk": C,
                    "chunks": S // C, "s_local": s_local, "offload": offload, "causal": 1,
-                   "parallelism": f"ulysses-sp{world}", "l2": "inputs 2.7 GB/tensor >> 126 MB L2, no flush",
+                   "parallelism": f"ulysses-sp{world}" + ("-nccl1" if world == 1 and args.exchange_path else ""), "l2": "inputs 2.7 GB/tensor >> 126 MB L2, no flush",
                    "flops_per_step": f_fwd + f_bwd, "flop_convention": "14*d per causal pair per q-head",
                    "sparsity": args.sparsity, "residency": args.residency or [0, 0],
                    "bwd_order": ["kv_outer", "q_outer"][st1["bwd_order"]]},
@@ -390,7 +392,7 @@ def run_ours(args):
         "max_seq_per_gpu": max_seq_record(),
         # the all-to-alls on the comm stream (p > 1): CUDA events around each exchange; bus GB/s = bytes sent to other
         # ranks / exchange time (NVLink 5: 900 GB/s per direction per GPU)
-        "exchange": None if world == 1 else {
+        "exchange": None if (world == 1 and not args.exchange_path) else {
             "ms_per_step": xch["total_ms"] / args.steps, "count_per_step": xch["n"] // args.steps,
             "bytes_per_step": xch["bytes"] // args.steps,
             "bus_GBps": (xch["bytes"] / (xch["total_ms"] / 1e3) / 1e9) if xch["total_ms"] > 0 else None,
@@ -423,6 +425,9 @@ def main():
                          "the device")
     ap.add_argument("--bwd-order", default="kv", choices=["kv", "q", "auto"],
                     help="backward loop order (fpdt_set_bwd_order): kv = the paper's (KV outer), q = GQA-aware Q outer")
+    ap.add_argument("--exchange-path", action="store_true",
+                    help="N = 1: run the sequence-parallel schedule through a one-rank NCCL communicator (pack, "
+                         "ncclAlltoAll, unpack per chunk) instead of the in-place world-size-1 path")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="A/B check: time the step without the library's per-launch CUDA events (no roofline)")
