@@ -59,6 +59,14 @@ constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 128
 #define FPDT_BWD_REGS_DQ 104
 #define FPDT_BWD_REGS_CTL 72
 #endif
+// dQ staging groups: 32 rows (each dQ warp stages its rows and issues their reduce-add: a warp waits only for its own
+// previous reduce-add to have read its staging) or 64 (two halves, a named barrier each).  In the bench step (same box,
+// A/B/A/B): 32 -> bwd 838 at 1560 MHz, 64 -> 829 at 1590 MHz; 16 (half warps) -> 818-819 vs 830-831 for 32.
+#ifndef FPDT_BWD_DQ_ROWS
+#define FPDT_BWD_DQ_ROWS 32
+#endif
+constexpr int kDQRows = FPDT_BWD_DQ_ROWS;
+static_assert(kDQRows == 32 || kDQRows == 64, "dQ staging group");
 constexpr int kRegsSoftmax = FPDT_BWD_REGS_SOFTMAX, kRegsDQ = FPDT_BWD_REGS_DQ, kRegsCtl = FPDT_BWD_REGS_CTL;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
 // The dQ product runs in fp16 (dS and a copy of K rounded to fp16, fp32 accumulation): its sum cancels
@@ -531,16 +539,21 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       tmem_wait_ld();
       tc_fence_before();
       mbar_arrive(bar(B_DQE));
-      // Two independent 64-row halves (warps 8-9: query rows 0-63, warps 10-11: rows 64-127), each with its own half
-      // of the staging, named barrier and issuing thread: while one half waits for its previous reduce-add to finish
-      // reading its staging, the TMA engine works on the other half's.  Staging per half: D/32 column chunks
-      // [64 rows][32 fp32] (128B-swizzled) + a [64][16] chunk (64B-swizzled) when D % 32 == 16 — the 16-byte piece j
-      // of row rr lives at piece j ^ (rr & 7) (resp. j ^ ((rr >> 1) & 3)), so the 32 rows of a warp hit all 32 banks.
-      const int hrow = r >> 6, rr = r & 63;
+      // Independent row groups of kDQRows rows (one per dQ warp at 32), each with its own part of the staging, barrier
+      // and issuing thread: while one group waits for its previous reduce-add to finish reading its staging, the TMA
+      // engine works on the others'.  Staging per group: D/32 column chunks [GR rows][32 fp32] (128B-swizzled) + a
+      // [GR][16] chunk (64B-swizzled) when D % 32 == 16 — the 16-byte piece j of row rr lives at piece j ^ (rr & 7)
+      // (resp. j ^ ((rr >> 1) & 3)), so the 32 rows of a warp hit all 32 banks.
+      constexpr int GR = kDQRows;  // rows per staging group (one issuing thread, one named barrier or warp)
+      const int hrow = r / GR, rr = r % GR;
       const bool hlead = rr == 0;
-      constexpr uint32_t HB = 64 * D * 4;
+      constexpr uint32_t HB = GR * D * 4;
+      auto gsync = [&] {
+        if constexpr (GR == 32) __syncwarp();
+        else named_bar(2 + hrow, GR);
+      };
       if (hlead) bulk_wait_read0();
-      named_bar(2 + hrow, 64);
+      gsync();
       const float2 sc = make_float2(a.scale, a.scale);
       uint8_t* stg = smem + C::oDQ + hrow * HB;
 #pragma unroll
@@ -548,23 +561,23 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
         const float2 x0 = __fmul2_rn(make_float2(v[c], v[c + 1]), sc);
         const float2 x1 = __fmul2_rn(make_float2(v[c + 2], v[c + 3]), sc);
         const int j = (c & 31) >> 2;
-        const uint32_t off = c < (D / 32) * 32 ? (c >> 5) * 8192 + rr * 128 + ((j ^ (rr & 7)) << 4)
-                                               : (D / 32) * 8192 + rr * 64 + ((j ^ ((rr >> 1) & 3)) << 4);
+        const uint32_t off = c < (D / 32) * 32 ? (c >> 5) * (GR * 128) + rr * 128 + ((j ^ (rr & 7)) << 4)
+                                               : (D / 32) * (GR * 128) + rr * 64 + ((j ^ ((rr >> 1) & 3)) << 4);
         *reinterpret_cast<float4*>(stg + off) = make_float4(x0.x, x0.y, x1.x, x1.y);
       }
       fence_async_shared();
-      named_bar(2 + hrow, 64);
+      gsync();
       if (hlead) {
         const uint32_t sb = sDQ + hrow * HB;
-        const int row0 = qt * 128 + 64 * hrow;
+        const int row0 = qt * 128 + GR * hrow;
 #pragma unroll
-        for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_3d(&tm.dq32h, sb + cc * 8192, cc * 32, row0, h);
-        if (D % 32) tma_reduce_add_3d(&tm.dq16h, sb + (D / 32) * 8192, (D / 32) * 32, row0, h);
+        for (int cc = 0; cc < D / 32; ++cc) tma_reduce_add_3d(&tm.dq32h, sb + cc * (GR * 128), cc * 32, row0, h);
+        if (D % 32) tma_reduce_add_3d(&tm.dq16h, sb + (D / 32) * (GR * 128), (D / 32) * 32, row0, h);
         bulk_commit();
         if (hrow == 0) TRACE(11, n);
       }
     }
-    if ((r & 63) == 0) bulk_wait0();
+    if (r % kDQRows == 0) bulk_wait0();
   }
   tc_fence_before();
   __syncthreads();
@@ -585,9 +598,9 @@ int launch_pipe(const BwdArgs& a, cudaStream_t s) {
   ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
   ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
   ok &= make_tile_tmap<D>(&tm.o, a.dout.base, a.dout.rows, a.dout.heads);
-  ok &= make_tmap_f32_head_major(&tm.dq32h, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 32, 64,
+  ok &= make_tmap_f32_head_major(&tm.dq32h, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 32, kDQRows,
                                  CU_TENSOR_MAP_SWIZZLE_128B);
-  ok &= make_tmap_f32_head_major(&tm.dq16h, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 16, 64,
+  ok &= make_tmap_f32_head_major(&tm.dq16h, a.dq_acc, a.n_q_rows, a.hq, D, a.dq_head_stride, 16, kDQRows,
                                  CU_TENSOR_MAP_SWIZZLE_64B);
   if (!ok) return -1;
   const dim3 grid(a.n_kv_rows / 128, a.hq / a.G);
