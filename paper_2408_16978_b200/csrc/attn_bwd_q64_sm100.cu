@@ -23,7 +23,9 @@
 //     (one buffer per 64-column group: a group's next staging waits until its previous reduce-add has read it).
 // The dQ read-out thread owns one head_dim column (a TMEM lane) and 64 query rows. It stages column groups of
 // [64 rows][64 cols] fp32 (and a 16-column group at d = 80) without swizzle: a warp writes 128 contiguous bytes
-// per row. Each group leaves as one TMA reduce-add box.
+// per row. Each group leaves as one TMA reduce-add box.  (Round 2: 32-column groups, one per warp, each warp its own
+// issuer -- the change that gained 1% in the d = 80 pipe kernel -- lost 1.5-2.5% here: 986 / 973 vs 1010 / 987
+// TFLOP/s, diagonal / full pair.)
 // Warp roles and the issue order are those of attn_bwd_pipe_sm100.cu.
 #include "attn_tile.cuh"
 #include "kernels.h"
