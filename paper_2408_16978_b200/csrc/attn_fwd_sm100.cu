@@ -72,6 +72,13 @@ constexpr float kRescaleThreshold = 8.0f;
 #ifndef FPDT_FWD_POLY_MMA_SMSP
 #define FPDT_FWD_POLY_MMA_SMSP 3
 #endif
+// P aliased onto S (d = 128): PV issued in FPDT_FWD_SPLIT_PV key chunks (1, 2 or 4), each as soon as its P is in TMEM,
+// so that the first half of PV_t(j) runs during the exponentials of keys 64-127 (S_t(j+1) has to wait for all of PV_t(j)
+// there).  Measured (C = 64K, 32 x 128, diagonal / full pair, same box): 1 -> 1131 / 1151-1158, 2 -> 1160-1172 /
+// 1181-1186, 4 -> 1149 / 1155 TFLOP/s.
+#ifndef FPDT_FWD_SPLIT_PV
+#define FPDT_FWD_SPLIT_PV 2
+#endif
 #ifndef FPDT_FWD_POLY_EVERY_D128
 #define FPDT_FWD_POLY_EVERY_D128 8
 #endif
@@ -86,6 +93,9 @@ struct FwdCfg {
   static constexpr bool kSepP = 2 * 128 + 64 + 2 * NO <= 512;
   static constexpr uint32_t tP = 256, tO0 = kSepP ? 320 : 256, tOstride = kSepP ? NO : 128;
   static constexpr int kStages = (D == 128) ? 2 : FPDT_FWD_STAGES;
+  // P aliased onto S (d = 128): PV issued in FPDT_FWD_SPLIT_PV key chunks (1, 2 or 4; see the macro)
+  static constexpr int kPVChunks = kSepP ? 1 : FPDT_FWD_SPLIT_PV;
+  static_assert(kPVChunks == 1 || kPVChunks == 2 || kPVChunks == 4, "PV chunks");
   static constexpr int kPolyEvery = (D == 128) ? FPDT_FWD_POLY_EVERY_D128 : FPDT_FWD_POLY_EVERY;
   static constexpr int kQBytes = 2 * T::kBytes;
   static constexpr int kOnes = kSumMMA ? 128 * 16 * 2 : 0;      // the ones atom right after each V tile
@@ -123,11 +133,12 @@ __device__ __forceinline__ float max3(float a, float b, float c) {
 // the sum of the fp32 values when kSum (else 0).  kEvery > 0: every kEvery-th pair on the FMA pipe.
 template <int kEvery, bool kSum, bool kStore = true>
 __device__ __forceinline__ float exp_pack_store(const float* x, float sl2, float mb, uint32_t tS,
-                                                uint32_t* pko = nullptr) {
+                                                uint32_t* pko = nullptr, int c0 = 0, int c1 = 128) {
   float2 acc0 = make_float2(0.f, 0.f), acc1 = make_float2(0.f, 0.f);
   const float2 s2 = make_float2(sl2, sl2), nm = make_float2(-mb, -mb);
 #pragma unroll
   for (int c = 0; c < 128; c += 32) {
+    if (c < c0 || c >= c1) continue;  // c0, c1 are compile-time after unrolling
     uint32_t pkl[16];
     uint32_t* pk = kStore ? pkl : pko + c / 2;
 #pragma unroll
@@ -158,10 +169,11 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
   using T = Tile<D>;
   using C = FwdCfg<D>;
   constexpr int ST = C::kStages;
+  constexpr int kPVChunks = C::kPVChunks;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   __shared__ uint64_t bar_q, bar_k[ST], bar_v[ST], bar_kv_empty[ST], bar_s[2], bar_p[2], bar_o[2], bar_sfree[2],
-      bar_pvdone[2];
+      bar_pvdone[2], bar_pa[2][3];
   __shared__ uint32_t tmem_slot;
 
   const uint32_t warp = warp_id(), lane = lane_id();
@@ -211,6 +223,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
       mbar_init(smem_u32(&bar_o[t]), 1);
       mbar_init(smem_u32(&bar_sfree[t]), 128);
       mbar_init(smem_u32(&bar_pvdone[t]), 1);
+      for (int k = 0; k < 3; ++k) mbar_init(smem_u32(&bar_pa[t][k]), 128);
     }
     fence_mbar_init();
   }
@@ -259,11 +272,32 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         for (int kk = 0; kk < T::kKSteps; ++kk)
           mma_ss(tS[t], T::desc_kmajor(sq, kk), T::desc_kmajor(sk, kk), idS, kk > 0);
       };
-      auto issue_PV = [&](int t, int s, int j) {
+      auto issue_PV = [&](int t, int s, int j, int k0 = 0, int k1 = 8) {
         const uint32_t sv = sKV + s * C::kStageBytes + T::kBytes;
 #pragma unroll
-        for (int kk = 0; kk < 8; ++kk)
+        for (int kk = k0; kk < k1; ++kk)
           mma_ts(tO[t], tPa[t] + kk * 8, T::desc_mn(sv, kk), idPV, (j > 0 || kk > 0) ? 1u : 0u);
+      };
+      // kPVChunks > 1: PV_t(j) in key chunks, each as soon as its P is in TMEM
+      auto issue_PV_split = [&](int t, int s, int j) {
+        if constexpr (kPVChunks > 1) {
+          constexpr int KS = 8 / kPVChunks;  // 16-key MMA steps per chunk
+#pragma unroll
+          for (int k = 0; k < kPVChunks - 1; ++k) {
+            mbar_wait(smem_u32(&bar_pa[t][k]), j & 1);
+            tc_fence_after();
+            issue_PV(t, s, j, k * KS, (k + 1) * KS);
+          }
+          mbar_wait(smem_u32(&bar_p[t]), j & 1);
+          TRACE(4 + t, j);
+          tc_fence_after();
+          issue_PV(t, s, j, 8 - KS, 8);
+        } else {
+          mbar_wait(smem_u32(&bar_p[t]), j & 1);
+          TRACE(4 + t, j);
+          tc_fence_after();
+          issue_PV(t, s, j);
+        }
       };
       mbar_wait(smem_u32(&bar_q), 0);
       tc_fence_after();
@@ -323,10 +357,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
           mma_commit(smem_u32(&bar_s[1]));
         }
         mbar_wait(smem_u32(&bar_v[s]), ph);
-        mbar_wait(smem_u32(&bar_p[0]), j & 1);
-        TRACE(4, j);
-        tc_fence_after();
-        issue_PV(0, s, j);
+        issue_PV_split(0, s, j);
         const bool more = j + 1 < n_tiles;
         const int s2 = (j + 1) % ST;
         if (more) {
@@ -338,10 +369,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         } else {
           mma_commit(smem_u32(&bar_o[0]));
         }
-        mbar_wait(smem_u32(&bar_p[1]), j & 1);
-        TRACE(5, j);
-        tc_fence_after();
-        issue_PV(1, s, j);
+        issue_PV_split(1, s, j);
         mma_commit(smem_u32(&bar_kv_empty[s]));
         if (more) {
           issue_S(1, s2);
@@ -447,8 +475,26 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
 #pragma unroll
         for (int c = 0; c < 64; c += 16) tmem_st16(tPw + c, pk + c);
       } else {
-        sum = any_masked ? exp_pack_store<0, kSumHere>(x, sl2, mb, tPw)
-                         : exp_pack_store<C::kPolyEvery, kSumHere>(x, sl2, mb, tPw);
+        if constexpr (kPVChunks > 1) {
+          // P in key chunks: each lets the MMA warp run PV_t(j) over that part of the contraction while the
+          // exponentials of the next chunk run
+          constexpr int W = 128 / kPVChunks;
+          sum = 0.f;
+#pragma unroll
+          for (int k = 0; k < kPVChunks - 1; ++k) {
+            sum += any_masked ? exp_pack_store<0, kSumHere, true>(x, sl2, mb, tPw, nullptr, k * W, (k + 1) * W)
+                              : exp_pack_store<C::kPolyEvery, kSumHere, true>(x, sl2, mb, tPw, nullptr, k * W,
+                                                                              (k + 1) * W);
+            tmem_wait_st();
+            tc_fence_before();
+            mbar_arrive(smem_u32(&bar_pa[t][k]));
+          }
+          sum += any_masked ? exp_pack_store<0, kSumHere, true>(x, sl2, mb, tPw, nullptr, 128 - W, 128)
+                            : exp_pack_store<C::kPolyEvery, kSumHere, true>(x, sl2, mb, tPw, nullptr, 128 - W, 128);
+        } else {
+          sum = any_masked ? exp_pack_store<0, kSumHere>(x, sl2, mb, tPw)
+                           : exp_pack_store<C::kPolyEvery, kSumHere>(x, sl2, mb, tPw);
+        }
       }
       if constexpr (kSumHere) l_run += sum;
       if (lane == 0 && j < 1024) TRACE(10 + 4 * t, 1024 * (warp & 3) + j);
