@@ -67,6 +67,14 @@ constexpr int kLaunchRegs = (65536 / kThreads) & ~7;  // 128
 #endif
 constexpr int kDQRows = FPDT_BWD_DQ_ROWS;
 static_assert(kDQRows == 32 || kDQRows == 64, "dQ staging group");
+// multicast cluster: kCS CTAs on adjacent key tiles, each loading kCR = 128 / kCS rows of every Q / dO tile (4: bwd
+// 811 vs 849 TFLOP/s in the step, A/B/A/B -- four CTAs in lockstep wait on each other more than the loads cost)
+#ifndef FPDT_BWD_CLUSTER
+#define FPDT_BWD_CLUSTER 2
+#endif
+constexpr int kCS = FPDT_BWD_CLUSTER, kCR = 128 / kCS;
+constexpr uint16_t kCMask = (uint16_t)((1u << kCS) - 1);
+static_assert(kCS == 2 || kCS == 4, "multicast cluster size");
 constexpr int kRegsSoftmax = FPDT_BWD_REGS_SOFTMAX, kRegsDQ = FPDT_BWD_REGS_DQ, kRegsCtl = FPDT_BWD_REGS_CTL;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
 // The dQ product runs in fp16 (dS and a copy of K rounded to fp16, fp32 accumulation): its sum cancels
@@ -184,7 +192,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
   if (a.causal) {
     // first query tile that can see this key tile (MC: the pair's first key tile; the second CTA's first tile of a
     // diagonal pair is then fully masked, P = 0)
-    const int64_t rel = a.kv_pos0 + (int64_t)(MC ? (kt & ~1) : kt) * 128 - a.q_pos0;
+    const int64_t rel = a.kv_pos0 + (int64_t)(MC ? (kt & ~(kCS - 1)) : kt) * 128 - a.q_pos0;
     if (rel > 0) qt_first = (int)(rel / 128);
     if (qt_first > n_qt_total) qt_first = n_qt_total;
   }
@@ -200,11 +208,11 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
     mbar_init(bar(B_KV), 1);
     for (int s = 0; s < QS; ++s) {
       mbar_init(bar(B_QF + s), 1);
-      mbar_init(bar(B_QE + s), MC ? 2 : 1);
+      mbar_init(bar(B_QE + s), MC ? kCS : 1);
     }
     for (int s = 0; s < OS; ++s) {
       mbar_init(bar(B_OF + s), 1);
-      mbar_init(bar(B_OE + s), MC ? 2 : 1);
+      mbar_init(bar(B_OE + s), MC ? kCS : 1);
     }
     mbar_init(bar(B_S), 1);
     mbar_init(bar(B_SFREE), 256);
@@ -246,8 +254,8 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
           if constexpr (MC) {
 #pragma unroll
             for (int at = 0; at < T::kAtoms; ++at)
-              tma_load_3d_mc(base + C::oQ + qs * C::TB + at * T::kAtomBytes + crank * 64 * T::kRowBytes, &tm.q64, fq,
-                             at * T::kAtomCols, a.q.head0 + h, qrow + 64 * (int)crank, 3, pol_q);
+              tma_load_3d_mc(base + C::oQ + qs * C::TB + at * T::kAtomBytes + crank * kCR * T::kRowBytes, &tm.q64,
+                             fq, at * T::kAtomCols, a.q.head0 + h, qrow + kCR * (int)crank, kCMask, pol_q);
           } else {
             T::load(base + C::oQ + qs * C::TB, &tm.q, fq, a.q.head0 + h, qrow, pol_q);
           }
@@ -258,8 +266,9 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
           if constexpr (MC) {
 #pragma unroll
             for (int at = 0; at < T::kAtoms; ++at)
-              tma_load_3d_mc(base + C::oO + os * C::TB + at * T::kAtomBytes + crank * 64 * T::kRowBytes, &tm.o64,
-                             bar(B_OF + os), at * T::kAtomCols, a.dout.head0 + h, qrow + 64 * (int)crank, 3, pol_q);
+              tma_load_3d_mc(base + C::oO + os * C::TB + at * T::kAtomBytes + crank * kCR * T::kRowBytes, &tm.o64,
+                             bar(B_OF + os), at * T::kAtomCols, a.dout.head0 + h, qrow + kCR * (int)crank, kCMask,
+                             pol_q);
           } else {
             T::load(base + C::oO + os * C::TB, &tm.o, bar(B_OF + os), a.dout.head0 + h, qrow, pol_q);
           }
@@ -316,7 +325,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             mma_ts(tdV, tdP + 64 * (kk >> 2) + (kk & 3) * 8, T::desc_mn(sO(n), kk), idG, (n > 0 || kk > 0));
-          if constexpr (MC) mma_commit_mc(bar(B_OE + n % OS), 3);  // dO_n consumed (dP_n precedes dV_n), both CTAs
+          if constexpr (MC) mma_commit_mc(bar(B_OE + n % OS), kCMask);  // dO_n consumed (dP_n precedes dV_n), both CTAs
           else mma_commit(bar(B_OE + n % OS));
           // dK += dS^T Q_n   (A = dS^T in TMEM); first, so that Q_n is released early
           mbar_wait(bar(B_DS), n & 1);
@@ -325,7 +334,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
 #pragma unroll
           for (int kk = 0; kk < 8; ++kk)
             mma_ts(tdK, tdP + 64 * (kk >> 2) + 32 + (kk & 3) * 8, T::desc_mn(sQ(n), kk), idG, (n > 0 || kk > 0));
-          if constexpr (MC) mma_commit_mc(bar(B_QE + n % QS), 3);  // Q_n consumed
+          if constexpr (MC) mma_commit_mc(bar(B_QE + n % QS), kCMask);  // Q_n consumed
           else mma_commit(bar(B_QE + n % QS));
           if (more) issue_dP(n + 1);
           // dQ_n = dS K   (A = the dS smem tile, MN-major)
@@ -593,8 +602,8 @@ int launch_pipe(const BwdArgs& a, cudaStream_t s) {
   constexpr uint32_t kAtomCols = Tile<D>::kAtomCols;
   constexpr CUtensorMapSwizzle kSw = D == 80 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B;
   bool ok = make_tile_tmap<D>(&tm.q, a.q.base, a.q.rows, a.q.heads);
-  ok &= make_tmap_rows_heads_dim(&tm.q64, a.q.base, a.q.rows, a.q.heads, D, kAtomCols, 64, kSw);
-  ok &= make_tmap_rows_heads_dim(&tm.o64, a.dout.base, a.dout.rows, a.dout.heads, D, kAtomCols, 64, kSw);
+  ok &= make_tmap_rows_heads_dim(&tm.q64, a.q.base, a.q.rows, a.q.heads, D, kAtomCols, kCR, kSw);
+  ok &= make_tmap_rows_heads_dim(&tm.o64, a.dout.base, a.dout.rows, a.dout.heads, D, kAtomCols, kCR, kSw);
   ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
   ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
   ok &= make_tile_tmap<D>(&tm.o, a.dout.base, a.dout.rows, a.dout.heads);
@@ -607,7 +616,7 @@ int launch_pipe(const BwdArgs& a, cudaStream_t s) {
 #ifndef FPDT_BWD_MC
 #define FPDT_BWD_MC 1
 #endif
-  if (FPDT_BWD_MC && grid.x % 2 == 0) {
+  if (FPDT_BWD_MC && grid.x % kCS == 0) {
     if (int e = set_max_dynamic_smem((const void*)attn_bwd_pipe_kernel<D, true>, C::kSmem)) return e;
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = grid;
@@ -616,7 +625,7 @@ int launch_pipe(const BwdArgs& a, cudaStream_t s) {
     cfg.stream = s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
-    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.x = kCS;
     attr[0].val.clusterDim.y = 1;
     attr[0].val.clusterDim.z = 1;
     cfg.attrs = attr;
