@@ -68,7 +68,10 @@ constexpr float kRescaleThreshold = 8.0f;
 // vs 891 TFLOP/s; 4 -> 891; 2 -> 901 standalone (warp 1 then FMA-bound).  (Also measured: making the MMA thread wait
 // for each MMA group to complete before issuing the next evens the warps too, but serialises the pipe: 870-917.  A third
 // code path -- warps 0 and 4, beside the TMA producer, with their own split -- dropped the forward to 785-803 in the
-// step: the unrolled exponential loops are large, and each SMSP's path has to stay in the instruction caches.)
+// step: the unrolled exponential loops are large, and each SMSP's path has to stay in the instruction caches.  Also
+// measured and not kept: exponentials with the running max first and the row max formed alongside them (a second
+// pass only when a rescale is due; the same results): 748 vs 893 in the step -- the restructured loop costs more than
+// the ~290 clk row-max phase it takes off the critical path.)
 #ifndef FPDT_FWD_POLY_MMA_SMSP
 #define FPDT_FWD_POLY_MMA_SMSP 3
 #endif
