@@ -75,6 +75,9 @@ static_assert(kDQRows == 32 || kDQRows == 64, "dQ staging group");
 constexpr int kCS = FPDT_BWD_CLUSTER, kCR = 128 / kCS;
 constexpr uint16_t kCMask = (uint16_t)((1u << kCS) - 1);
 static_assert(kCS == 2 || kCS == 4, "multicast cluster size");
+#ifndef FPDT_BWD_FOLD_D
+#define FPDT_BWD_FOLD_D 1
+#endif
 constexpr int kRegsSoftmax = FPDT_BWD_REGS_SOFTMAX, kRegsDQ = FPDT_BWD_REGS_DQ, kRegsCtl = FPDT_BWD_REGS_CTL;
 static_assert(2 * 128 * (kRegsSoftmax - kLaunchRegs) <= 128 * (2 * kLaunchRegs - kRegsDQ - kRegsCtl), "register pool");
 // The dQ product runs in fp16 (dS and a copy of K rounded to fp16, fp32 accumulation): its sum cancels
@@ -99,7 +102,14 @@ struct PipeCfg {
   static constexpr int oDS = oKH + ((TB + 1023) / 1024) * 1024;
   static constexpr int oDQ = oDS + kDS;
   static constexpr int oStats = oDQ + kDQ;
-  static constexpr int oBars = oStats + QS * kStats;
+  // kFoldD: D enters dP^T = V dO^T - D as one more 16-column k-step -- a constant atom of V' (columns -1, -1, 0, ...)
+  // and, per dO stage, an atom of dO' (bf16 hi / lo of D in columns 0 / 1) -- instead of the softmax warps' broadcast
+  // shared-memory reads of D and their subtraction
+  static constexpr bool kFoldD = FPDT_BWD_FOLD_D != 0 && D == 80;  // the extra atoms use the d = 80 (SW32) format
+  static constexpr int kXAtom = 128 * 16 * 2;  // one 16-column SW32 atom of 128 rows
+  static constexpr int oVX = ((oStats + QS * kStats + 1023) / 1024) * 1024;
+  static constexpr int oOX = oVX + (kFoldD ? kXAtom : 0);
+  static constexpr int oBars = oOX + (kFoldD ? OS * kXAtom : 0);
   static constexpr int kSmem = oBars + 256;
   static_assert(kSmem <= 227 * 1024, "shared memory budget");
   static constexpr uint32_t tS = 0, tdP = 128, tdQ = 256, tdK = 256 + D, tdV = 256 + 2 * D;
@@ -211,7 +221,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
       mbar_init(bar(B_QE + s), MC ? kCS : 1);
     }
     for (int s = 0; s < OS; ++s) {
-      mbar_init(bar(B_OF + s), 1);
+      mbar_init(bar(B_OF + s), C::kFoldD ? 1 + 64 : 1);  // + the 64 threads writing the stage's dO' atom
       mbar_init(bar(B_OE + s), MC ? kCS : 1);
     }
     mbar_init(bar(B_S), 1);
@@ -250,7 +260,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
           TRACE(12, n);
           const uint32_t fq = bar(B_QF + qs);
           const uint32_t stats = base + C::oStats + qs * C::kStats;
-          mbar_expect_tx(fq, C::TB + 1024);
+          mbar_expect_tx(fq, C::TB + (C::kFoldD ? 512 : 1024));
           if constexpr (MC) {
 #pragma unroll
             for (int at = 0; at < T::kAtoms; ++at)
@@ -260,7 +270,7 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
             T::load(base + C::oQ + qs * C::TB, &tm.q, fq, a.q.head0 + h, qrow, pol_q);
           }
           bulk_load(stats, a.lse2 + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, fq);
-          bulk_load(stats + 512, a.Dstat + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, fq);
+          if constexpr (!C::kFoldD) bulk_load(stats + 512, a.Dstat + (int64_t)h * a.stat_ld + (int64_t)qt * 128, 512, fq);
           if (n >= OS) mbar_wait(bar(B_OE + os), ((n / OS) - 1) & 1);
           mbar_expect_tx(bar(B_OF + os), C::TB);
           if constexpr (MC) {
@@ -300,6 +310,9 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
 #pragma unroll
           for (int kk = 0; kk < T::kKSteps; ++kk)
             mma_ss(tdP, T::desc_kmajor(sV, kk), T::desc_kmajor(sO(n), kk), idS, kk > 0);
+          if constexpr (C::kFoldD)
+            mma_ss(tdP, T::desc_kmajor(base + C::oVX, 0), T::desc_kmajor(base + C::oOX + (n % OS) * C::kXAtom, 0), idS,
+                   1u);
           mma_commit(bar(B_DP));
         };
         mbar_wait(bar(B_KV), 0);
@@ -352,6 +365,39 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
           TRACE(8, n);
         }
         mma_commit(bar(B_KVDONE));
+      }
+    } else if (C::kFoldD && warp >= 14) {
+      // ---------------------------------------------------------------- the extra dP^T k-step's atoms (kFoldD)
+      // thread t writes rows t and t + 64: the constant V' atom and the zero halves once, then per query tile the
+      // bf16 hi / lo split of D into the dO stage's dO' atom (SW32: 16-byte piece c of row r at c ^ ((r >> 2) & 1))
+      const int t = (int)threadIdx.x - 448;
+#pragma unroll
+      for (int k = 0; k < 2; ++k) {
+        const int r = t + 64 * k;
+        const uint32_t sw = (uint32_t)(r >> 2) & 1u;
+        uint8_t* vx = smem + C::oVX + r * 32;
+        *reinterpret_cast<uint4*>(vx + ((0u ^ sw) << 4)) = make_uint4(0xbf80bf80u, 0u, 0u, 0u);  // -1, -1 (bf16)
+        *reinterpret_cast<uint4*>(vx + ((1u ^ sw) << 4)) = make_uint4(0u, 0u, 0u, 0u);
+#pragma unroll
+        for (int s2 = 0; s2 < OS; ++s2)
+          *reinterpret_cast<uint4*>(smem + C::oOX + s2 * C::kXAtom + r * 32 + ((1u ^ sw) << 4)) =
+              make_uint4(0u, 0u, 0u, 0u);
+      }
+      for (int n = 0; n < n_iter; ++n) {
+        const int os = n % OS;
+        const int qt = qt_first + n / G, h = g * G + n % G;
+        if (n >= OS) mbar_wait(bar(B_OE + os), ((n / OS) - 1) & 1);
+#pragma unroll
+        for (int k = 0; k < 2; ++k) {
+          const int r = t + 64 * k;
+          const float dv = a.Dstat[(int64_t)h * a.stat_ld + (int64_t)qt * 128 + r];
+          const __nv_bfloat16 hi = __float2bfloat16_rn(dv);
+          const float lo = dv - __bfloat162float(hi);
+          *reinterpret_cast<uint4*>(smem + C::oOX + os * C::kXAtom + r * 32 + ((0u ^ ((uint32_t)(r >> 2) & 1u)) << 4)) =
+              make_uint4(pack_bf16x2(__bfloat162float(hi), lo), 0u, 0u, 0u);
+        }
+        fence_async_shared();  // generic-proxy writes -> the tensor core's operand reads
+        mbar_arrive(bar(B_OF + os));
       }
     }
   } else if (warp < 8) {
@@ -437,11 +483,17 @@ attn_bwd_pipe_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__
         // dS in place of dP (fp32), bf16 to TMEM; the fp16 copy for the smem tile is packed below
 #pragma unroll
         for (int i = 0; i < 64; i += 4) {
-          const float4 dd = lds4(st + 128 + i);
-          const float2 a0 = __fmul2_rn(make_float2(p[i], p[i + 1]),
-                                       __fadd2_rn(make_float2(dp[i], dp[i + 1]), make_float2(-dd.x, -dd.y)));
-          const float2 a1 = __fmul2_rn(make_float2(p[i + 2], p[i + 3]),
-                                       __fadd2_rn(make_float2(dp[i + 2], dp[i + 3]), make_float2(-dd.z, -dd.w)));
+          float2 a0, a1;
+          if constexpr (C::kFoldD) {  // dP^T already holds dP - D
+            a0 = __fmul2_rn(make_float2(p[i], p[i + 1]), make_float2(dp[i], dp[i + 1]));
+            a1 = __fmul2_rn(make_float2(p[i + 2], p[i + 3]), make_float2(dp[i + 2], dp[i + 3]));
+          } else {
+            const float4 dd = lds4(st + 128 + i);
+            a0 = __fmul2_rn(make_float2(p[i], p[i + 1]),
+                            __fadd2_rn(make_float2(dp[i], dp[i + 1]), make_float2(-dd.x, -dd.y)));
+            a1 = __fmul2_rn(make_float2(p[i + 2], p[i + 3]),
+                            __fadd2_rn(make_float2(dp[i + 2], dp[i + 3]), make_float2(-dd.z, -dd.w)));
+          }
           dp[i] = a0.x; dp[i + 1] = a0.y; dp[i + 2] = a1.x; dp[i + 3] = a1.y;
         }
 #pragma unroll
