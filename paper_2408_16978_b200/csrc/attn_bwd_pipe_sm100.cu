@@ -35,8 +35,10 @@
 //   WG0 (0-3)   softmax-gradient, query columns [0,64)   (thread = key row = TMEM lane); final dK    168 regs
 //   WG1 (4-7)   softmax-gradient, query columns [64,128)                                ; final dV    168 regs
 //   WG2 (8-11)  dQ read-out (thread = query row) -> smem staging -> TMA bulk reduce-add              104 regs
-//   WG3 (12)    TMA producer; (13) TMEM allocator + single-thread MMA issuer; (14, 15) idle          72 regs
-// Shared memory (d = 80: 215 KB): K, V | 2 Q stages (+ lse2/D rows) | 2 dO stages | fp16 K | dS (fp16) | dQ staging.
+//   WG3 (12)    TMA producer; (13) TMEM allocator + single-thread MMA issuer; (14, 15) the dO' atoms of the D
+//               fold (d = 80, PipeCfg::kFoldD: dP^T = V dO^T - D as a sixth k-step)                   72 regs
+// Shared memory (d = 80: 226 KB): K, V | 2 Q stages (+ lse2 rows) | 2 dO stages | fp16 K | dS (fp16) | dQ staging |
+// V' atom | 2 dO' atoms.
 // TMEM: S^T [0,128) | dP^T [128,256), then per query half h: P^T [128+64h, +32), dS^T [160+64h, +32) (bf16) |
 //       dQ [256,256+D) | dK | dV  (496 columns at d = 80).
 #include "attn_tile.cuh"
