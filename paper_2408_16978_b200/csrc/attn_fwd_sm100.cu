@@ -71,7 +71,9 @@ constexpr float kRescaleThreshold = 8.0f;
 // step: the unrolled exponential loops are large, and each SMSP's path has to stay in the instruction caches.  Also
 // measured and not kept: exponentials with the running max first and the row max formed alongside them (a second
 // pass only when a rescale is due; the same results): 748 vs 893 in the step -- the restructured loop costs more than
-// the ~290 clk row-max phase it takes off the critical path.)
+// the ~290 clk row-max phase it takes off the critical path.  The producer as lane 1 of the MMA warp (SMSP 0 free of
+// control threads): 651 vs 766 -- and the control roles selected by `lane == 0` instead of elect.sync alone already
+// cost 905 -> 766 TFLOP/s in the step.)
 #ifndef FPDT_FWD_POLY_MMA_SMSP
 #define FPDT_FWD_POLY_MMA_SMSP 3
 #endif
