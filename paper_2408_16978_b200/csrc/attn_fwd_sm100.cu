@@ -53,8 +53,10 @@ constexpr float kRescaleThreshold = 8.0f;
 //   d = 80:  0, 1, 2, 3 -> 800, 669, 811, 865; 4 -> 940-948 / 966-985; 5 -> 954-955 / 957-987; 6 -> 915-935; 8 -> 902-941
 //   d = 128: 0 -> 1147-1149; 4 -> 1142-1145; 5 -> 1147-1148; 6 -> 1151-1159; 8 -> 1147-1162; 12, 16 -> 1139-1152
 // Inside the bench step on one box (tools/gpu_ab_fwdpoly.sh), d = 80: 4 -> 895, 5 -> 910, 6 -> 876 TFLOP/s.
+// With the MMA-SMSP split below (round 2, bench step, same box, A/B/A/B): 4 -> fwd 909, 5 -> 901 TFLOP/s (and 4 with no
+// MMA-SMSP split 894-896).
 #ifndef FPDT_FWD_POLY_EVERY
-#define FPDT_FWD_POLY_EVERY 5
+#define FPDT_FWD_POLY_EVERY 4
 #endif
 #ifndef FPDT_FWD_STAGES
 #define FPDT_FWD_STAGES 3  // K/V ring depth at d <= 80 (d = 128: 2, the shared-memory limit); in the bench step on one
