@@ -86,8 +86,10 @@ constexpr float kRescaleThreshold = 8.0f;
 #ifndef FPDT_FWD_SPLIT_PV
 #define FPDT_FWD_SPLIT_PV 2
 #endif
+// d = 128 with the split PV (round 2, C = 64K, 32 x 128, diagonal / full pair, same box): 3 -> 1174 / 1197,
+// 4 -> 1172 / 1193-1195, 5 -> 1182-1188 / 1193-1194, 6 -> 1169 / 1181, 8 -> 1165-1170 / 1179-1180, 12 -> 1175 / 1179
 #ifndef FPDT_FWD_POLY_EVERY_D128
-#define FPDT_FWD_POLY_EVERY_D128 8
+#define FPDT_FWD_POLY_EVERY_D128 5
 #endif
 
 template <int D>
