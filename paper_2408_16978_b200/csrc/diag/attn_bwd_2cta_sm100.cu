@@ -157,7 +157,7 @@ __device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst_cluster, uint32_t
                "r"(src), "r"(bytes), "r"(bar_cluster)
                : "memory");
 }
-__device__ __forceinline__ void st_async_u4(uint32_t cluster_addr, const uint32_t (&w)[4], uint32_t cluster_bar) {
+[[maybe_unused]] __device__ __forceinline__ void st_async_u4(uint32_t cluster_addr, const uint32_t (&w)[4], uint32_t cluster_bar) {
   asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v4.b32 [%0], {%1, %2, %3, %4}, [%5];" ::"r"(
                    cluster_addr),
                "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(cluster_bar)
