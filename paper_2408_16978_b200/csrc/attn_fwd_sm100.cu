@@ -114,6 +114,7 @@ struct FwdCfg {
 
 struct TmapSet {
   CUtensorMap q, k, v;
+  CUtensorMap k64, v64;  // 64-row boxes: each CTA of a cluster pair multicasts one half of a K / V tile (MC)
 };
 
 __device__ __forceinline__ float ex2(float x) {
@@ -172,7 +173,13 @@ __device__ __forceinline__ float exp_pack_store(const float* x, float sl2, float
   return kSum ? (acc0.x + acc0.y) + (acc1.x + acc1.y) : 0.f;
 }
 
-template <int D>
+// MC: clusters of two CTAs on adjacent query-tile pairs of one head, which walk the same key / value tiles (for the
+// causal diagonal the pair's longer range; the shorter CTA's extra tiles are fully masked); each CTA loads one 64-row
+// half of every K and V tile and multicasts it into both, and a stage is refilled once both have consumed it.
+#ifndef FPDT_FWD_MC
+#define FPDT_FWD_MC 1
+#endif
+template <int D, bool MC>
 __global__ void __launch_bounds__(kThreads, 1)
 attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdArgs a) {
   using T = Tile<D>;
@@ -194,8 +201,11 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
   const int pair = gridDim.x - 1 - blockIdx.x;
   const int64_t q_pos_first = a.q_pos0 + (int64_t)pair * 256;
   int n_tiles = a.n_kv_rows / 128;
+  const uint32_t crank = MC ? cluster_ctarank() : 0;
   if (a.causal) {
-    const int64_t reach = q_pos_first + 256 - a.kv_pos0;  // keys visible to the last row of the CTA
+    // keys visible to the last row of the CTA (MC: of the cluster's later query-tile pair, rank 0)
+    const int64_t last_first = MC ? a.q_pos0 + (int64_t)(gridDim.x - 1 - (blockIdx.x & ~1u)) * 256 : q_pos_first;
+    const int64_t reach = last_first + 256 - a.kv_pos0;
     const int64_t need = (reach + 127) / 128;
     n_tiles = (int)(need < n_tiles ? need : n_tiles);
   }
@@ -224,7 +234,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
     for (int s = 0; s < ST; ++s) {
       mbar_init(smem_u32(&bar_k[s]), 1);
       mbar_init(smem_u32(&bar_v[s]), 1);
-      mbar_init(smem_u32(&bar_kv_empty[s]), 1);
+      mbar_init(smem_u32(&bar_kv_empty[s]), MC ? 2 : 1);
     }
     for (int t = 0; t < 2; ++t) {
       mbar_init(smem_u32(&bar_s[t]), 1);
@@ -239,6 +249,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
+  if constexpr (MC) cluster_sync();  // the partner's barriers exist before any multicast load or commit reaches them
   const uint32_t tmem = tmem_slot;
 
   if (warp >= 8) {
@@ -262,9 +273,20 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
         const uint32_t sk = sKV + s * C::kStageBytes, sv = sk + T::kBytes;
         const int krow = (int)(a.kv_row0 + (int64_t)j * 128);
         mbar_expect_tx(smem_u32(&bar_k[s]), T::kBytes);
-        T::load(sk, &tm.k, smem_u32(&bar_k[s]), a.k.head0 + g, krow, pol_kv);
         mbar_expect_tx(smem_u32(&bar_v[s]), T::kBytes);
-        T::load(sv, &tm.v, smem_u32(&bar_v[s]), a.v.head0 + g, krow, pol_kv);
+        if constexpr (MC) {
+#pragma unroll
+          for (int at = 0; at < T::kAtoms; ++at) {
+            const uint32_t off = at * T::kAtomBytes + crank * 64 * T::kRowBytes;
+            tma_load_3d_mc(sk + off, &tm.k64, smem_u32(&bar_k[s]), at * T::kAtomCols, a.k.head0 + g,
+                           krow + 64 * (int)crank, 3, pol_kv);
+            tma_load_3d_mc(sv + off, &tm.v64, smem_u32(&bar_v[s]), at * T::kAtomCols, a.v.head0 + g,
+                           krow + 64 * (int)crank, 3, pol_kv);
+          }
+        } else {
+          T::load(sk, &tm.k, smem_u32(&bar_k[s]), a.k.head0 + g, krow, pol_kv);
+          T::load(sv, &tm.v, smem_u32(&bar_v[s]), a.v.head0 + g, krow, pol_kv);
+        }
       }
     }
    } else if (warp == 9) {
@@ -348,7 +370,10 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
             tc_fence_after();
             issue_PV(t, s, j);
             mma_commit(smem_u32(&bar_pvdone[t]));
-            if (t == 1) mma_commit(smem_u32(&bar_kv_empty[s]));
+            if (t == 1) {
+              if constexpr (MC) mma_commit_mc(smem_u32(&bar_kv_empty[s]), 3);  // stage s consumed, in both CTAs
+              else mma_commit(smem_u32(&bar_kv_empty[s]));
+            }
             if (!more) mma_commit(smem_u32(&bar_o[t]));
             if (j < 1024) TRACE(4 + t, 1024 + j);  // PV_t(j) issued and committed
           }
@@ -379,7 +404,8 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
           mma_commit(smem_u32(&bar_o[0]));
         }
         issue_PV_split(1, s, j);
-        mma_commit(smem_u32(&bar_kv_empty[s]));
+        if constexpr (MC) mma_commit_mc(smem_u32(&bar_kv_empty[s]), 3);
+        else mma_commit(smem_u32(&bar_kv_empty[s]));
         if (more) {
           issue_S(1, s2);
           mma_commit(smem_u32(&bar_s[1]));
@@ -579,6 +605,7 @@ attn_fwd_kernel(const __grid_constant__ TmapSet tm, const __grid_constant__ FwdA
   }
   tc_fence_before();
   __syncthreads();
+  if constexpr (MC) cluster_sync();  // no CTA leaves while its partner may still multicast into it or arrive on it
   if (warp == 9) tmem_dealloc<512>(tmem);
 }
 
@@ -589,10 +616,32 @@ int launch_fwd(const FwdArgs& a, cudaStream_t s) {
   bool ok = make_tile_tmap<D>(&tm.q, a.q.base, a.q.rows, a.q.heads);
   ok &= make_tile_tmap<D>(&tm.k, a.k.base, a.k.rows, a.k.heads);
   ok &= make_tile_tmap<D>(&tm.v, a.v.base, a.v.rows, a.v.heads);
+  constexpr CUtensorMapSwizzle kSw = D == 80 ? CU_TENSOR_MAP_SWIZZLE_32B : CU_TENSOR_MAP_SWIZZLE_128B;
+  ok &= make_tmap_rows_heads_dim(&tm.k64, a.k.base, a.k.rows, a.k.heads, D, Tile<D>::kAtomCols, 64, kSw);
+  ok &= make_tmap_rows_heads_dim(&tm.v64, a.v.base, a.v.rows, a.v.heads, D, Tile<D>::kAtomCols, 64, kSw);
   if (!ok) return -1;
-  if (int e = set_max_dynamic_smem((const void*)attn_fwd_kernel<D>, C::kSmem)) return e;
   dim3 grid(a.n_q_rows / 256, a.hq);
-  attn_fwd_kernel<D><<<grid, kThreads, C::kSmem, s>>>(tm, a);
+  // d = 128 only: there the K/V tiles are 32 KB each (C = 64K, 32 heads: 1228-1240 vs 1213-1228 TFLOP/s, diagonal / full
+  // pair); at d = 80 the pairs lost 1-2% (957 / 964 vs 977 / 972 standalone, 924 vs 930 in the bench step)
+  if (FPDT_FWD_MC && D == 128 && grid.x % 2 == 0) {
+    if (int e = set_max_dynamic_smem((const void*)attn_fwd_kernel<D, true>, C::kSmem)) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(kThreads);
+    cfg.dynamicSmemBytes = C::kSmem;
+    cfg.stream = s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    if (cudaError_t e = cudaLaunchKernelEx(&cfg, attn_fwd_kernel<D, true>, tm, a)) return (int)e;
+    return (int)cudaGetLastError();
+  }
+  if (int e = set_max_dynamic_smem((const void*)attn_fwd_kernel<D, false>, C::kSmem)) return e;
+  attn_fwd_kernel<D, false><<<grid, kThreads, C::kSmem, s>>>(tm, a);
   return (int)cudaGetLastError();
 }
 
