@@ -83,7 +83,8 @@ template <int D>
 struct Cfg {
   using TK = TileR<D, 128>;
   using TQ = TileR<D, BQ>;
-  static constexpr int QS = 3, OS = 2;
+  static constexpr int QS = 3, OS = 2;  // (round 2: 2 Q stages -> 906-911 / 859-860 vs 1041 / 1017 TFLOP/s at d = 128,
+                                         // so no shared memory can be freed here for a D fold as in the pipe kernel)
   static constexpr int kDQW = (D + 31) / 32;       // dQ read-out warps (thread = one head_dim column)
   static constexpr int kDS = 128 * BQ * 2;         // dS, [128 keys][64 queries] bf16, MN-major (queries contiguous)
   static constexpr int kDQB = BQ * D * 4;          // dQ staging: column groups [64 rows][<=64 cols] fp32
